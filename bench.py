@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""FAGP posterior mean+var throughput on B200 -- BASELINE.json's metric and config.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--config c3]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (one rank per GPU, NCCL)
+
+A step is one full posterior -- fit (fused Phi-gen + Gram, [NCCL all-reduce], Cholesky
+with the jitter contract, solves, TRTRI) and predict (fused Phi*-gen + mean + variance) --
+over the config's synthetic inputs (reference generator, bench.py:177-196 of the
+reference).  Train and test rows are split evenly over the ranks (strong scaling: the
+total problem is fixed).  Prints ONE JSON line on rank 0.
+
+  value       test samples/s (N* / T), inputs resident in HBM, CUDA events per step,
+              max over ranks; L2 flushed (256 MiB write) between steps, outside the events
+  e2e         same metric through the public API fagp_posterior() from pinned host
+              tensors to host numpy results (H2D + D2H inside the timed region)
+  roofline    the dominant kernel's algorithmic FP64 flops per launch / its event-timed
+              duration, against the measured FP64 DMMA peak (profiles/fp64_peak_r01.json)
+  cpu_baseline  the CPU oracle port (oracle/fagp_oracle.py, the reference's algorithm and
+              evaluation order on numpy/OpenBLAS) on a bounded sample, rank 0, N=1 only
+--impl reference times that CPU path alone as the reference arm.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (p, M, N train, N* test)
+    "c1": (1, 10, 1_000, 1_000),
+    "c2": (2, 10, 100_000, 100_000),
+    "c3": (3, 10, 1_000_000, 1_000_000),
+    "c5": (5, 6, 8_000_000, 2_000_000),
+}
+METRIC = "posterior mean+var samples/s (N=1e6, p=3, M=10); % FP64 tensor peak"
+NOISE_VAR = 0.0025
+FP64_PEAK_FILE = ROOT / "profiles" / "fp64_peak_r01.json"
+NCU_SUMMARY_FILE = ROOT / "profiles" / "ncu_summary_r01.json"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def useful_flops(N, Ns, m):
+    """SURVEY.md §8d algorithmic count: Gram N m(m+1) + t 2Nm + chol m^3/3 + trtri m^3/3
+    + mean 2N*m + var N* m(m+1) + 2N*m."""
+    return N * m * (m + 1) + 2 * N * m + 2 * m**3 / 3 + 2 * Ns * m + Ns * m * (m + 1) + 2 * Ns * m
+
+
+def launches_per_step(m):
+    """Kernels of ours launched by one PosteriorEngine.run() (no jitter retry)."""
+    nblk = -(-m // 32)
+    potrf = nblk + 2 * (nblk - 1)
+    mp = 32
+    while mp < m:
+        mp *= 2
+    levels = 0
+    h = 32
+    while h < mp:
+        levels += 1
+        h *= 2
+    trtri = 1 + 1 + 2 * levels  # pad, diag_inv, 2 GEMMs per level
+    factor = 1 + 1 + potrf + 1 + 1 + 2 + 1 + trtri + 1  # build G/t, build A, potrf, zero, vec, trsv x2, vec, trtri, op
+    return 2 + 2 + factor + 1  # basis_eval x2, gram + reduce, factor, predict
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.sw_power_cap", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown"]
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits", "-lms",
+                 "100", "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, ValueError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def fp64_peak():
+    try:
+        d = json.loads(FP64_PEAK_FILE.read_text())
+        return float(d["fp64_dmma_tflops"]), "measured: register-only DMMA loop, profiles/fp64_peak_r01.json"
+    except (OSError, KeyError, ValueError):
+        return 37.0, "fallback: 148 SM x 1.965 GHz x 128 FP64 flop/clk (datasheet ~37 TF)"
+
+
+def ncu_traffic(kernel):
+    try:
+        d = json.loads(NCU_SUMMARY_FILE.read_text())
+        return d["kernels"][kernel]["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
+def make_inputs(cfg, rank, world):
+    from paper_2403_12797_b200.datagen import generate, test_inputs, train_seed
+    from paper_2403_12797_b200.distributed import shard_range
+
+    p, M, N, Ns = CONFIGS[cfg]
+    ds = generate(N, p, train_seed(p), 0.05)
+    Xs = test_inputs(Ns, p)
+    a, b = shard_range(N, rank, world)
+    c, d = shard_range(Ns, rank, world)
+    return ds.X[a:b], ds.y[a:b], Xs[c:d]
+
+
+def cpu_baseline(cfg, sample_n):
+    """The oracle port (the reference algorithm on numpy/OpenBLAS) on a bounded sample."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import fagp_oracle as O
+    from threadpoolctl import threadpool_info
+
+    from paper_2403_12797_b200.datagen import generate, test_inputs, train_seed
+
+    p, M, N, Ns = CONFIGS[cfg]
+    n = min(sample_n, N)
+    ns = max(1, int(round(n * Ns / N)))
+    ds = generate(n, p, train_seed(p), 0.05)
+    Xs = test_inputs(ns, p)
+    t0 = time.perf_counter()
+    O.posterior(ds.X, ds.y, Xs, [1.0] * p, [1.0] * p, M, NOISE_VAR, block=None, predict_block=32768)
+    dt = time.perf_counter() - t0
+    threads = max([i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"] or [1])
+    return {"value": ns / dt, "unit": "samples/s", "cores": int(threads), "kind": "port",
+            "sample": f"N={n} train / N*={ns} test rows of config {cfg} (p={p}, M={M}), one full posterior "
+                      f"(materialised Phi, OpenBLAS SYRK/GEMV, LAPACK potrf), {dt:.2f} s; samples/s scales "
+                      f"linearly in N=N* (m^3 terms negligible)"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    p, M, N, Ns = CONFIGS[args.config]
+    sample = args.cpu_sample
+    vals = []
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(args.config, sample)
+        if i >= args.warmup:
+            vals.append(cb)
+    v = statistics.median([c["value"] for c in vals])
+    cb = dict(vals[-1])
+    cb["value"] = v
+    out = {"metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": 1e3 * (cb_n(args) / v), "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator)",
+           "impl": "reference", "config": config_dict(args, world=1),
+           "cpu_baseline": cb, "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                                       "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def cb_n(args):
+    p, M, N, Ns = CONFIGS[args.config]
+    n = min(args.cpu_sample, N)
+    return max(1, int(round(n * Ns / N)))
+
+
+def config_dict(args, world):
+    p, M, N, Ns = CONFIGS[args.config]
+    return {"workload": f"{args.config}: FAGP posterior mean+var, p={p}, M={M} (m={M**p} features), "
+                        f"N={N} train / N*={Ns} test, eps=rho=1, sigma2={NOISE_VAR}",
+            "p": p, "M": M, "m": M**p, "N_train": N, "N_test": Ns, "parallelism": f"dp{world} (rows sharded)",
+            "l2": "flushed between steps (256 MiB write, outside the timed events)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
+    ap.add_argument("--cpu-sample", type=int, default=100_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+
+    from paper_2403_12797_b200 import GpModel, fagp_posterior
+    from paper_2403_12797_b200 import _lib
+    from paper_2403_12797_b200.distributed import init_from_env
+    from paper_2403_12797_b200.engine import PosteriorEngine
+    from paper_2403_12797_b200.kernels import ArdKernelParams
+
+    rank, world = init_from_env("nccl")
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+
+        group = dist.group.WORLD
+    p, M, N, Ns = CONFIGS[args.config]
+    m = M**p
+    Xh, yh, Xsh = make_inputs(args.config, rank, world)
+    X = torch.from_numpy(Xh).cuda()
+    y = torch.from_numpy(yh).cuda()
+    Xs = torch.from_numpy(Xsh).cuda()
+    kernel = ArdKernelParams.isotropic(p, 1.0, 1.0)
+    eng = PosteriorEngine(kernel, M, X.shape[0], Xs.shape[0], NOISE_VAR, 0.0, device=X.device, group=group)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=X.device)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        eng.run(X, y, Xs)
+    eng.check(X, Xs)
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            e = ev[k]
+            e[0].record(stream)
+            eng.flags.zero_()
+            eng.stage_tables(X, Xs)
+            e[1].record(stream)
+            eng.stage_gram(y)
+            e[2].record(stream)
+            eng.stage_reduce()
+            st = eng.stage_factor()
+            if st != 0:
+                eng.raise_errors(X, Xs, factor_failed=True)
+            e[3].record(stream)
+            eng.stage_predict()
+            e[4].record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    step_ms = [e[0].elapsed_time(e[4]) for e in ev]
+    gram_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    factor_ms = [e[2].elapsed_time(e[3]) for e in ev]
+    pred_ms = [e[3].elapsed_time(e[4]) for e in ev]
+    tab_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    eng.check(X, Xs)
+    ms = statistics.mean(step_ms)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=X.device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = Ns / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (per launch, this rank's shard) ----
+    n_loc, ns_loc = X.shape[0], Xs.shape[0]
+    gram_flops = n_loc * m * (m + 1) + 2 * n_loc * m
+    pred_flops = ns_loc * m * (m + 1) + 4 * ns_loc * m
+    g_ms, p_ms = statistics.mean(gram_ms), statistics.mean(pred_ms)
+    peak, peak_src = fp64_peak()
+    if g_ms >= p_ms:
+        dom, dflops, dms = "gram_kernel (fagp_gram: K1 + K1b reduce)", gram_flops, g_ms
+        traffic = ncu_traffic("gram_kernel")
+    else:
+        dom, dflops, dms = "predict_kernel (fagp_predict: K5)", pred_flops, p_ms
+        traffic = ncu_traffic("predict_kernel")
+    achieved = dflops / (dms / 1e3) / 1e12
+    roofline = {"bound": "tensor", "kernel": dom, "achieved": round(achieved, 3), "peak": peak, "unit": "TFLOP/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                "flops_per_launch": dflops}
+    step_tf = useful_flops(N, Ns, m) / world / (ms / 1e3) / 1e12
+
+    # ---- end to end through the public API (pinned host in, host numpy out) ----
+    e2e = None
+    if not args.no_e2e:
+        Xp = torch.from_numpy(Xh).pin_memory()
+        yp = torch.from_numpy(yh).pin_memory()
+        Xsp = torch.from_numpy(Xsh).pin_memory()
+
+        class Train:
+            X = Xp
+            y = yp
+
+        model = GpModel(kernel, NOISE_VAR, n_eigen=M)
+        fagp_posterior(Train, Xsp, model, memory_cap=None, group=group)  # warm-up
+        times = []
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = fagp_posterior(Train, Xsp, model, memory_cap=None, group=group)
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+            assert r.mean.shape == (ns_loc,) and r.var.shape == (ns_loc,)
+        t = statistics.mean(times)
+        if world > 1:
+            tt = torch.tensor([t], dtype=torch.float64, device=X.device)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            t = float(tt.item())
+        e2e = {"value": Ns / t, "unit": "samples/s", "ms_per_step": t * 1e3,
+               "h2d_bytes_per_step": int((Xh.size + yh.size + Xsh.size) * 8),
+               "d2h_bytes_per_step": int(2 * Xsh.shape[0] * 8),
+               "path": "fagp_posterior(pinned host tensors) -> host numpy mean, var"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.config, args.cpu_sample)
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": round(value, 1), "unit": "samples/s", "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator)",
+               "config": config_dict(args, world), "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
+               "clocks": clk.summary(), "gpu_launches": launches_per_step(m) * args.steps,
+               "phases_ms": {"tables": round(statistics.mean(tab_ms), 3), "gram": round(g_ms, 3),
+                             "allreduce+factor": round(statistics.mean(factor_ms), 3), "predict": round(p_ms, 3)},
+               "step_tflops_useful": round(step_tf, 3), "step_frac_of_peak": round(step_tf / peak, 4),
+               "jitter": eng.jitter.value, "lib": str(_lib.LIB_PATH.name)}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

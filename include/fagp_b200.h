@@ -1,0 +1,177 @@
+/*
+ * fagp_b200.h — C ABI of the B200-native FAGP posterior (libfagp_b200.so).
+ *
+ * The reference (`/root/reference/pkg/src/fagp`, pure Python on numpy/OpenBLAS) has no
+ * native FFI of its own: its hot path calls BLAS/LAPACK through numpy/scipy.  These entry
+ * points replace exactly those call sites, one per stage of `fagp_posterior`
+ * (posterior.py:267-318).  Each declaration cites the reference code it replaces.
+ *
+ * Conventions
+ *  - Every array argument is a DEVICE pointer (row-major, float64, contiguous) unless the
+ *    comment says "host".  The caller owns every buffer (inputs, outputs, workspace);
+ *    the library never allocates device memory and holds no global state.
+ *  - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).  All work is
+ *    stream-ordered.  Only fagp_factor and fagp_read_flags synchronise `stream` (they
+ *    must return a status that depends on device results).
+ *  - Return value: a fagp_status.  The Python host layer maps them onto the reference's
+ *    exceptions (errors.py:6-21): EINVAL -> ValueError, EBUDGET -> BudgetError,
+ *    ENOTPD / ENONFINITE -> NumericalError.
+ */
+#ifndef FAGP_B200_H
+#define FAGP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FAGP_ABI_VERSION 1
+#define FAGP_MAX_P 16 /* input dimensions supported by the feature kernels */
+
+typedef enum fagp_status {
+  FAGP_OK = 0,
+  FAGP_EINVAL = 1,       /* bad shape / argument            -> ValueError            */
+  FAGP_EBUDGET = 2,      /* size over a configured cap      -> BudgetError           */
+  FAGP_ENOTPD = 3,       /* Cholesky breakdown (+pivot)     -> NumericalError        */
+  FAGP_ENONFINITE = 4,   /* non-finite feature (+row, col)  -> NumericalError        */
+  FAGP_ECUDA = 5,        /* CUDA runtime / launch failure                            */
+  FAGP_EWORKSPACE = 6,   /* workspace smaller than *_workspace_size()                */
+  FAGP_EUNSUPPORTED = 7  /* shape outside what the kernels support (p > FAGP_MAX_P)  */
+} fagp_status;
+
+/* Device flag bits written by the feature-generating kernels (fagp_read_flags). */
+#define FAGP_FLAG_X_NONFINITE 1u   /* an input coordinate is not finite  (mercer.py:334-335) */
+#define FAGP_FLAG_PHI_NONFINITE 2u /* a feature value is not finite      (mercer.py:371-376) */
+
+/*
+ * Basis description: the truncated tensor-product SE eigenbasis (mercer.py:1-45).
+ * `table` is a device array of fagp_basis_table_len(p, M) doubles, laid out as
+ *   [0,   p)          rho_beta[d]   = rho_d * beta_d          (mercer.py:279)
+ *   [p,  2p)          neg_delta2[d] = -delta2_d               (mercer.py:281, 94-99)
+ *   [2p, 3p)          sqrt_beta[d]  = sqrt(beta_d)            (mercer.py:281)
+ *   [3p, 3p + p*M)    lam1d[d*M+i]  = eigenvalues_1d(...)[i]  (mercer.py:146-161)
+ * All entries are computed on the host with the reference's own scalar formulas so
+ * they are bit-identical to it (shape_params, mercer.py:102-119).  m must equal M^p.
+ */
+typedef struct fagp_basis {
+  int32_t p;           /* input dimension, 1..FAGP_MAX_P                         */
+  int32_t M;           /* eigenvalues per dimension (GpModel.n_eigen)            */
+  int64_t m;           /* number of tensor-product features, M^p                 */
+  const double* table; /* device, see layout above                               */
+} fagp_basis;
+
+/* ---- library meta ------------------------------------------------------------------ */
+int fagp_abi_version(void);
+const char* fagp_strerror(int status);
+int64_t fagp_basis_table_len(int32_t p, int32_t M);
+
+/* Multi-index enumeration, HOST output (m x p int64, 1-based, first dimension slowest).
+ * Replaces mercer.multi_indices (mercer.py:195-216); bit-exact with it. */
+int fagp_multi_indices(int32_t M, int32_t p, int64_t* out_host);
+
+/* Copy the device flag word to the host (synchronises stream) and clear it. */
+int fagp_read_flags(uint32_t* flags_dev, uint32_t* flags_host, void* stream);
+
+/* ---- (1) eigen-decomposition ------------------------------------------------------- */
+/* Product eigenvalues lam[j] = ((1*lam1[i1])*lam2[i2])*...  (mercer.py:350-353),
+ * the floored copy max(lam, max(lam)*floor_rel) (mercer.py:259-266) and its square root
+ * s = sqrt(lam_floored) (posterior.py:169-170).  Any output may be NULL. */
+int fagp_eigenvalues(const fagp_basis* basis, double floor_rel, double* lam, double* lam_floored,
+                     double* sqrt_lam, void* stream);
+
+/* Normalized Hermite values h_k(z), k < count (mercer.py:122-143).  out: n x count. */
+int fagp_hermite(const double* z, int64_t n, int32_t count, double* out, void* stream);
+
+/* Per-dimension eigenfunction table (_phi_1d, mercer.py:276-281) for every row:
+ * T[r, d*M + i] = (sqrt_beta_d * exp((-delta2_d * x) * x)) * h_i((rho_d beta_d) * x),
+ * x = X[r, d].  X: N x p, T: N x (p*M).  Sets FAGP_FLAG_X_NONFINITE in *flags. */
+int fagp_basis_eval(const double* X, int64_t N, const fagp_basis* basis, double* T,
+                    uint32_t* flags, void* stream);
+
+/* ---- (2) feature matrix ------------------------------------------------------------ */
+/* Materialise Phi (N x m) from the table T (mercer.py:284-292).  Not on the posterior
+ * path (the Gram and predict kernels generate Phi tiles on chip); kept for the
+ * EigenSystem.phi attribute and for parity tests. */
+int fagp_features(const double* T, int64_t N, const fagp_basis* basis, double* phi,
+                  uint32_t* flags, void* stream);
+
+/* Locate the first non-finite Phi entry in row-major order (np.argwhere(~isfinite(phi))[0],
+ * mercer.py:371-376) without materialising Phi.  *first_dev (device int64) receives
+ * row * m + col, or -1 when every feature is finite. */
+int fagp_find_nonfinite(const double* T, int64_t N, const fagp_basis* basis, int64_t* first_dev,
+                        void* stream);
+
+/* Fused feature generation + Gram contraction on FP64 tensor cores (DMMA).
+ * Replaces `backend.gemm(phi, phi, transpose_a=True)` (posterior.py:168) and
+ * `backend.gemm(phi, y - c, transpose_a=True)` (posterior.py:229,233):
+ *   gram_ext = [Phi | r]^T [Phi | r],  r = y - mean_const,
+ * returned as the packed upper triangle of the (m+1) x (m+1) matrix, row-major:
+ * element (i, j), i <= j, at i*(2(m+1) - i - 1)/2 + j.  Column m holds t = Phi^T r.
+ * Phi is never written to HBM.  Deterministic for fixed (N, basis): fixed split-K tree,
+ * no floating-point atomics.  T comes from fagp_basis_eval on the same X. */
+int64_t fagp_gram_packed_len(int64_t m);
+size_t fagp_gram_workspace_size(int64_t N, const fagp_basis* basis);
+int fagp_gram(const double* T, const double* y, double mean_const, int64_t N,
+              const fagp_basis* basis, double* gram_ext_packed, void* workspace,
+              size_t workspace_bytes, uint32_t* flags, void* stream);
+
+/* ---- (3) Cholesky factorisation and solves ----------------------------------------- */
+/* Scaled system A = (s_i G_ij) s_j + sigma2 I (posterior.py:171-174) from the packed Gram,
+ * its Cholesky factor with the reference's jitter schedule [0, b, 10b, 100b],
+ * b = 1e-12 trace(A)/m (backend.py:154-189), the mean weights
+ * w = s * A^{-1}(s * t) (posterior.py:233-235), and V = L^{-1} diag(s) written
+ * transposed into the predict operand.  Synchronises `stream` once per attempt.
+ * Outputs (device): L (m x m, lower; upper part zeroed), G (m x m symmetric, nullable),
+ * t (m), w (m), predict_op (fagp_predict_operand_len(m) doubles; its mean column is
+ * filled with w).  Host outputs: *jitter (the jitter that succeeded), *pivot_index
+ * (1-based LAPACK-style leading minor on ENOTPD, else 0). */
+size_t fagp_factor_workspace_size(int64_t m);
+int64_t fagp_predict_operand_len(int64_t m);
+int fagp_factor(const double* gram_ext_packed, const double* sqrt_lam, double sigma2, int64_t m,
+                int32_t jitter_attempts, double* L, double* G, double* t, double* w,
+                double* predict_op, double* jitter, int32_t* pivot_index, void* workspace,
+                size_t workspace_bytes, void* stream);
+
+/* Overwrite the mean column of the predict operand with w (used after the reference's
+ * fault-injection hook flips w, posterior.py:245-246). */
+int fagp_set_mean_weights(double* predict_op, const double* w, int64_t m, void* stream);
+
+/* Plain lower Cholesky of a symmetric m x m matrix, in place, no jitter: the single
+ * dpotrf call inside SpdFactor (backend.py:172).  *info_dev (device int32) receives 0 or
+ * the 1-based index of the first non-positive pivot.  Upper part is left untouched. */
+size_t fagp_potrf_workspace_size(int64_t m);
+int fagp_potrf(double* A, int64_t m, int32_t* info_dev, void* workspace, size_t workspace_bytes,
+               void* stream);
+
+/* cho_solve (backend.py:191-193): B <- A^{-1} B given the lower factor L; B is m x nrhs. */
+int fagp_potrs(const double* L, int64_t m, double* B, int64_t nrhs, void* stream);
+
+/* General FP64 DMMA GEMM, C = alpha op(A) op(B) + beta C, row-major (op = transpose when
+ * trans_* != 0).  Backs Backend.gemm (backend.py:90-130) and the optional full covariance
+ * (posterior.py:258-263) -- neither is on the mean/variance path. */
+int fagp_dgemm(int32_t trans_a, int32_t trans_b, int64_t M, int64_t N, int64_t K, double alpha,
+               const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+               int64_t ldc, void* stream);
+
+/* V = L^{-1} diag(s) (lower triangular; s may be NULL for L^{-1}).  Replaces the
+ * covariance inner matrix solve_inner(I) (posterior.py:252-255) in restated form. */
+size_t fagp_trtri_workspace_size(int64_t m);
+int fagp_trtri(const double* L, const double* s, int64_t m, double* V, void* workspace,
+               size_t workspace_bytes, void* stream);
+
+/* ---- (4) predictive mean and variance ---------------------------------------------- */
+/* Fused Phi*-generation + FP64 DMMA contraction with [V^T | w] + row reduction:
+ *   mean[i] = mean_const + Phi*_i . w                   (posterior.py:247)
+ *   var[i]  = sigma2 * || V phi*_i ||^2                 (= diag of posterior.py:249-263,
+ *                                                          the variance cli.py:222 reports)
+ * Ts = fagp_basis_eval(Xstar).  var may be NULL (mean only). */
+int fagp_predict(const double* Ts, int64_t Ns, const fagp_basis* basis, const double* predict_op,
+                 double sigma2, double mean_const, double* mean, double* var, uint32_t* flags,
+                 void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FAGP_B200_H */

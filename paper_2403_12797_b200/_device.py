@@ -1,0 +1,78 @@
+"""Device-memory plumbing on top of torch (allocation, host<->device copies, streams).
+
+torch is used only as an allocator / stream provider here; all arithmetic on the posterior
+path happens in libfagp_b200.so.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+_DTYPES = {"float64": "float64", "int64": "int64", "int32": "int32", "uint8": "uint8"}
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def device_of(device=None):
+    torch = _torch()
+    if not torch.cuda.is_available():
+        from ._lib import ExtensionMissing
+
+        raise ExtensionMissing("no CUDA device: paper_2403_12797_b200 runs only on the GPU (no CPU fallback)")
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device(device)
+
+
+def empty(shape, dtype="float64", device=None):
+    torch = _torch()
+    return torch.empty(shape, dtype=getattr(torch, _DTYPES[dtype]), device=device_of(device))
+
+
+def zeros(shape, dtype="float64", device=None):
+    torch = _torch()
+    return torch.zeros(shape, dtype=getattr(torch, _DTYPES[dtype]), device=device_of(device))
+
+
+def to_device(a, device=None, dtype="float64"):
+    """numpy / list / torch tensor -> contiguous CUDA float64 tensor (no copy when already so)."""
+    torch = _torch()
+    tdt = getattr(torch, _DTYPES[dtype])
+    dev = device_of(device)
+    if isinstance(a, torch.Tensor):
+        t = a.to(device=dev, dtype=tdt)
+        return t.contiguous()
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.dtype(dtype)))
+    return torch.from_numpy(arr).to(dev, non_blocking=False)
+
+
+def to_host(t):
+    """CUDA tensor -> numpy (synchronising copy)."""
+    return t.detach().cpu().numpy()
+
+
+def is_tensor(a):
+    torch = _torch()
+    return isinstance(a, torch.Tensor)
+
+
+def points(X, p, name):
+    """Coerce an (N, p) point set to a device tensor, mirroring posterior._as_points
+    (posterior.py:93-97) and the host-side checks of eigensystem (mercer.py:331-335)."""
+    torch = _torch()
+    if isinstance(X, torch.Tensor):
+        Xt = X
+        if Xt.dim() == 1:
+            Xt = Xt.reshape(1, -1) if Xt.numel() else Xt.reshape(0, p)
+        if Xt.dim() != 2 or Xt.shape[1] != p:
+            raise ValueError(f"{name} has {Xt.shape[-1]} columns, expected p={p}")
+        return to_device(Xt)
+    Xh = np.atleast_2d(np.asarray(X, dtype=float))
+    if Xh.shape[1] != p:
+        raise ValueError(f"{name} has {Xh.shape[1]} columns, expected p={p}")
+    # finiteness is checked on the device (FAGP_FLAG_X_NONFINITE from fagp_basis_eval)
+    return to_device(Xh)

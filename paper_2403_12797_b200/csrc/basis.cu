@@ -1,0 +1,329 @@
+// Stage (1) of the path: SE Mercer eigenvalues and 1-D Hermite eigenfunctions.
+//
+// Follows /root/reference/pkg/src/fagp/mercer.py:
+//   normalized_hermite   mercer.py:122-143   (three-term recurrence, kept in registers)
+//   _phi_1d              mercer.py:276-281   (sqrt(beta) * exp((-delta2*x)*x) * h(rho*beta*x))
+//   eigensystem lam      mercer.py:350-353   (tensor products, first dimension slowest)
+//   lam_floored          mercer.py:259-266
+//   multi_indices        mercer.py:195-216
+//   _assemble_phi        mercer.py:284-292   (materialised Phi, test/API use only)
+// Every multiply/subtract is issued as an explicit round-to-nearest op (__dmul_rn,
+// __dsub_rn) so nvcc cannot contract it into an FMA: the result then matches numpy's
+// evaluation order bit for bit except for exp(), whose CUDA and numpy-SIMD versions differ
+// by at most a couple of ulps on a small fraction of arguments.
+#include <cstring>
+
+#include "common.cuh"
+
+namespace fagp {
+
+// Recurrence coefficients exactly as the reference computes them with Python floats:
+// c1[k] = sqrt(2/(k+1)), c2[k] = sqrt(k/(k+1))  (mercer.py:137-142).  IEEE division and
+// square root are correctly rounded on both sides, so these are bit-identical.
+__device__ __forceinline__ double herm_c1(int k) { return __dsqrt_rn(__ddiv_rn(2.0, double(k + 1))); }
+__device__ __forceinline__ double herm_c2(int k) {
+  return __dsqrt_rn(__ddiv_rn(double(k), double(k + 1)));
+}
+
+__global__ void hermite_kernel(const double* __restrict__ z, int64_t n, int count,
+                               double* __restrict__ out) {
+  extern __shared__ double coef[];  // [count] c1, [count] c2
+  for (int k = threadIdx.x; k < count; k += blockDim.x) {
+    coef[k] = herm_c1(k);
+    coef[count + k] = herm_c2(k);
+  }
+  __syncthreads();
+  const double sqrt2 = 1.4142135623730951;  // math.sqrt(2.0)
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    const double zr = z[r];
+    double* o = out + r * count;
+    double hm1 = 1.0;
+    o[0] = 1.0;
+    if (count > 1) {
+      double h = __dmul_rn(zr, sqrt2);
+      o[1] = h;
+      for (int k = 1; k < count - 1; ++k) {
+        // (z * c1[k]) * h_k - c2[k] * h_{k-1}
+        double hn = __dsub_rn(__dmul_rn(__dmul_rn(zr, coef[k]), h), __dmul_rn(coef[count + k], hm1));
+        o[k + 1] = hn;
+        hm1 = h;
+        h = hn;
+      }
+    }
+  }
+}
+
+// T[r, d*M + i] = phi_{i+1}(X[r, d]) for every row r and dimension d.
+// One thread per (row, dim); rows are staged through shared memory so the table rows
+// are written to HBM with coalesced 8-byte stores.
+__global__ void basis_eval_kernel(const double* __restrict__ X, int64_t N, BasisView b,
+                                  double* __restrict__ T, uint32_t* flags, int rows_per_cta) {
+  extern __shared__ double sm[];
+  const int M = b.M, p = b.p, pM = p * M;
+  double* c1 = sm;           // [M]
+  double* c2 = sm + M;       // [M]
+  double* stage = sm + 2 * M;  // [rows_per_cta * pM]
+  for (int k = threadIdx.x; k < M; k += blockDim.x) {
+    c1[k] = herm_c1(k);
+    c2[k] = herm_c2(k);
+  }
+  const int64_t row0 = int64_t(blockIdx.x) * rows_per_cta;
+  const int nrows = int(tmin<int64_t>(rows_per_cta, N - row0));
+  __syncthreads();
+  bool bad_x = false;
+  const double sqrt2 = 1.4142135623730951;
+  for (int task = threadIdx.x; task < nrows * p; task += blockDim.x) {
+    const int rl = task / p, d = task - rl * p;
+    const double x = X[(row0 + rl) * p + d];
+    bad_x |= not_finite(x);
+    const double zr = __dmul_rn(b.rho_beta()[d], x);
+    // sqrt(beta) * exp((-delta2 * x) * x)
+    const double env = __dmul_rn(b.sqrt_beta()[d], exp(__dmul_rn(__dmul_rn(b.neg_delta2()[d], x), x)));
+    double* o = stage + rl * pM + d * M;
+    double hm1 = 1.0;
+    o[0] = __dmul_rn(env, 1.0);
+    if (M > 1) {
+      double h = __dmul_rn(zr, sqrt2);
+      o[1] = __dmul_rn(env, h);
+      for (int k = 1; k < M - 1; ++k) {
+        double hn = __dsub_rn(__dmul_rn(__dmul_rn(zr, c1[k]), h), __dmul_rn(c2[k], hm1));
+        o[k + 1] = __dmul_rn(env, hn);
+        hm1 = h;
+        h = hn;
+      }
+    }
+  }
+  __syncthreads();
+  double* dst = T + row0 * pM;
+  for (int i = threadIdx.x; i < nrows * pM; i += blockDim.x) dst[i] = stage[i];
+  if (bad_x) raise_flag(flags, FAGP_FLAG_X_NONFINITE);
+}
+
+// Phi[r, j] = ((T[r, i_0] * T[r, M + i_1]) * T[r, 2M + i_2]) * ...  with j's mixed-radix
+// digits i_d (first dimension slowest), matching _assemble_phi's broadcast order.
+__global__ void features_kernel(const double* __restrict__ T, int64_t N, BasisView b,
+                                double* __restrict__ phi, uint32_t* flags) {
+  const int64_t m = b.m;
+  const int M = b.M, p = b.p, pM = p * M;
+  bool bad = false;
+  const int64_t total = N * m;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = e / m;
+    int64_t j = e - r * m;
+    const double* Tr = T + r * pM;
+    // digits from the last (fastest) dimension up
+    int dig[FAGP_MAX_P];
+    for (int d = p - 1; d >= 0; --d) {
+      dig[d] = int(j % M);
+      j /= M;
+    }
+    double v = Tr[dig[0]];
+    for (int d = 1; d < p; ++d) v = __dmul_rn(v, Tr[d * M + dig[d]]);
+    bad |= not_finite(v);
+    phi[e] = v;
+  }
+  if (bad) raise_flag(flags, FAGP_FLAG_PHI_NONFINITE);
+}
+
+// Smallest linear index r*m + j with a non-finite Phi[r, j]; int64 max when none.
+__global__ void find_nonfinite_kernel(const double* __restrict__ T, int64_t N, BasisView b,
+                                      unsigned long long* first) {
+  const int64_t m = b.m;
+  const int M = b.M, p = b.p, pM = p * M;
+  const int64_t total = N * m;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = e / m;
+    int64_t j = e - r * m;
+    const double* Tr = T + r * pM;
+    int dig[FAGP_MAX_P];
+    for (int d = p - 1; d >= 0; --d) {
+      dig[d] = int(j % M);
+      j /= M;
+    }
+    double v = Tr[dig[0]];
+    for (int d = 1; d < p; ++d) v = __dmul_rn(v, Tr[d * M + dig[d]]);
+    if (not_finite(v)) atomicMin(first, (unsigned long long)e);
+  }
+}
+
+__global__ void finish_first_kernel(int64_t* first) {
+  if (*reinterpret_cast<unsigned long long*>(first) == ~0ull) *first = -1;
+}
+
+// lam_j = ((1*lam1[i_0]) * lam2[i_1]) * ...; floored = max(lam, max(lam) * floor_rel);
+// s = sqrt(floored).  One CTA: m is at most a few 1e4 and this runs once per fit.
+__global__ void eigenvalues_kernel(BasisView b, double floor_rel, double* lam, double* lam_floored,
+                                   double* sqrt_lam) {
+  __shared__ double red[1024];
+  const int64_t m = b.m;
+  const int M = b.M, p = b.p;
+  const double* l1 = b.lam1d();
+  double mx = -1.0;
+  bool nan_seen = false;
+  for (int64_t j = threadIdx.x; j < m; j += blockDim.x) {
+    int64_t q = j;
+    int dig[FAGP_MAX_P];
+    for (int d = p - 1; d >= 0; --d) {
+      dig[d] = int(q % M);
+      q /= M;
+    }
+    double v = __dmul_rn(1.0, l1[dig[0]]);
+    for (int d = 1; d < p; ++d) v = __dmul_rn(v, l1[d * M + dig[d]]);
+    if (lam) lam[j] = v;
+    if (v != v) nan_seen = true;
+    mx = v > mx ? v : mx;
+  }
+  red[threadIdx.x] = nan_seen ? __longlong_as_double(0x7ff8000000000000LL) : mx;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      double a = red[threadIdx.x], c = red[threadIdx.x + s];
+      red[threadIdx.x] = (a != a || c != c) ? (a != a ? a : c) : (a > c ? a : c);
+    }
+    __syncthreads();
+  }
+  const double floor_v = __dmul_rn(red[0], floor_rel);  // lam.max() * floor_rel
+  for (int64_t j = threadIdx.x; j < m; j += blockDim.x) {
+    int64_t q = j;
+    int dig[FAGP_MAX_P];
+    for (int d = p - 1; d >= 0; --d) {
+      dig[d] = int(q % M);
+      q /= M;
+    }
+    double v = __dmul_rn(1.0, l1[dig[0]]);
+    for (int d = 1; d < p; ++d) v = __dmul_rn(v, l1[d * M + dig[d]]);
+    // np.maximum propagates NaN from either side
+    double f = (v != v || floor_v != floor_v) ? (v != v ? v : floor_v) : (v > floor_v ? v : floor_v);
+    if (lam_floored) lam_floored[j] = f;
+    if (sqrt_lam) sqrt_lam[j] = __dsqrt_rn(f);
+  }
+}
+
+}  // namespace fagp
+
+using namespace fagp;
+
+extern "C" {
+
+int fagp_abi_version(void) { return FAGP_ABI_VERSION; }
+
+const char* fagp_strerror(int status) {
+  switch (status) {
+    case FAGP_OK: return "ok";
+    case FAGP_EINVAL: return "invalid argument";
+    case FAGP_EBUDGET: return "size exceeds the configured budget";
+    case FAGP_ENOTPD: return "matrix is not positive definite";
+    case FAGP_ENONFINITE: return "non-finite feature value";
+    case FAGP_ECUDA: return "CUDA runtime error";
+    case FAGP_EWORKSPACE: return "workspace too small";
+    case FAGP_EUNSUPPORTED: return "shape not supported by the kernels";
+    default: return "unknown status";
+  }
+}
+
+int64_t fagp_basis_table_len(int32_t p, int32_t M) {
+  if (p < 1 || M < 1) return -1;
+  return int64_t(3) * p + int64_t(p) * M;
+}
+
+int fagp_multi_indices(int32_t M, int32_t p, int64_t* out) {
+  if (M < 1 || p < 1 || out == nullptr) return FAGP_EINVAL;
+  int64_t m = 1;
+  for (int d = 0; d < p; ++d) {
+    m *= M;
+    if (m > (int64_t(1) << 40)) return FAGP_EUNSUPPORTED;
+  }
+  for (int64_t j = 0; j < m; ++j) {
+    int64_t q = j;
+    for (int d = p - 1; d >= 0; --d) {
+      out[j * p + d] = 1 + q % M;
+      q /= M;
+    }
+  }
+  return FAGP_OK;
+}
+
+int fagp_read_flags(uint32_t* flags_dev, uint32_t* flags_host, void* stream) {
+  if (flags_dev == nullptr || flags_host == nullptr) return FAGP_EINVAL;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  FAGP_CUDA_TRY(cudaMemcpyAsync(flags_host, flags_dev, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  FAGP_CUDA_TRY(cudaStreamSynchronize(s));
+  FAGP_CUDA_TRY(cudaMemsetAsync(flags_dev, 0, sizeof(uint32_t), s));
+  return FAGP_OK;
+}
+
+int fagp_find_nonfinite(const double* T, int64_t N, const fagp_basis* basis, int64_t* first_dev,
+                        void* stream) {
+  int st = check_basis(basis);
+  if (st) return st;
+  if (first_dev == nullptr || N < 0 || (N > 0 && T == nullptr)) return FAGP_EINVAL;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  FAGP_CUDA_TRY(cudaMemsetAsync(first_dev, 0xff, sizeof(int64_t), s));
+  if (N > 0) {
+    int64_t total = N * basis->m;
+    int grid = int(tmin<int64_t>(ceil_div(total, 256), 16 * num_sms()));
+    find_nonfinite_kernel<<<grid, 256, 0, s>>>(T, N, view(basis), reinterpret_cast<unsigned long long*>(first_dev));
+    FAGP_LAUNCH_CHECK();
+  }
+  finish_first_kernel<<<1, 1, 0, s>>>(first_dev);
+  FAGP_LAUNCH_CHECK();
+  return FAGP_OK;
+}
+
+int fagp_eigenvalues(const fagp_basis* basis, double floor_rel, double* lam, double* lam_floored,
+                     double* sqrt_lam, void* stream) {
+  int st = check_basis(basis);
+  if (st) return st;
+  eigenvalues_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(view(basis), floor_rel, lam,
+                                                                        lam_floored, sqrt_lam);
+  FAGP_LAUNCH_CHECK();
+  return FAGP_OK;
+}
+
+int fagp_hermite(const double* z, int64_t n, int32_t count, double* out, void* stream) {
+  if (count < 1 || n < 0 || (n > 0 && (z == nullptr || out == nullptr))) return FAGP_EINVAL;
+  if (n == 0) return FAGP_OK;
+  size_t smem = size_t(2) * count * sizeof(double);
+  if (smem > 200 * 1024) return FAGP_EUNSUPPORTED;
+  if (smem > 48 * 1024)
+    FAGP_CUDA_TRY(cudaFuncSetAttribute(hermite_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  int grid = int(tmin<int64_t>(ceil_div(n, 256), 4 * num_sms()));
+  hermite_kernel<<<grid, 256, smem, static_cast<cudaStream_t>(stream)>>>(z, n, count, out);
+  FAGP_LAUNCH_CHECK();
+  return FAGP_OK;
+}
+
+int fagp_basis_eval(const double* X, int64_t N, const fagp_basis* basis, double* T, uint32_t* flags,
+                    void* stream) {
+  int st = check_basis(basis);
+  if (st) return st;
+  if (N < 0 || (N > 0 && (X == nullptr || T == nullptr))) return FAGP_EINVAL;
+  if (N == 0) return FAGP_OK;
+  const int64_t pM = int64_t(basis->p) * basis->M;
+  const int rows = int(tmax<int64_t>(1, tmin<int64_t>(64, (96 * 1024) / (pM * 8))));
+  size_t smem = (size_t(2) * basis->M + size_t(rows) * pM) * sizeof(double);
+  if (smem > 200 * 1024) return FAGP_EUNSUPPORTED;
+  FAGP_CUDA_TRY(cudaFuncSetAttribute(basis_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  int64_t grid = ceil_div(N, rows);
+  basis_eval_kernel<<<unsigned(grid), 256, smem, static_cast<cudaStream_t>(stream)>>>(X, N, view(basis), T, flags, rows);
+  FAGP_LAUNCH_CHECK();
+  return FAGP_OK;
+}
+
+int fagp_features(const double* T, int64_t N, const fagp_basis* basis, double* phi, uint32_t* flags,
+                  void* stream) {
+  int st = check_basis(basis);
+  if (st) return st;
+  if (N < 0 || (N > 0 && (T == nullptr || phi == nullptr))) return FAGP_EINVAL;
+  if (N == 0) return FAGP_OK;
+  int64_t total = N * basis->m;
+  int grid = int(tmin<int64_t>(ceil_div(total, 256), 16 * num_sms()));
+  features_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(T, N, view(basis), phi, flags);
+  FAGP_LAUNCH_CHECK();
+  return FAGP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,108 @@
+// Shared device helpers for libfagp_b200 (sm_100a).
+//
+// FP64 tensor-core path on B200: tcgen05 has no f64 kind, so the FP64 MMA is the
+// warp-level mma.sync.m8n8k4.f64, which lowers to SASS DMMA.8x8x4 (256 FMA/instr).
+// Measured on the pool's B200s: 37.06 TF/s register-only (profiles/fp64_peak_r01.json),
+// i.e. one DMMA per 16 clocks per SM sub-partition at 1965 MHz.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/fagp_b200.h"
+
+#define FAGP_CUDA_TRY(expr)                         \
+  do {                                              \
+    cudaError_t _e = (expr);                        \
+    if (_e != cudaSuccess) return FAGP_ECUDA;       \
+  } while (0)
+
+#define FAGP_LAUNCH_CHECK()                          \
+  do {                                               \
+    if (cudaGetLastError() != cudaSuccess) return FAGP_ECUDA; \
+  } while (0)
+
+namespace fagp {
+
+constexpr int kNumSMs = 148;  // B200; only used as a grid-sizing hint (queried at run time)
+
+__host__ inline int num_sms() {
+  static int cached = 0;  // read-only after first call; value is a device property
+  if (cached == 0) {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
+      cached = n;
+    else
+      cached = kNumSMs;
+  }
+  return cached;
+}
+
+// D += A(8x4) * B(4x8) on the FP64 tensor pipe.  Fragment layout (lane = 0..31):
+//   a = A[lane>>2][lane&3], b = B[lane&3][lane>>2],
+//   d0,d1 = D[lane>>2][2*(lane&3) + {0,1}].
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// Integer test for Inf/NaN (exponent all ones); keeps the FP64 pipe free.
+__device__ __forceinline__ bool not_finite(double v) {
+  return ((__double2hiint(v) >> 20) & 0x7ff) == 0x7ff;
+}
+
+__device__ __forceinline__ void cp_async_16(void* smem, const void* gmem) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_8(void* smem, const void* gmem) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Basis table accessors (layout documented in include/fagp_b200.h).
+struct BasisView {
+  int p, M;
+  int64_t m;
+  const double* table;
+  __host__ __device__ const double* rho_beta() const { return table; }
+  __host__ __device__ const double* neg_delta2() const { return table + p; }
+  __host__ __device__ const double* sqrt_beta() const { return table + 2 * p; }
+  __host__ __device__ const double* lam1d() const { return table + 3 * p; }
+};
+
+inline int check_basis(const fagp_basis* b) {
+  if (b == nullptr || b->table == nullptr) return FAGP_EINVAL;
+  if (b->p < 1 || b->M < 1) return FAGP_EINVAL;
+  if (b->p > FAGP_MAX_P) return FAGP_EUNSUPPORTED;
+  int64_t m = 1;
+  for (int d = 0; d < b->p; ++d) {
+    m *= b->M;
+    if (m > (int64_t(1) << 31)) return FAGP_EUNSUPPORTED;
+  }
+  if (m != b->m) return FAGP_EINVAL;
+  return FAGP_OK;
+}
+
+inline BasisView view(const fagp_basis* b) { return BasisView{b->p, b->M, b->m, b->table}; }
+
+template <class T>
+__host__ __device__ __forceinline__ T tmin(T a, T b) { return a < b ? a : b; }
+template <class T>
+__host__ __device__ __forceinline__ T tmax(T a, T b) { return a < b ? b : a; }
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+__device__ __forceinline__ void raise_flag(uint32_t* flags, uint32_t bit) {
+  if (flags) atomicOr(flags, bit);
+}
+
+}  // namespace fagp

@@ -1,0 +1,679 @@
+// Stage (3) of the path: the m x m system.  Replaces, in order,
+//   A = (s G) s + sigma2 I                       posterior.py:171-174
+//   SpdFactor: dpotrf(lower) + jitter schedule   backend.py:154-189
+//   u = cho_solve(A, s*t); w = s*u               posterior.py:233-235, backend.py:191-193
+//   solve_inner(I) for the covariance            posterior.py:252-255  -> V = L^{-1} diag(s)
+// with hand-written kernels:
+//   K2  system_build_kernel   unpack the packed Gram, scale, shift, jitter
+//   K3  blocked right-looking Cholesky, NB = 32:
+//         chol_diag_kernel (one warp factors + inverts the diagonal block, reports the
+//         1-based LAPACK pivot on breakdown), panel = A21 * inv(L11)^T and trailing
+//         A22 -= L21 L21^T, both on the generic FP64-DMMA GEMM below
+//   K4a trsv kernels (single CTA, forward / backward substitution)
+//   K4b TRTRI by recursive doubling (diagonal-block inverses + 2 batched GEMMs per level)
+// The host-side driver keeps the reference's jitter schedule: [0, b, 10b, 100b] with
+// b = 1e-12 * trace(A) / m, trace in numpy's summation order.
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace fagp {
+namespace la {
+
+// ---------------------------------------------------------------------------------------
+// Generic FP64 DMMA GEMM: C = alpha * A op(B) + beta * C, row-major, optional batching
+// (blockIdx.z with element strides), optional lower-triangle-only output.
+constexpr int GT = 64, GK = 16, GNT = 128;
+constexpr int ASP = GK + 4;  // 20 % 16 == 4
+constexpr int BSP = GT + 4;  // 68 % 16 == 4
+
+struct GemmArgs {
+  int M, N, K;
+  double alpha, beta;
+  const double* A;
+  int64_t lda, sA;
+  const double* B;
+  int64_t ldb, sB;
+  double* C;
+  int64_t ldc, sC;
+  int lower_only;
+  const int* info;  // skip all work when *info != 0 (after a Cholesky breakdown)
+};
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(GNT) dgemm_kernel(GemmArgs g) {
+  if (g.info && *g.info) return;
+  const int row0 = blockIdx.y * GT, col0 = blockIdx.x * GT;
+  if (g.lower_only && col0 > row0 + GT - 1) return;
+  const double* A = g.A + blockIdx.z * g.sA;
+  const double* B = g.B + blockIdx.z * g.sB;
+  double* C = g.C + blockIdx.z * g.sC;
+  __shared__ double As[GT * ASP];
+  __shared__ double Bs[GK * BSP];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+  double acc[4][4][2];
+#pragma unroll
+  for (int s = 0; s < 4; ++s)
+#pragma unroll
+    for (int t = 0; t < 4; ++t) acc[s][t][0] = acc[s][t][1] = 0.0;
+
+  for (int k0 = 0; k0 < g.K; k0 += GK) {
+#pragma unroll
+    for (int q = 0; q < (GT * GK) / GNT; ++q) {
+      const int e = tid + q * GNT;
+      if (TA) {  // A stored K x M
+        const int k = e / GT, r = e % GT;
+        const int gr = row0 + r, gk = k0 + k;
+        As[r * ASP + k] = (gr < g.M && gk < g.K) ? A[int64_t(gk) * g.lda + gr] : 0.0;
+      } else {
+        const int r = e / GK, k = e % GK;
+        const int gr = row0 + r, gk = k0 + k;
+        As[r * ASP + k] = (gr < g.M && gk < g.K) ? A[int64_t(gr) * g.lda + gk] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < (GT * GK) / GNT; ++q) {
+      const int e = tid + q * GNT;
+      if (TB) {
+        const int n = e / GK, k = e % GK;
+        const int gn = col0 + n, gk = k0 + k;
+        Bs[k * BSP + n] = (gn < g.N && gk < g.K) ? B[int64_t(gn) * g.ldb + gk] : 0.0;
+      } else {
+        const int k = e / GT, n = e % GT;
+        const int gn = col0 + n, gk = k0 + k;
+        Bs[k * BSP + n] = (gn < g.N && gk < g.K) ? B[int64_t(gk) * g.ldb + gn] : 0.0;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < GK / 4; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int s = 0; s < 4; ++s) a[s] = As[(wm * 32 + s * 8 + (lane >> 2)) * ASP + kk * 4 + (lane & 3)];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) b[t] = Bs[(kk * 4 + (lane & 3)) * BSP + wn * 32 + t * 8 + (lane >> 2)];
+#pragma unroll
+      for (int s = 0; s < 4; ++s)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) dmma_8x8x4(acc[s][t][0], acc[s][t][1], a[s], b[t]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int i = row0 + wm * 32 + s * 8 + (lane >> 2);
+    if (i >= g.M) continue;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = col0 + wn * 32 + t * 8 + 2 * (lane & 3) + e;
+        if (j >= g.N || (g.lower_only && j > i)) continue;
+        double* c = C + int64_t(i) * g.ldc + j;
+        const double v = g.alpha * acc[s][t][e];
+        *c = (g.beta == 0.0) ? v : fma(g.beta, *c, v);
+      }
+    }
+  }
+}
+
+inline int gemm(bool transB, const GemmArgs& g, int batch, cudaStream_t s, bool transA = false) {
+  if (g.M <= 0 || g.N <= 0 || batch <= 0) return FAGP_OK;
+  dim3 grid(unsigned(ceil_div(g.N, GT)), unsigned(ceil_div(g.M, GT)), unsigned(batch));
+  if (transA) {
+    if (transB)
+      dgemm_kernel<true, true><<<grid, GNT, 0, s>>>(g);
+    else
+      dgemm_kernel<true, false><<<grid, GNT, 0, s>>>(g);
+  } else {
+    if (transB)
+      dgemm_kernel<false, true><<<grid, GNT, 0, s>>>(g);
+    else
+      dgemm_kernel<false, false><<<grid, GNT, 0, s>>>(g);
+  }
+  FAGP_LAUNCH_CHECK();
+  return FAGP_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// One warp: lower-triangular inverse of the 32x32 block in S (identity-padded beyond nb),
+// lane c computes column c by forward substitution.  Result into Xs.
+__device__ __forceinline__ void warp_trinv(const double (*S)[33], double (*Xs)[33], int lane) {
+  const int c = lane;
+  for (int i = 0; i < 32; ++i) {
+    double v = 0.0;
+    if (i >= c) {
+      double sum = (i == c) ? 1.0 : 0.0;
+      for (int l = c; l < i; ++l) sum -= S[i][l] * Xs[l][c];
+      v = sum / S[i][i];
+    }
+    Xs[i][c] = v;
+  }
+}
+
+// Diagonal step of the blocked Cholesky: factor A[k0:k0+nb, k0:k0+nb] (lower) in place and
+// write inv(L11) (32x32, identity-padded) to Dinv.  Breakdown (pivot <= 0 or NaN, as in
+// LAPACK dpotrf2) records the 1-based global index in *info and stops.
+__global__ void chol_diag_kernel(double* A, int64_t lda, int64_t k0, int nb, int* info, double* Dinv) {
+  if (*info) return;
+  __shared__ double S[32][33];
+  __shared__ double Xs[32][33];
+  const int lane = threadIdx.x;
+  for (int r = 0; r < 32; ++r)
+    S[r][lane] = (r < nb && lane < nb) ? A[(k0 + r) * lda + k0 + lane] : (r == lane ? 1.0 : 0.0);
+  __syncwarp();
+  for (int j = 0; j < nb; ++j) {
+    const double d = S[j][j];
+    if (!(d > 0.0)) {
+      if (lane == 0) atomicCAS(info, 0, int(k0 + j + 1));
+      return;
+    }
+    const double ljj = sqrt(d);
+    __syncwarp();
+    if (lane == j) S[j][j] = ljj;
+    if (lane > j) S[lane][j] = S[lane][j] / ljj;
+    __syncwarp();
+    if (lane > j && lane < nb) {
+      const double lij = S[lane][j];
+      for (int l = j + 1; l <= lane; ++l) S[lane][l] -= lij * S[l][j];
+    }
+    __syncwarp();
+  }
+  for (int r = 0; r < nb; ++r)
+    if (lane <= r && lane < nb) A[(k0 + r) * lda + k0 + lane] = S[r][lane];
+  // zero the strictly upper entries of S beyond the factor (they still hold A values)
+  for (int r = 0; r < 32; ++r)
+    if (lane > r) S[r][lane] = 0.0;
+  __syncwarp();
+  warp_trinv(S, Xs, lane);
+  __syncwarp();
+  for (int r = 0; r < 32; ++r) Dinv[r * 32 + lane] = Xs[r][lane];
+}
+
+int potrf_blocked(double* A, int64_t m, int64_t lda, int* info, double* Dinv, cudaStream_t s) {
+  for (int64_t k0 = 0; k0 < m; k0 += 32) {
+    const int nb = int(tmin<int64_t>(32, m - k0));
+    chol_diag_kernel<<<1, 32, 0, s>>>(A, lda, k0, nb, info, Dinv);
+    FAGP_LAUNCH_CHECK();
+    const int64_t rest = m - k0 - nb;
+    if (rest <= 0) break;
+    double* A21 = A + (k0 + nb) * lda + k0;
+    GemmArgs pan{int(rest), nb, nb, 1.0, 0.0, A21, lda, 0, Dinv, 32, 0, A21, lda, 0, 0, info};
+    int st = gemm(true, pan, 1, s);
+    if (st) return st;
+    double* A22 = A + (k0 + nb) * lda + (k0 + nb);
+    GemmArgs upd{int(rest), int(rest), nb, -1.0, 1.0, A21, lda, 0, A21, lda, 0, A22, lda, 0, 1, info};
+    st = gemm(true, upd, 1, s);
+    if (st) return st;
+  }
+  return FAGP_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// Triangular solves, one CTA per right-hand side (column of X, row stride ldx).
+constexpr int TS_NT = 1024;
+
+__global__ void __launch_bounds__(TS_NT) trsv_lower_kernel(const double* L, int64_t ld, int64_t m, double* X,
+                                                           int64_t ldx) {
+  double* x = X + blockIdx.x;
+  __shared__ double xb[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int64_t k0 = 0; k0 < m; k0 += 32) {
+    const int nb = int(tmin<int64_t>(32, m - k0));
+    if (warp == 0) {
+      double v = lane < nb ? x[(k0 + lane) * ldx] : 0.0;
+      for (int j = 0; j < nb; ++j) {
+        if (lane == j) v = v / L[(k0 + j) * ld + k0 + j];
+        const double xj = __shfl_sync(0xffffffffu, v, j);
+        if (lane > j && lane < nb) v -= L[(k0 + lane) * ld + k0 + j] * xj;
+      }
+      if (lane < nb) {
+        xb[lane] = v;
+        x[(k0 + lane) * ldx] = v;
+      }
+    }
+    __syncthreads();
+    for (int64_t i = k0 + nb + warp; i < m; i += TS_NT / 32) {
+      double prod = lane < nb ? L[i * ld + k0 + lane] * xb[lane] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) prod += __shfl_xor_sync(0xffffffffu, prod, o);
+      if (lane == 0) x[i * ldx] -= prod;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(TS_NT) trsv_lower_trans_kernel(const double* L, int64_t ld, int64_t m,
+                                                                 double* X, int64_t ldx) {
+  double* x = X + blockIdx.x;
+  __shared__ double xb[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t nblk = ceil_div(m, 32);
+  for (int64_t kb = nblk - 1; kb >= 0; --kb) {
+    const int64_t k0 = kb * 32;
+    const int nb = int(tmin<int64_t>(32, m - k0));
+    if (warp == 0) {
+      double v = lane < nb ? x[(k0 + lane) * ldx] : 0.0;
+      for (int j = nb - 1; j >= 0; --j) {
+        if (lane == j) v = v / L[(k0 + j) * ld + k0 + j];
+        const double xj = __shfl_sync(0xffffffffu, v, j);
+        if (lane < j) v -= L[(k0 + j) * ld + k0 + lane] * xj;
+      }
+      if (lane < nb) {
+        xb[lane] = v;
+        x[(k0 + lane) * ldx] = v;
+      }
+    }
+    __syncthreads();
+    for (int64_t j = tid; j < k0; j += TS_NT) {
+      double acc = 0.0;
+      for (int i = 0; i < nb; ++i) acc += L[(k0 + i) * ld + j] * xb[i];
+      x[j * ldx] -= acc;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Elementwise helpers.
+__device__ __forceinline__ double packed_at(const double* P, int64_t me, int64_t i, int64_t j) {
+  if (i > j) {
+    int64_t t = i;
+    i = j;
+    j = t;
+  }
+  return P[i * (2 * me - i - 1) / 2 + j];
+}
+
+// A[i,j] = (s_i * G_ij) * s_j  (+ sigma2 + jitter on the diagonal); optional G and t.
+__global__ void system_build_kernel(const double* __restrict__ P, const double* __restrict__ s, double sigma2,
+                                    double jit, int64_t m, double* __restrict__ A, double* __restrict__ G,
+                                    double* __restrict__ t) {
+  const int64_t me = m + 1;
+  const int64_t total = m * m;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / m, j = e - (e / m) * m;
+    const double g = packed_at(P, me, i, j);
+    if (G) G[e] = g;
+    if (A) {
+      double a = __dmul_rn(__dmul_rn(s[i], g), s[j]);
+      if (i == j) {
+        a = __dadd_rn(a, sigma2);
+        if (jit != 0.0) a = __dadd_rn(a, jit);
+      }
+      A[e] = a;
+    }
+    if (t && j == 0) t[i] = P[i * (2 * me - i - 1) / 2 + m];
+  }
+}
+
+// numpy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src), as np.trace uses it:
+// result = 0.0 + pairwise(diag).
+__device__ double np_pairwise_sum(const double* a, int64_t n) {
+  // iterative emulation of the recursion with an explicit stack
+  struct Frame {
+    int64_t off, n;
+  };
+  Frame stack[64];
+  double vals[64];
+  int sp = 0, vp = 0;
+  stack[sp++] = Frame{0, n};
+  // post-order evaluation: push markers by encoding n < 0 as "combine"
+  while (sp > 0) {
+    Frame f = stack[--sp];
+    if (f.n < 0) {
+      const double r = vals[--vp];
+      const double l = vals[--vp];
+      vals[vp++] = l + r;
+      continue;
+    }
+    const int64_t cnt = f.n;
+    const double* p = a + f.off;
+    if (cnt < 8) {
+      double res = 0.0;
+      for (int64_t i = 0; i < cnt; ++i) res += p[i];
+      vals[vp++] = res;
+    } else if (cnt <= 128) {
+      double r[8];
+      for (int j = 0; j < 8; ++j) r[j] = p[j];
+      int64_t i;
+      for (i = 8; i < cnt - (cnt % 8); i += 8)
+        for (int j = 0; j < 8; ++j) r[j] += p[i + j];
+      double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+      for (; i < cnt; ++i) res += p[i];
+      vals[vp++] = res;
+    } else {
+      int64_t n2 = cnt / 2;
+      n2 -= n2 % 8;
+      stack[sp++] = Frame{0, -1};
+      stack[sp++] = Frame{f.off + n2, cnt - n2};
+      stack[sp++] = Frame{f.off, n2};
+    }
+  }
+  return vals[0];
+}
+
+__global__ void trace_kernel(const double* A, int64_t m, double* diag_tmp, double* out) {
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) diag_tmp[i] = A[i * m + i];
+  __syncthreads();
+  if (threadIdx.x == 0) *out = 0.0 + np_pairwise_sum(diag_tmp, m);
+}
+
+__global__ void zero_upper_kernel(double* A, int64_t m) {
+  const int64_t total = m * m;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / m, j = e - (e / m) * m;
+    if (j > i) A[e] = 0.0;
+  }
+}
+
+__global__ void vec_mul_kernel(const double* a, const double* b, double* out, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = __dmul_rn(a[i], b[i]);
+}
+
+// ---------------------------------------------------------------------------------------
+// TRTRI by recursive doubling on an identity-padded copy of size mp2 = 32 * 2^k.
+inline int64_t trtri_dim(int64_t m) {
+  int64_t d = 32;
+  while (d < m) d *= 2;
+  return d;
+}
+
+__global__ void pad_lower_kernel(const double* L, int64_t m, int64_t mp, double* Lp) {
+  const int64_t total = mp * mp;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / mp, j = e - (e / mp) * mp;
+    double v;
+    if (i < m && j < m)
+      v = j <= i ? L[i * m + j] : 0.0;
+    else
+      v = (i == j) ? 1.0 : 0.0;
+    Lp[e] = v;
+  }
+}
+
+__global__ void diag_inv_kernel(const double* Lp, int64_t mp, double* X) {
+  __shared__ double S[32][33];
+  __shared__ double Xs[32][33];
+  const int lane = threadIdx.x;
+  const int64_t b0 = int64_t(blockIdx.x) * 32;
+  for (int r = 0; r < 32; ++r) S[r][lane] = lane <= r ? Lp[(b0 + r) * mp + b0 + lane] : 0.0;
+  __syncwarp();
+  warp_trinv(S, Xs, lane);
+  __syncwarp();
+  for (int r = 0; r < 32; ++r) X[(b0 + r) * mp + b0 + lane] = Xs[r][lane];
+}
+
+// X = inv(Lp) (mp x mp, lower).  ws needs mp*mp (Lp) + mp*mp (X) + mp*mp/4 (Tmp) doubles.
+int trtri_padded(const double* L, int64_t m, double* Lp, double* X, double* Tmp, cudaStream_t s) {
+  const int64_t mp = trtri_dim(m);
+  const int grid = int(tmin<int64_t>(ceil_div(mp * mp, 256), 8 * num_sms()));
+  pad_lower_kernel<<<grid, 256, 0, s>>>(L, m, mp, Lp);
+  FAGP_LAUNCH_CHECK();
+  FAGP_CUDA_TRY(cudaMemsetAsync(X, 0, size_t(mp) * mp * sizeof(double), s));
+  diag_inv_kernel<<<unsigned(mp / 32), 32, 0, s>>>(Lp, mp, X);
+  FAGP_LAUNCH_CHECK();
+  for (int64_t h = 32; h < mp; h *= 2) {
+    const int count = int(mp / (2 * h));
+    const int64_t dstride = 2 * h * (mp + 1);
+    // Tmp_q = L21_q * X11_q
+    GemmArgs g1{int(h), int(h), int(h), 1.0, 0.0, Lp + h * mp, mp, dstride, X, mp, dstride, Tmp, h, h * h, 0, nullptr};
+    int st = gemm(false, g1, count, s);
+    if (st) return st;
+    // X21_q = -X22_q * Tmp_q
+    GemmArgs g2{int(h), int(h), int(h), -1.0, 0.0, X + h * (mp + 1), mp, dstride, Tmp, h, h * h, X + h * mp, mp, dstride, 0, nullptr};
+    st = gemm(false, g2, count, s);
+    if (st) return st;
+  }
+  return FAGP_OK;
+}
+
+// V[i,j] = X[i,j] * s_j for j <= i < m, else 0   (s may be null)
+__global__ void scale_lower_kernel(const double* X, int64_t mp, const double* s, int64_t m, double* V) {
+  const int64_t total = m * m;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / m, j = e - (e / m) * m;
+    double v = 0.0;
+    if (j <= i) v = s ? __dmul_rn(X[i * mp + j], s[j]) : X[i * mp + j];
+    V[e] = v;
+  }
+}
+
+// predict operand P (rows pr = round_up(m, 32), cols pc = round_up(m + 1, 128)):
+// P[j, k] = V[k, j] = X[k, j] * s_j for j <= k < m; P[j, m] = w_j; zero elsewhere.
+constexpr int OP_ROW_ALIGN = 32, OP_COL_ALIGN = 128;
+inline int64_t op_rows(int64_t m) { return round_up(m, OP_ROW_ALIGN); }
+inline int64_t op_cols(int64_t m) { return round_up(m + 1, OP_COL_ALIGN); }
+
+__global__ void predict_operand_kernel(const double* X, int64_t mp, const double* s, const double* w, int64_t m,
+                                       double* P, int64_t pr, int64_t pc) {
+  __shared__ double tile[32][33];
+  const int64_t j0 = int64_t(blockIdx.y) * 32, k0 = int64_t(blockIdx.x) * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  // read X[k, j] for k in [k0, k0+32), j in [j0, j0+32): coalesced along j
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t k = k0 + r, j = j0 + tx;
+    double v = 0.0;
+    if (k < m && j < m && j <= k) v = __dmul_rn(X[k * mp + j], s[j]);
+    tile[r][tx] = v;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t j = j0 + r, k = k0 + tx;
+    if (j < pr && k < pc) {
+      double v = tile[tx][r];
+      if (k == m) v = (j < m && w) ? w[j] : 0.0;
+      P[j * pc + k] = v;
+    }
+  }
+}
+
+__global__ void set_mean_weights_kernel(double* P, const double* w, int64_t m, int64_t pc) {
+  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < m; j += int64_t(gridDim.x) * blockDim.x)
+    P[j * pc + m] = w[j];
+}
+
+// ---------------------------------------------------------------------------------------
+// Workspace carving.
+struct FactorWs {
+  int* info;
+  double* scalar;  // trace
+  double* Dinv;    // 32 x 32
+  double* vec;     // m
+  double* Lp;      // mp2^2
+  double* X;       // mp2^2
+  double* Tmp;     // mp2^2 / 4
+  size_t bytes;
+};
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+inline FactorWs carve(void* base, int64_t m) {
+  FactorWs w{};
+  const int64_t mp = trtri_dim(m);
+  size_t off = 0;
+  char* b = static_cast<char*>(base);
+  auto take = [&](size_t bytes) {
+    char* p = b ? b + off : nullptr;
+    off += align256(bytes);
+    return p;
+  };
+  w.info = reinterpret_cast<int*>(take(sizeof(int)));
+  w.scalar = reinterpret_cast<double*>(take(sizeof(double)));
+  w.Dinv = reinterpret_cast<double*>(take(32 * 32 * sizeof(double)));
+  w.vec = reinterpret_cast<double*>(take(size_t(m) * sizeof(double)));
+  w.Lp = reinterpret_cast<double*>(take(size_t(mp) * mp * sizeof(double)));
+  w.X = reinterpret_cast<double*>(take(size_t(mp) * mp * sizeof(double)));
+  w.Tmp = reinterpret_cast<double*>(take(size_t(mp) * mp / 4 * sizeof(double) + sizeof(double)));
+  w.bytes = off;
+  return w;
+}
+
+inline size_t potrf_ws_bytes() { return align256(sizeof(int)) + align256(32 * 32 * sizeof(double)); }
+
+}  // namespace la
+}  // namespace fagp
+
+using namespace fagp;
+using namespace fagp::la;
+
+extern "C" {
+
+size_t fagp_factor_workspace_size(int64_t m) {
+  if (m < 1) return 0;
+  return carve(nullptr, m).bytes;
+}
+
+int64_t fagp_predict_operand_len(int64_t m) {
+  if (m < 1) return -1;
+  return op_rows(m) * op_cols(m);
+}
+
+size_t fagp_potrf_workspace_size(int64_t m) { return m < 1 ? 0 : potrf_ws_bytes(); }
+
+int fagp_potrf(double* A, int64_t m, int32_t* info_dev, void* workspace, size_t workspace_bytes, void* stream) {
+  if (A == nullptr || m < 1 || info_dev == nullptr) return FAGP_EINVAL;
+  if (workspace == nullptr || workspace_bytes < potrf_ws_bytes()) return FAGP_EWORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* Dinv = reinterpret_cast<double*>(static_cast<char*>(workspace) + align256(sizeof(int)));
+  FAGP_CUDA_TRY(cudaMemsetAsync(info_dev, 0, sizeof(int32_t), s));
+  return potrf_blocked(A, m, m, reinterpret_cast<int*>(info_dev), Dinv, s);
+}
+
+int fagp_potrs(const double* L, int64_t m, double* B, int64_t nrhs, void* stream) {
+  if (L == nullptr || B == nullptr || m < 1 || nrhs < 0) return FAGP_EINVAL;
+  if (nrhs == 0) return FAGP_OK;
+  if (nrhs > 65535) return FAGP_EUNSUPPORTED;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  trsv_lower_kernel<<<unsigned(nrhs), TS_NT, 0, s>>>(L, m, m, B, nrhs);
+  FAGP_LAUNCH_CHECK();
+  trsv_lower_trans_kernel<<<unsigned(nrhs), TS_NT, 0, s>>>(L, m, m, B, nrhs);
+  FAGP_LAUNCH_CHECK();
+  return FAGP_OK;
+}
+
+size_t fagp_trtri_workspace_size(int64_t m) {
+  if (m < 1) return 0;
+  const int64_t mp = trtri_dim(m);
+  return align256(size_t(mp) * mp * sizeof(double)) * 2 + align256(size_t(mp) * mp / 4 * sizeof(double) + 8);
+}
+
+int fagp_trtri(const double* L, const double* s, int64_t m, double* V, void* workspace, size_t workspace_bytes,
+               void* stream) {
+  if (L == nullptr || V == nullptr || m < 1) return FAGP_EINVAL;
+  if (workspace == nullptr || workspace_bytes < fagp_trtri_workspace_size(m)) return FAGP_EWORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t mp = trtri_dim(m);
+  double* Lp = static_cast<double*>(workspace);
+  double* X = reinterpret_cast<double*>(static_cast<char*>(workspace) + align256(size_t(mp) * mp * sizeof(double)));
+  double* Tmp = reinterpret_cast<double*>(reinterpret_cast<char*>(X) + align256(size_t(mp) * mp * sizeof(double)));
+  int rc = trtri_padded(L, m, Lp, X, Tmp, st);
+  if (rc) return rc;
+  const int grid = int(tmin<int64_t>(ceil_div(m * m, 256), 8 * num_sms()));
+  scale_lower_kernel<<<grid, 256, 0, st>>>(X, mp, s, m, V);
+  FAGP_LAUNCH_CHECK();
+  return FAGP_OK;
+}
+
+int fagp_dgemm(int32_t trans_a, int32_t trans_b, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+               int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, void* stream) {
+  if (M < 0 || N < 0 || K < 0 || C == nullptr || (K > 0 && (A == nullptr || B == nullptr))) return FAGP_EINVAL;
+  if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return FAGP_EUNSUPPORTED;
+  if (ceil_div(M, GT) > 65535) return FAGP_EUNSUPPORTED;
+  GemmArgs g{int(M), int(N), int(K), alpha, beta, A, lda, 0, B, ldb, 0, C, ldc, 0, 0, nullptr};
+  return gemm(trans_b != 0, g, 1, static_cast<cudaStream_t>(stream), trans_a != 0);
+}
+
+int fagp_set_mean_weights(double* predict_op, const double* w, int64_t m, void* stream) {
+  if (predict_op == nullptr || w == nullptr || m < 1) return FAGP_EINVAL;
+  set_mean_weights_kernel<<<unsigned(ceil_div(m, 256)), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      predict_op, w, m, op_cols(m));
+  FAGP_LAUNCH_CHECK();
+  return FAGP_OK;
+}
+
+int fagp_factor(const double* packed, const double* sqrt_lam, double sigma2, int64_t m, int32_t jitter_attempts,
+                double* L, double* G, double* t, double* w, double* predict_op, double* jitter_out,
+                int32_t* pivot_out, void* workspace, size_t workspace_bytes, void* stream) {
+  if (packed == nullptr || sqrt_lam == nullptr || L == nullptr || t == nullptr || w == nullptr || m < 1 ||
+      jitter_attempts < 0)
+    return FAGP_EINVAL;
+  if (!(sigma2 > 0.0) || !std::isfinite(sigma2)) return FAGP_EINVAL;
+  FactorWs ws = carve(workspace, m);
+  if (workspace == nullptr || workspace_bytes < ws.bytes) return FAGP_EWORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int grid = int(tmin<int64_t>(ceil_div(m * m, 256), 8 * num_sms()));
+  if (pivot_out) *pivot_out = 0;
+  if (jitter_out) *jitter_out = 0.0;
+
+  // G and t once (A is rebuilt per attempt below)
+  system_build_kernel<<<grid, 256, 0, s>>>(packed, sqrt_lam, sigma2, 0.0, m, nullptr, G, t);
+  FAGP_LAUNCH_CHECK();
+
+  double base = 0.0;
+  bool have_base = false;
+  int info_h = 0;
+  for (int attempt = 0; attempt <= jitter_attempts; ++attempt) {
+    double jit = 0.0;
+    if (attempt > 0) {
+      if (!have_base) {
+        // trace of the un-jittered A, in numpy's summation order (np.trace)
+        system_build_kernel<<<grid, 256, 0, s>>>(packed, sqrt_lam, sigma2, 0.0, m, L, nullptr, nullptr);
+        FAGP_LAUNCH_CHECK();
+        trace_kernel<<<1, 256, 0, s>>>(L, m, ws.vec, ws.scalar);
+        FAGP_LAUNCH_CHECK();
+        double tr = 0.0;
+        FAGP_CUDA_TRY(cudaMemcpyAsync(&tr, ws.scalar, sizeof(double), cudaMemcpyDeviceToHost, s));
+        FAGP_CUDA_TRY(cudaStreamSynchronize(s));
+        base = 1e-12 * tr / double(m);
+        have_base = true;
+      }
+      double p10 = 1.0;
+      for (int k = 1; k < attempt; ++k) p10 *= 10.0;
+      jit = base * p10;
+    }
+    system_build_kernel<<<grid, 256, 0, s>>>(packed, sqrt_lam, sigma2, jit, m, L, nullptr, nullptr);
+    FAGP_LAUNCH_CHECK();
+    FAGP_CUDA_TRY(cudaMemsetAsync(ws.info, 0, sizeof(int), s));
+    int rc = potrf_blocked(L, m, m, ws.info, ws.Dinv, s);
+    if (rc) return rc;
+    FAGP_CUDA_TRY(cudaMemcpyAsync(&info_h, ws.info, sizeof(int), cudaMemcpyDeviceToHost, s));
+    FAGP_CUDA_TRY(cudaStreamSynchronize(s));
+    if (jitter_out) *jitter_out = jit;
+    if (info_h == 0) break;
+  }
+  if (info_h != 0) {
+    if (pivot_out) *pivot_out = info_h;
+    return FAGP_ENOTPD;
+  }
+  zero_upper_kernel<<<grid, 256, 0, s>>>(L, m);
+  FAGP_LAUNCH_CHECK();
+  // w = s * A^{-1} (s * t)
+  const int vgrid = int(ceil_div(m, 256));
+  vec_mul_kernel<<<vgrid, 256, 0, s>>>(sqrt_lam, t, ws.vec, m);
+  FAGP_LAUNCH_CHECK();
+  trsv_lower_kernel<<<1, TS_NT, 0, s>>>(L, m, m, ws.vec, 1);
+  FAGP_LAUNCH_CHECK();
+  trsv_lower_trans_kernel<<<1, TS_NT, 0, s>>>(L, m, m, ws.vec, 1);
+  FAGP_LAUNCH_CHECK();
+  vec_mul_kernel<<<vgrid, 256, 0, s>>>(sqrt_lam, ws.vec, w, m);
+  FAGP_LAUNCH_CHECK();
+  if (predict_op) {
+    int rc = trtri_padded(L, m, ws.Lp, ws.X, ws.Tmp, s);
+    if (rc) return rc;
+    const int64_t pr = op_rows(m), pc = op_cols(m);
+    dim3 g2(unsigned(ceil_div(pc, 32)), unsigned(ceil_div(pr, 32)));
+    predict_operand_kernel<<<g2, dim3(32, 8), 0, s>>>(ws.X, trtri_dim(m), sqrt_lam, w, m, predict_op, pr, pc);
+    FAGP_LAUNCH_CHECK();
+  }
+  return FAGP_OK;
+}
+
+}  // extern "C"

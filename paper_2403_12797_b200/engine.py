@@ -1,0 +1,146 @@
+"""PosteriorEngine: the fused FAGP posterior pipeline with every buffer preallocated.
+
+One engine per (basis, N, N*) shape.  ``run`` issues, on the current CUDA stream:
+
+    fagp_basis_eval(X), fagp_basis_eval(X*)           K0   1-D eigenfunction tables
+    fagp_gram                                          K1   fused Phi-gen + DMMA Gram (+ t)
+    [all_reduce(SUM) of the packed Gram over `group`]  C1   NCCL over NVLink when sharded
+    fagp_factor                                        K2-K4  A, Cholesky+jitter, w, V^T
+    fagp_predict                                       K5   fused Phi*-gen + DMMA + row sums
+
+and performs exactly one host synchronisation (inside fagp_factor, which must read the
+Cholesky status to run the reference's jitter schedule).  No allocation happens inside
+``run``, so it is safe to time and to call repeatedly.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+from . import _device as dev
+from . import _lib
+from .errors import NumericalError
+from .mercer import LAMBDA_FLOOR_REL, Basis, raise_nonfinite
+
+JITTER_ATTEMPTS = 3  # backend.py:165
+
+
+class PosteriorEngine:
+    def __init__(self, kernel, n_eigen, N, Ns, noise_var, mean_const=0.0, delta2_variant="rho_squared",
+                 device=None, group=None, want_var=True, keep_gram=False):
+        L = _lib.lib()
+        self.basis = Basis(kernel, n_eigen, delta2_variant, device=device)
+        b = self.basis
+        self.device = b.table.device
+        self.N, self.Ns = int(N), int(Ns)
+        self.noise_var = float(noise_var)
+        self.mean_const = float(mean_const)
+        self.group = group
+        self.want_var = want_var
+        m, pM = b.m, b.p * b.n
+        e = lambda *shape: dev.empty(shape, device=self.device)  # noqa: E731
+        self.T = e(self.N, pM)
+        self.Ts = e(self.Ns, pM)
+        self.packed = e(int(L.fagp_gram_packed_len(m)))
+        self.gram_ws_bytes = int(L.fagp_gram_workspace_size(self.N, b.ref))
+        self.gram_ws = e(max(1, self.gram_ws_bytes // 8))
+        self.lam, self.lam_floored, self.sqrt_lam = e(m), e(m), e(m)
+        self.L = e(m, m)
+        self.G = e(m, m) if keep_gram else None
+        self.t, self.w = e(m), e(m)
+        self.predict_op = e(int(L.fagp_predict_operand_len(m)))
+        self.factor_ws_bytes = int(L.fagp_factor_workspace_size(m))
+        self.factor_ws = e(max(1, self.factor_ws_bytes // 8))
+        self.mean = e(self.Ns)
+        self.var = e(self.Ns) if want_var else None
+        self.flags = dev.zeros((2,), dtype="int32", device=self.device)
+        self.jitter = ctypes.c_double(0.0)
+        self.pivot = ctypes.c_int32(0)
+        self.status = 0
+        _lib.check(L.fagp_eigenvalues(b.ref, LAMBDA_FLOOR_REL, _lib.ptr(self.lam), _lib.ptr(self.lam_floored),
+                                      _lib.ptr(self.sqrt_lam), _lib.stream_handle()), "eigenvalues")
+
+    def _flag(self, k):
+        return ctypes.c_void_p(self.flags.data_ptr() + 4 * k)
+
+    # -- stages (each usable alone, e.g. for per-kernel timing) --------------------------
+    def stage_tables(self, X, Xs, stream=None):
+        L, s, b = _lib.lib(), _lib.stream_handle(stream), self.basis
+        if self.N:
+            _lib.check(L.fagp_basis_eval(_lib.ptr(X), self.N, b.ref, _lib.ptr(self.T), self._flag(0), s), "basis_eval")
+        if self.Ns:
+            _lib.check(L.fagp_basis_eval(_lib.ptr(Xs), self.Ns, b.ref, _lib.ptr(self.Ts), self._flag(1), s),
+                       "basis_eval")
+
+    def stage_gram(self, y, stream=None):
+        L, s, b = _lib.lib(), _lib.stream_handle(stream), self.basis
+        _lib.check(L.fagp_gram(_lib.ptr(self.T), _lib.ptr(y) if self.N else None, self.mean_const, self.N, b.ref,
+                               _lib.ptr(self.packed), _lib.ptr(self.gram_ws), self.gram_ws_bytes, self._flag(0), s),
+                   "gram")
+
+    def stage_reduce(self):
+        if self.group is not None:
+            from .distributed import all_reduce_sum
+
+            all_reduce_sum(self.packed, self.group)
+
+    def stage_factor(self, stream=None):
+        L, s, b = _lib.lib(), _lib.stream_handle(stream), self.basis
+        self.status = L.fagp_factor(_lib.ptr(self.packed), _lib.ptr(self.sqrt_lam), self.noise_var, b.m,
+                                    JITTER_ATTEMPTS, _lib.ptr(self.L), _lib.ptr(self.G), _lib.ptr(self.t),
+                                    _lib.ptr(self.w), _lib.ptr(self.predict_op), ctypes.byref(self.jitter),
+                                    ctypes.byref(self.pivot), _lib.ptr(self.factor_ws), self.factor_ws_bytes, s)
+        if self.status not in (_lib.FAGP_OK, _lib.FAGP_ENOTPD):
+            _lib.check(self.status, "factor")
+        return self.status
+
+    def set_mean_weights(self, stream=None):
+        _lib.check(_lib.lib().fagp_set_mean_weights(_lib.ptr(self.predict_op), _lib.ptr(self.w), self.basis.m,
+                                                    _lib.stream_handle(stream)), "set_mean_weights")
+
+    def stage_predict(self, stream=None):
+        L, s, b = _lib.lib(), _lib.stream_handle(stream), self.basis
+        if self.Ns:
+            _lib.check(L.fagp_predict(_lib.ptr(self.Ts), self.Ns, b.ref, _lib.ptr(self.predict_op), self.noise_var,
+                                      self.mean_const, _lib.ptr(self.mean), _lib.ptr(self.var), self._flag(1), s),
+                       "predict")
+
+    # -- the whole step -------------------------------------------------------------------
+    def run(self, X, y, Xs, fault_flip=False):
+        """One posterior evaluation from device-resident inputs; returns device (mean, var)."""
+        self.flags.zero_()
+        self.stage_tables(X, Xs)
+        self.stage_gram(y)
+        self.stage_reduce()
+        st = self.stage_factor()
+        if st != _lib.FAGP_OK:
+            self.raise_errors(X, Xs, factor_failed=True)
+        if fault_flip:
+            self.w.neg_()
+            self.set_mean_weights()
+        self.stage_predict()
+        return self.mean, self.var
+
+    def raise_errors(self, X=None, Xs=None, factor_failed=False, after_predict=False):
+        """Raise the reference's exception for whatever went wrong (validation order of
+        fagp_posterior: train X, train Phi, test X, test Phi, then the factorisation)."""
+        fl = [int(v) for v in dev.to_host(self.flags)]
+        b = self.basis
+        if fl[0] & _lib.FLAG_X_NONFINITE:
+            raise ValueError("X must be finite")
+        if fl[0] & _lib.FLAG_PHI_NONFINITE:
+            raise_nonfinite(self.T, X, b)
+        if fl[1] & _lib.FLAG_X_NONFINITE:
+            raise ValueError("X must be finite")
+        if (fl[1] & _lib.FLAG_PHI_NONFINITE) or factor_failed:
+            if self.Ns:
+                raise_nonfinite(self.Ts, Xs, b)
+        if factor_failed:
+            piv = int(self.pivot.value)
+            raise NumericalError(
+                f"matrix of order {b.m} is not positive definite: leading minor {piv} failed even with "
+                f"diagonal jitter up to the third escalation", pivot_index=piv)
+
+    def check(self, X, Xs):
+        """Post-run validation (one small D2H read of the flag words)."""
+        self.raise_errors(X, Xs)

@@ -1,0 +1,48 @@
+"""CPU: the C-ABI library loads and exports every symbol include/fagp_b200.h declares."""
+
+import ctypes
+import re
+from pathlib import Path
+
+from paper_2403_12797_b200 import _lib
+
+HEADER = Path(__file__).resolve().parents[1] / "include" / "fagp_b200.h"
+
+
+def declared_functions():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return set(re.findall(r"\b(fagp_[a-z0-9_]+)\s*\(", text))
+
+
+def test_header_declares_expected_surface():
+    names = declared_functions()
+    for must in ("fagp_gram", "fagp_factor", "fagp_predict", "fagp_basis_eval", "fagp_multi_indices",
+                 "fagp_eigenvalues", "fagp_potrf", "fagp_potrs", "fagp_trtri", "fagp_strerror"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+
+
+def test_bindings_cover_header():
+    assert declared_functions() == set(_lib.SIGNATURES)
+
+
+def test_host_only_entry_points():
+    lib = _lib.load()
+    assert lib.fagp_abi_version() == _lib.ABI_VERSION
+    assert lib.fagp_strerror(_lib.FAGP_ENOTPD) == b"matrix is not positive definite"
+    assert lib.fagp_basis_table_len(3, 10) == 3 * 3 + 30
+    assert lib.fagp_gram_packed_len(1000) == 1001 * 1002 // 2
+    assert lib.fagp_predict_operand_len(1000) == 1024 * 1024
+    assert lib.fagp_factor_workspace_size(1000) > 0
+    b = _lib.FagpBasis(3, 10, 1000, None)
+    assert lib.fagp_gram_workspace_size(1000000, ctypes.byref(b)) == 0  # null table is rejected
+    buf = (ctypes.c_int64 * 24)()
+    assert lib.fagp_multi_indices(2, 3, buf) == 0
+    assert list(buf)[:6] == [1, 1, 1, 1, 1, 2]
+    assert lib.fagp_multi_indices(0, 3, buf) == _lib.FAGP_EINVAL

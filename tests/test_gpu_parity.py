@@ -1,0 +1,227 @@
+"""GPU parity: the CUDA path against the reference outputs (golden) and the oracle.
+
+Tolerances (BASELINE.json north_star):
+  * multi-indices, lam, lam_floored        bit-exact
+  * Phi (exp differs by ulps, F5)          rtol 1e-13
+  * G, t                                   max|d| / max|ref| <= 1e-12
+  * mean, var                              elementwise relative <= 1e-9
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import fagp_oracle as O
+import paper_2403_12797_b200 as F
+from conftest import CASE_NAMES, rel_err, scaled_err
+from paper_2403_12797_b200 import _device as dev
+from paper_2403_12797_b200.posterior import _stage_tables, factor_packed, gram_packed
+
+pytestmark = pytest.mark.gpu
+
+MEAN_VAR_RTOL = 1e-9
+GRAM_TOL = 1e-12
+
+
+def unpack(packed, m):
+    me = m + 1
+    full = np.zeros((me, me))
+    iu = np.triu_indices(me)
+    full[iu] = packed
+    full = full + np.triu(full, 1).T
+    return full[:m, :m], full[:m, m]
+
+
+def test_library_is_the_cuda_extension():
+    from paper_2403_12797_b200 import _lib
+
+    L = _lib.lib()
+    assert L._name.endswith("libfagp_b200.so")
+    assert torch.cuda.is_available()
+
+
+@pytest.mark.parametrize("name", CASE_NAMES)
+def test_posterior_mean_var_parity(cases, name):
+    c = cases[name]
+    res = F.fagp_posterior(c.dataset(), c.Xs, c.model(), delta2_variant=c.variant, memory_cap=None)
+    assert res.mean.shape == (c.Ns,) and res.var.shape == (c.Ns,)
+    assert rel_err(res.mean, c.ref["mean"]) <= MEAN_VAR_RTOL, rel_err(res.mean, c.ref["mean"])
+    assert rel_err(res.var, c.ref["var"]) <= MEAN_VAR_RTOL, rel_err(res.var, c.ref["var"])
+
+
+@pytest.mark.parametrize("name", CASE_NAMES)
+def test_gram_and_t_parity(cases, name):
+    c = cases[name]
+    basis = F.Basis(c.kernel(), c.M, c.variant)
+    X = dev.to_device(c.X)
+    T = _stage_tables(basis, X, None, None)
+    packed = dev.to_host(gram_packed(basis, T, dev.to_device(c.y), c.mean_const))
+    G, t = unpack(packed, basis.m)
+    assert scaled_err(t, c.ref["t"]) <= GRAM_TOL
+    assert scaled_err(np.diag(G), c.ref["G_diag"]) <= GRAM_TOL
+    rows = [0, 1, basis.m // 2, basis.m - 1]
+    assert scaled_err(G[rows], c.ref["G_rows"]) <= GRAM_TOL
+    assert abs(np.linalg.norm(G) - float(c.ref["G_fro"])) <= GRAM_TOL * float(c.ref["G_fro"])
+    if "G" in c.ref:
+        assert scaled_err(G, c.ref["G"]) <= GRAM_TOL
+    assert np.array_equal(G, G.T)
+
+
+@pytest.mark.parametrize("name", ["c1", "c3s", "ard4", "lin2", "c5s"])
+def test_eigenvalues_bit_exact(cases, name):
+    c = cases[name]
+    basis = F.Basis(c.kernel(), c.M, c.variant)
+    f, st, _ = factor_packed(basis, dev.zeros((int(basis.m + 1) * (basis.m + 2) // 2,)), c.noise_var, 0.0, 0)
+    assert np.array_equal(dev.to_host(f.lam), c.ref["lam"])
+    assert np.array_equal(dev.to_host(f.lam_floored), c.ref["lam_floored"])
+    assert np.array_equal(dev.to_host(f.sqrt_lam), np.sqrt(c.ref["lam_floored"]))
+
+
+@pytest.mark.parametrize("name", ["c1", "c3s", "ard4", "lin2"])
+def test_features_match_reference_phi(cases, name):
+    c = cases[name]
+    es = F.eigensystem(c.X[:8], c.kernel(), c.M, delta2_variant=c.variant)
+    np.testing.assert_allclose(es.phi, c.ref["phi_head"], rtol=1e-13, atol=0)
+    assert np.array_equal(es.lam, c.ref["lam"])
+
+
+def test_multi_indices_bit_exact(golden):
+    for key, ref in golden.items():
+        if key.startswith("indices/"):
+            n, p = (int(v) for v in key.split("/")[1].split("_"))
+            got = F.multi_indices(n, p)
+            assert got.dtype == np.int64 and np.array_equal(got, ref)
+
+
+def test_factor_jitter_matches_reference(cases):
+    for name in ("c1", "c2s", "c3s"):
+        c = cases[name]
+        basis = F.Basis(c.kernel(), c.M, c.variant)
+        T = _stage_tables(basis, dev.to_device(c.X), None, None)
+        packed = gram_packed(basis, T, dev.to_device(c.y), c.mean_const)
+        f, st, piv = factor_packed(basis, packed, c.noise_var, c.mean_const, c.N)
+        assert st == 0 and piv == 0
+        assert f.jitter == float(c.ref["jitter"])
+
+
+def test_weights_match_oracle(cases):
+    c = cases["c2s"]
+    basis = F.Basis(c.kernel(), c.M, c.variant)
+    T = _stage_tables(basis, dev.to_device(c.X), None, None)
+    packed = gram_packed(basis, T, dev.to_device(c.y), c.mean_const)
+    f, st, _ = factor_packed(basis, packed, c.noise_var, c.mean_const, c.N)
+    G, t = unpack(dev.to_host(packed), basis.m)
+    o = O.factor(G, t, c.ref["lam"], c.noise_var)
+    assert scaled_err(dev.to_host(f.w), o["w"]) < 1e-10
+    Lg = dev.to_host(f.L)
+    assert scaled_err(Lg, o["L"]) < 1e-12
+    assert np.all(np.triu(Lg, 1) == 0)
+
+
+def test_run_to_run_bitwise_determinism(cases):
+    c = cases["c3s"]
+    a = F.fagp_posterior(c.dataset(), c.Xs, c.model(), memory_cap=None)
+    b = F.fagp_posterior(c.dataset(), c.Xs, c.model(), memory_cap=None)
+    assert np.array_equal(a.mean, b.mean) and np.array_equal(a.var, b.var)
+
+
+def test_split_api_matches_one_shot(cases):
+    c = cases["c2s"]
+    full = F.fagp_posterior(c.dataset(), c.Xs, c.model(), memory_cap=None)
+    es = F.eigensystem(c.X, c.kernel(), c.M, memory_cap=None)
+    es_s = F.eigensystem(c.Xs, c.kernel(), c.M, memory_cap=None)
+    split = F.fagp_posterior_from_eigensystems(es, es_s, c.y, c.model())
+    assert np.array_equal(full.mean, split.mean) and np.array_equal(full.var, split.var)
+    h = F.fit(c.dataset(), c.model(), memory_cap=None)
+    pr = F.predict(h, c.Xs)
+    assert np.array_equal(full.mean, pr.mean) and np.array_equal(full.var, pr.var)
+
+
+def test_device_inputs_match_host_inputs(cases):
+    c = cases["c1"]
+
+    class DS:
+        X = torch.as_tensor(c.X, device="cuda")
+        y = torch.as_tensor(c.y, device="cuda")
+
+    a = F.fagp_posterior(DS, torch.as_tensor(c.Xs, device="cuda"), c.model(), return_device=True)
+    b = F.fagp_posterior(c.dataset(), c.Xs, c.model())
+    assert a.mean.is_cuda and np.array_equal(dev.to_host(a.mean), b.mean)
+
+
+def test_full_covariance_matches_reference_diag(cases):
+    c = cases["ard4"]
+    res = F.fagp_posterior(c.dataset(), c.Xs, c.model(), want_cov=True)
+    assert res.cov.shape == (c.Ns, c.Ns)
+    assert np.array_equal(res.cov, res.cov.T)
+    assert rel_err(np.diag(res.cov), c.ref["var"]) < 1e-9
+
+
+def test_hermite_kats_on_device():
+    h = F.normalized_hermite(np.array([0.75, -2.5, 5.0]), 91)
+    assert h[0, 12] == pytest.approx(-0.52375113515335598, rel=1e-13)
+    assert h[1, 40] == pytest.approx(-8.0292666658136296, rel=1e-13)
+    assert h[2, 90] == pytest.approx(77354.543657580687, rel=1e-12)
+    z = np.array([0.0, 0.5, -1.25])
+    hz = F.normalized_hermite(z, 3)
+    assert np.array_equal(hz, O.normalized_hermite(z, 3))  # bit-exact recurrence
+    assert np.all(np.isfinite(F.normalized_hermite(np.linspace(-8, 8, 33), 300)))
+    zz = np.linspace(-3, 3, 1001)
+    assert np.array_equal(F.normalized_hermite(zz, 40), O.normalized_hermite(zz, 40))
+
+
+def test_eigenfunction_kats_on_device():
+    p12 = F.KernelParams1D(1.0, 2.0)
+    assert F.eigenfunction_1d(7, 0.3, p12) == pytest.approx(0.61576462019268915, rel=1e-13)
+    assert F.eigenfunction_1d(1, 0.0, p12) == pytest.approx(2 ** 0.125, rel=1e-15)
+    for params in (F.KernelParams1D(1.0, 1.0), p12, F.KernelParams1D(0.2, 0.7)):
+        assert F.eigenfunction_1d(2, 0.0, params) == 0.0
+    assert F.eigenfunction_1d(3, 1.0, F.KernelParams1D(0.0, 1.0)) == pytest.approx(0.7071067811865476, rel=1e-12)
+    xs = np.linspace(0.05, 2.5, 9)
+    for i in range(1, 13):
+        np.testing.assert_allclose(F.eigenfunction_1d(i, -xs, F.KernelParams1D(1.0, 1.0)),
+                                   (-1.0) ** (i - 1) * F.eigenfunction_1d(i, xs, F.KernelParams1D(1.0, 1.0)),
+                                   rtol=1e-12)
+
+
+@pytest.mark.parametrize("p,M,N,Ns", [(1, 1, 5, 3), (1, 7, 33, 129), (2, 3, 200, 257), (3, 4, 1000, 130),
+                                      (6, 2, 500, 64), (1, 130, 2000, 50)])
+def test_ragged_shapes_against_oracle(p, M, N, Ns):
+    rng = np.random.default_rng(p * 1000 + M)
+    X = rng.uniform(-1, 1, (N, p))
+    y = np.cos(X).sum(1) + 0.05 * rng.standard_normal(N)
+    Xs = rng.uniform(-1, 1, (Ns, p))
+    eps = rng.uniform(0.3, 1.5, p)
+    rho = rng.uniform(0.5, 2.0, p)
+    kernel = F.ArdKernelParams(tuple(F.KernelParams1D(float(e), float(r)) for e, r in zip(eps, rho)))
+    model = F.GpModel(kernel, 0.01, mean_const=0.3, n_eigen=M)
+    ref = O.posterior(X, y, Xs, eps, rho, M, 0.01, 0.3)
+
+    class DS:
+        pass
+
+    DS.X, DS.y = X, y
+    res = F.fagp_posterior(DS, Xs, model, memory_cap=None)
+    assert rel_err(res.mean, ref["mean"]) <= MEAN_VAR_RTOL
+    assert rel_err(res.var, ref["var"]) <= MEAN_VAR_RTOL
+
+
+@pytest.mark.slow
+def test_c3_full_size_properties():
+    """BASELINE config C3 at full size: determinism, sanity bounds and subsample parity."""
+    from paper_2403_12797_b200.datagen import generate, test_inputs, train_seed
+
+    p, M, N = 3, 10, 1_000_000
+    ds = generate(N, p, train_seed(p), 0.05)
+    Xs = test_inputs(N, p)
+    kernel = F.ArdKernelParams.isotropic(p, 1.0, 1.0)
+    model = F.GpModel(kernel, 0.0025, n_eigen=M)
+    a = F.fagp_posterior(ds, Xs, model, memory_cap=None)
+    b = F.fagp_posterior(ds, Xs, model, memory_cap=None)
+    assert np.array_equal(a.mean, b.mean) and np.array_equal(a.var, b.var)
+    assert np.all(np.isfinite(a.mean)) and np.all(a.var >= 0)
+    # oracle on the full train set (blocked Gram), test subsample
+    idx = np.arange(0, N, 997)
+    ref = O.posterior(ds.X, ds.y, Xs[idx], [1.0] * p, [1.0] * p, M, 0.0025, block=65536)
+    assert rel_err(a.mean[idx], ref["mean"]) <= MEAN_VAR_RTOL
+    assert rel_err(a.var[idx], ref["var"]) <= MEAN_VAR_RTOL
