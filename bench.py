@@ -276,9 +276,9 @@ def main():
             e = ev[k]
             e[0].record(stream)
             eng.flags.zero_()
-            eng.stage_tables(X, Xs)
+            eng.stage_tables(X, y, Xs)
             e[1].record(stream)
-            eng.stage_gram(y)
+            eng.stage_gram()
             e[2].record(stream)
             eng.stage_reduce()
             st = eng.stage_factor()

@@ -84,11 +84,22 @@ int fagp_eigenvalues(const fagp_basis* basis, double floor_rel, double* lam, dou
 /* Normalized Hermite values h_k(z), k < count (mercer.py:122-143).  out: n x count. */
 int fagp_hermite(const double* z, int64_t n, int32_t count, double* out, void* stream);
 
-/* Per-dimension eigenfunction table (_phi_1d, mercer.py:276-281) for every row:
- * T[r, d*M + i] = (sqrt_beta_d * exp((-delta2_d * x) * x)) * h_i((rho_d beta_d) * x),
- * x = X[r, d].  X: N x p, T: N x (p*M).  Sets FAGP_FLAG_X_NONFINITE in *flags. */
-int fagp_basis_eval(const double* X, int64_t N, const fagp_basis* basis, double* T,
-                    uint32_t* flags, void* stream);
+/* Table rows.  Row r of a table T (N x W, W = fagp_table_width(p, M)) holds
+ *   [d*M + i]  (sqrt_beta_d * exp((-delta2_d * x) * x)) * h_i((rho_d beta_d) * x), x = X[r, d]
+ *              -- the per-dimension eigenfunctions, _phi_1d (mercer.py:276-281)
+ *   [p*M]      r = y[r] - mean_const (posterior.py:229), 0 when y is NULL
+ *   [p*M + 1]  1.0      [p*M + 2]  0.0      [p*M + 3 .. W)  0.0 (pad to an even width)
+ * so every column of [Phi | r | 0] is a product of p entries of one row. */
+int32_t fagp_table_width(int32_t p, int32_t M);
+
+/* Evaluate the table for every row of X (N x p).  Sets FAGP_FLAG_X_NONFINITE in *flags
+ * (nullable) when an input coordinate is not finite (mercer.py:334-335). */
+int fagp_basis_eval(const double* X, int64_t N, const fagp_basis* basis, const double* y,
+                    double mean_const, double* T, uint32_t* flags, void* stream);
+
+/* Rewrite the residual column of an existing table: T[r, p*M] = y[r] - mean_const. */
+int fagp_set_residual(double* T, int64_t N, const fagp_basis* basis, const double* y, double mean_const,
+                      void* stream);
 
 /* ---- (2) feature matrix ------------------------------------------------------------ */
 /* Materialise Phi (N x m) from the table T (mercer.py:284-292).  Not on the posterior
@@ -110,12 +121,12 @@ int fagp_find_nonfinite(const double* T, int64_t N, const fagp_basis* basis, int
  * returned as the packed upper triangle of the (m+1) x (m+1) matrix, row-major:
  * element (i, j), i <= j, at i*(2(m+1) - i - 1)/2 + j.  Column m holds t = Phi^T r.
  * Phi is never written to HBM.  Deterministic for fixed (N, basis): fixed split-K tree,
- * no floating-point atomics.  T comes from fagp_basis_eval on the same X. */
+ * no floating-point atomics.  T comes from fagp_basis_eval(X, y, mean_const).  Sets
+ * FAGP_FLAG_PHI_NONFINITE when a feature is not finite (detected on the Gram diagonal). */
 int64_t fagp_gram_packed_len(int64_t m);
 size_t fagp_gram_workspace_size(int64_t N, const fagp_basis* basis);
-int fagp_gram(const double* T, const double* y, double mean_const, int64_t N,
-              const fagp_basis* basis, double* gram_ext_packed, void* workspace,
-              size_t workspace_bytes, uint32_t* flags, void* stream);
+int fagp_gram(const double* T, int64_t N, const fagp_basis* basis, double* gram_ext_packed,
+              void* workspace, size_t workspace_bytes, uint32_t* flags, void* stream);
 
 /* ---- (3) Cholesky factorisation and solves ----------------------------------------- */
 /* Scaled system A = (s_i G_ij) s_j + sigma2 I (posterior.py:171-174) from the packed Gram,

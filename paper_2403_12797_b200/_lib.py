@@ -59,12 +59,14 @@ SIGNATURES = {
     "fagp_read_flags": (ctypes.c_int, [_P, _P, _P]),
     "fagp_eigenvalues": (ctypes.c_int, [_BASIS, _D, _P, _P, _P, _P]),
     "fagp_hermite": (ctypes.c_int, [_P, _I64, _I32, _P, _P]),
-    "fagp_basis_eval": (ctypes.c_int, [_P, _I64, _BASIS, _P, _P, _P]),
+    "fagp_table_width": (_I32, [_I32, _I32]),
+    "fagp_basis_eval": (ctypes.c_int, [_P, _I64, _BASIS, _P, _D, _P, _P, _P]),
+    "fagp_set_residual": (ctypes.c_int, [_P, _I64, _BASIS, _P, _D, _P]),
     "fagp_features": (ctypes.c_int, [_P, _I64, _BASIS, _P, _P, _P]),
     "fagp_find_nonfinite": (ctypes.c_int, [_P, _I64, _BASIS, _P, _P]),
     "fagp_gram_packed_len": (_I64, [_I64]),
     "fagp_gram_workspace_size": (_SZ, [_I64, _BASIS]),
-    "fagp_gram": (ctypes.c_int, [_P, _P, _D, _I64, _BASIS, _P, _P, _SZ, _P, _P]),
+    "fagp_gram": (ctypes.c_int, [_P, _I64, _BASIS, _P, _P, _SZ, _P, _P]),
     "fagp_factor_workspace_size": (_SZ, [_I64]),
     "fagp_predict_operand_len": (_I64, [_I64]),
     "fagp_factor": (ctypes.c_int, [_P, _P, _D, _I64, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),

@@ -54,16 +54,18 @@ __global__ void hermite_kernel(const double* __restrict__ z, int64_t n, int coun
   }
 }
 
-// T[r, d*M + i] = phi_{i+1}(X[r, d]) for every row r and dimension d.
+// T[r, d*M + i] = phi_{i+1}(X[r, d]) for every row r and dimension d, followed by the
+// residual r = y - c (0 without y), 1.0 and 0.0 (see table_width in common.cuh).
 // One thread per (row, dim); rows are staged through shared memory so the table rows
 // are written to HBM with coalesced 8-byte stores.
 __global__ void basis_eval_kernel(const double* __restrict__ X, int64_t N, BasisView b,
+                                  const double* __restrict__ y, double mean_const,
                                   double* __restrict__ T, uint32_t* flags, int rows_per_cta) {
   extern __shared__ double sm[];
-  const int M = b.M, p = b.p, pM = p * M;
-  double* c1 = sm;           // [M]
-  double* c2 = sm + M;       // [M]
-  double* stage = sm + 2 * M;  // [rows_per_cta * pM]
+  const int M = b.M, p = b.p, pM = p * M, W = table_width(p, M);
+  double* c1 = sm;             // [M]
+  double* c2 = sm + M;         // [M]
+  double* stage = sm + 2 * M;  // [rows_per_cta * W]
   for (int k = threadIdx.x; k < M; k += blockDim.x) {
     c1[k] = herm_c1(k);
     c2[k] = herm_c2(k);
@@ -80,7 +82,7 @@ __global__ void basis_eval_kernel(const double* __restrict__ X, int64_t N, Basis
     const double zr = __dmul_rn(b.rho_beta()[d], x);
     // sqrt(beta) * exp((-delta2 * x) * x)
     const double env = __dmul_rn(b.sqrt_beta()[d], exp(__dmul_rn(__dmul_rn(b.neg_delta2()[d], x), x)));
-    double* o = stage + rl * pM + d * M;
+    double* o = stage + rl * W + d * M;
     double hm1 = 1.0;
     o[0] = __dmul_rn(env, 1.0);
     if (M > 1) {
@@ -94,10 +96,23 @@ __global__ void basis_eval_kernel(const double* __restrict__ X, int64_t N, Basis
       }
     }
   }
+  for (int rl = threadIdx.x; rl < nrows; rl += blockDim.x) {
+    double* o = stage + rl * W;
+    o[table_col_r(pM)] = y ? __dsub_rn(y[row0 + rl], mean_const) : 0.0;  // r = y - c (posterior.py:229)
+    o[table_col_one(pM)] = 1.0;
+    o[table_col_zero(pM)] = 0.0;
+    for (int c = pM + 3; c < W; ++c) o[c] = 0.0;
+  }
   __syncthreads();
-  double* dst = T + row0 * pM;
-  for (int i = threadIdx.x; i < nrows * pM; i += blockDim.x) dst[i] = stage[i];
+  double* dst = T + row0 * W;
+  for (int i = threadIdx.x; i < nrows * W; i += blockDim.x) dst[i] = stage[i];
   if (bad_x) raise_flag(flags, FAGP_FLAG_X_NONFINITE);
+}
+
+__global__ void set_residual_kernel(double* __restrict__ T, int64_t N, int pM, int W, const double* __restrict__ y,
+                                    double mean_const) {
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < N; r += int64_t(gridDim.x) * blockDim.x)
+    T[r * W + table_col_r(pM)] = y ? __dsub_rn(y[r], mean_const) : 0.0;
 }
 
 // Phi[r, j] = ((T[r, i_0] * T[r, M + i_1]) * T[r, 2M + i_2]) * ...  with j's mixed-radix
@@ -105,14 +120,14 @@ __global__ void basis_eval_kernel(const double* __restrict__ X, int64_t N, Basis
 __global__ void features_kernel(const double* __restrict__ T, int64_t N, BasisView b,
                                 double* __restrict__ phi, uint32_t* flags) {
   const int64_t m = b.m;
-  const int M = b.M, p = b.p, pM = p * M;
+  const int M = b.M, p = b.p, W = table_width(p, M);
   bool bad = false;
   const int64_t total = N * m;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * blockDim.x) {
     const int64_t r = e / m;
     int64_t j = e - r * m;
-    const double* Tr = T + r * pM;
+    const double* Tr = T + r * W;
     // digits from the last (fastest) dimension up
     int dig[FAGP_MAX_P];
     for (int d = p - 1; d >= 0; --d) {
@@ -131,13 +146,13 @@ __global__ void features_kernel(const double* __restrict__ T, int64_t N, BasisVi
 __global__ void find_nonfinite_kernel(const double* __restrict__ T, int64_t N, BasisView b,
                                       unsigned long long* first) {
   const int64_t m = b.m;
-  const int M = b.M, p = b.p, pM = p * M;
+  const int M = b.M, p = b.p, W = table_width(p, M);
   const int64_t total = N * m;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * blockDim.x) {
     const int64_t r = e / m;
     int64_t j = e - r * m;
-    const double* Tr = T + r * pM;
+    const double* Tr = T + r * W;
     int dig[FAGP_MAX_P];
     for (int d = p - 1; d >= 0; --d) {
       dig[d] = int(j % M);
@@ -296,19 +311,36 @@ int fagp_hermite(const double* z, int64_t n, int32_t count, double* out, void* s
   return FAGP_OK;
 }
 
-int fagp_basis_eval(const double* X, int64_t N, const fagp_basis* basis, double* T, uint32_t* flags,
-                    void* stream) {
+int32_t fagp_table_width(int32_t p, int32_t M) { return (p < 1 || M < 1) ? -1 : table_width(p, M); }
+
+int fagp_set_residual(double* T, int64_t N, const fagp_basis* basis, const double* y, double mean_const,
+                      void* stream) {
+  int st = check_basis(basis);
+  if (st) return st;
+  if (N < 0 || (N > 0 && T == nullptr)) return FAGP_EINVAL;
+  if (N == 0) return FAGP_OK;
+  const int pM = basis->p * basis->M;
+  int grid = int(tmin<int64_t>(ceil_div(N, 256), 8 * num_sms()));
+  set_residual_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(T, N, pM, table_width(basis->p, basis->M),
+                                                                          y, mean_const);
+  FAGP_LAUNCH_CHECK();
+  return FAGP_OK;
+}
+
+int fagp_basis_eval(const double* X, int64_t N, const fagp_basis* basis, const double* y, double mean_const,
+                    double* T, uint32_t* flags, void* stream) {
   int st = check_basis(basis);
   if (st) return st;
   if (N < 0 || (N > 0 && (X == nullptr || T == nullptr))) return FAGP_EINVAL;
   if (N == 0) return FAGP_OK;
-  const int64_t pM = int64_t(basis->p) * basis->M;
-  const int rows = int(tmax<int64_t>(1, tmin<int64_t>(64, (96 * 1024) / (pM * 8))));
-  size_t smem = (size_t(2) * basis->M + size_t(rows) * pM) * sizeof(double);
+  const int64_t W = table_width(basis->p, basis->M);
+  const int rows = int(tmax<int64_t>(1, tmin<int64_t>(64, (96 * 1024) / (W * 8))));
+  size_t smem = (size_t(2) * basis->M + size_t(rows) * W) * sizeof(double);
   if (smem > 200 * 1024) return FAGP_EUNSUPPORTED;
   FAGP_CUDA_TRY(cudaFuncSetAttribute(basis_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   int64_t grid = ceil_div(N, rows);
-  basis_eval_kernel<<<unsigned(grid), 256, smem, static_cast<cudaStream_t>(stream)>>>(X, N, view(basis), T, flags, rows);
+  basis_eval_kernel<<<unsigned(grid), 256, smem, static_cast<cudaStream_t>(stream)>>>(X, N, view(basis), y,
+                                                                                     mean_const, T, flags, rows);
   FAGP_LAUNCH_CHECK();
   return FAGP_OK;
 }

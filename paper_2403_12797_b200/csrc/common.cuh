@@ -101,6 +101,13 @@ __host__ __device__ __forceinline__ T tmax(T a, T b) { return a < b ? b : a; }
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
+// Table row layout (fagp_basis_eval): [phi_{d,i} for d < p, i < M | r | 1.0 | 0.0 | pad],
+// width W = round_up(p*M + 3, 2) so every row starts 16-byte aligned (cp.async).
+__host__ __device__ __forceinline__ int table_width(int p, int M) { return (p * M + 3 + 1) & ~1; }
+__host__ __device__ __forceinline__ int table_col_r(int pM) { return pM; }
+__host__ __device__ __forceinline__ int table_col_one(int pM) { return pM + 1; }
+__host__ __device__ __forceinline__ int table_col_zero(int pM) { return pM + 2; }
+
 __device__ __forceinline__ void raise_flag(uint32_t* flags, uint32_t bit) {
   if (flags) atomicOr(flags, bit);
 }

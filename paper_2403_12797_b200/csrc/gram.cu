@@ -4,17 +4,23 @@
 // which numpy routes to DSYRK) and posterior.py:229,233 (`gemm(phi, r, transpose_a=True)`).
 //
 // Data layout
-//   T      (N, p*M)   per-row 1-D eigenfunction table from fagp_basis_eval (HBM, read via L1)
+//   T      (N, W) table rows from fagp_basis_eval: [phi_{d,i}(x_rd) (p*M) | r | 1 | 0 | pad]
 //   ext    Phi_ext = [Phi | r | 0-pad] of width Tt*BT, Tt = ceil((m+1)/BT); never in HBM
 //   ws     split-K partial tiles [S][npairs][BT][BT]  (upper-triangle tile pairs only)
 //   packed (m+1)(m+2)/2 upper triangle of Phi_ext^T Phi_ext, row-major
 //
-// K1 (gram_kernel): one CTA per (tile pair, row chunk).  Each pipeline stage generates
-// BK rows of the two Phi column tiles into shared memory -- Phi[r, j] is the product of p
-// table entries in the reference's broadcast order (mercer.py:287-291) -- and 8 warps
-// contract them with mma.m8n8k4.f64 (64x32 warp tiles, accumulators in registers).
-// Deterministic: each CTA sums its rows in a fixed order and K1b adds the chunk
-// partials in chunk order; no floating-point atomics.
+// Every column of Phi_ext is a product of p table entries of the same row: feature
+// column j multiplies phi_{d, i_d(j)} in the reference's broadcast order
+// (mercer.py:287-291); the residual column multiplies (r, 1, 1, ...) and padding columns
+// (0, 1, 1, ...).  So generation is one branch-free gather-multiply per element.
+//
+// K1 (gram_kernel_fast<P>): one CTA per (upper tile pair, row chunk), 8 warps on 64x32
+// DMMA warp tiles.  The table rows of chunk n+2 arrive by cp.async while the Phi tiles of
+// chunk n+1 are generated into shared memory interleaved with the DMMA k-loop of chunk n,
+// so generation fills issue slots between DMMAs instead of running as a separate phase.
+// K1b (gram_reduce_kernel): sums the split-K partials in chunk order (deterministic, no
+// atomics) and flags a non-finite diagonal (G_jj is non-finite iff a feature of column j
+// is), which keeps the per-element path check-free.
 #include "common.cuh"
 
 namespace fagp {
@@ -27,6 +33,7 @@ constexpr int SP = BT + 4;     // smem row stride in doubles; SP % 16 == 4 -> co
 constexpr int WM = 64, WN = 32;
 constexpr int FM = WM / 8, FN = WN / 8;
 constexpr int STAGE = BK * SP;  // doubles per operand per stage
+constexpr size_t kMaxSmem = 227 * 1024;
 
 struct Plan {
   int Tt;             // tiles per side of the extended matrix
@@ -49,7 +56,6 @@ inline Plan make_plan(int64_t N, int64_t m) {
     const bool enough = ctas >= 2 * sms || S == max_chunks;
     if (enough && eff >= 0.96) {
       best_S = S;
-      best_eff = 2.0;
       break;
     }
     if (eff > best_eff + 1e-9) {
@@ -62,8 +68,6 @@ inline Plan make_plan(int64_t N, int64_t m) {
   return pl;
 }
 
-inline size_t smem_bytes(int p) { return size_t(4) * STAGE * sizeof(double) + size_t(p) * NT * sizeof(int); }
-
 __device__ __forceinline__ void pair_coords(int pair, int Tt, int& ti, int& tj) {
   int t = 0, rem = pair;
   while (rem >= Tt - t) {
@@ -74,11 +78,26 @@ __device__ __forceinline__ void pair_coords(int pair, int Tt, int& ti, int& tj) 
   tj = t + rem;
 }
 
+// Table offset of factor d of extended column `col`: feature digit, residual (r, 1, ...)
+// or zero padding (0, 1, ...).
+__device__ __forceinline__ int col_offset(int64_t col, int64_t m, int M, int pM, int d, int p) {
+  if (col < m) {
+    int64_t q = col;
+    for (int e = p - 1; e > d; --e) q /= M;
+    return d * M + int(q % M);
+  }
+  if (d == 0) return col == m ? table_col_r(pM) : table_col_zero(pM);
+  return table_col_one(pM);
+}
+
+inline size_t fast_smem_bytes(int W) { return size_t(4) * STAGE * sizeof(double) + size_t(2) * BK * W * sizeof(double); }
+
+template <int P>
 __global__ void __launch_bounds__(NT, 1)
-gram_kernel(const double* __restrict__ T, const double* __restrict__ y, double mean_const, int64_t N,
-            BasisView b, Plan pl, double* __restrict__ ws, uint32_t* flags) {
+gram_kernel_fast(const double* __restrict__ T, int64_t N, BasisView b, Plan pl, double* __restrict__ ws) {
   extern __shared__ double sm[];
-  int* col_off = reinterpret_cast<int*>(sm + 4 * STAGE);  // [p][NT], private per thread
+  const int M = b.M, pM = P * M, W = table_width(P, M);
+  double* tbuf = sm + 4 * STAGE;  // [2][BK][W] staged table rows
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int pair = blockIdx.x % pl.npairs;
   const int chunk = blockIdx.x / pl.npairs;
@@ -88,47 +107,41 @@ gram_kernel(const double* __restrict__ T, const double* __restrict__ y, double m
   const int64_t r0 = int64_t(chunk) * pl.chunk_rows;
   const int64_t r1 = tmin<int64_t>(N, r0 + pl.chunk_rows);
   const int64_t m = b.m;
-  const int M = b.M, p = b.p, pM = p * M;
 
-  // ---- generator role: one Phi column per thread (two tiles for off-diagonal pairs) ----
+  // generator role: thread owns one column of one operand tile (gh = 0: tile ti -> buffer
+  // 0, gh = 1: tile tj -> buffer 1; a diagonal pair simply generates its tile twice) and
+  // generates rows 4kk..4kk+3 of the next chunk during DMMA k-step kk
   const int gc = tid % BT, gh = tid / BT;
-  const int gtile = diag ? ti : (gh ? tj : ti);
-  const int64_t gcol = int64_t(gtile) * BT + gc;
-  const int gop = diag ? 0 : gh;
-  const int krow0 = diag ? gh : 0, kstep = diag ? 2 : 1;
-  const int kind = gcol < m ? 0 : (gcol == m ? 1 : 2);  // feature | residual | zero pad
-  if (kind == 0) {
-    int64_t q = gcol;
-    for (int d = p - 1; d >= 0; --d) {
-      col_off[d * NT + tid] = d * M + int(q % M);
-      q /= M;
-    }
-  }
-  bool bad = false;
+  const int64_t gcol = int64_t(gh ? tj : ti) * BT + gc;
+  int off[P];
+#pragma unroll
+  for (int d = 0; d < P; ++d) off[d] = col_offset(gcol, m, M, pM, d, P);
 
-  auto generate = [&](int stage, int64_t base) {
-    double* dst = sm + (stage * 2 + gop) * STAGE + gc;
-#pragma unroll 4
-    for (int k = krow0; k < BK; k += kstep) {
-      const int64_t row = base + k;
-      double v = 0.0;
-      if (row < r1) {
-        if (kind == 0) {
-          const double* Tr = T + row * pM;
-          v = __ldg(Tr + col_off[tid]);
-          for (int d = 1; d < p; ++d) v = __dmul_rn(v, __ldg(Tr + col_off[d * NT + tid]));
-          bad |= not_finite(v);
-        } else if (kind == 1) {
-          v = __dsub_rn(__ldg(y + row), mean_const);
-        }
-      }
+  auto load_tab = [&](int slot, int64_t base) {
+    double* dst = tbuf + slot * (BK * W);
+    const int nrows = int(tmax<int64_t>(0, tmin<int64_t>(BK, r1 - base)));
+    const int nd = nrows * W;  // W is even: 16-byte copies, 16-byte aligned rows
+    const double* src = T + base * W;
+    for (int i = tid; i < nd / 2; i += NT) cp_async_16(dst + 2 * i, src + 2 * i);
+    for (int i = nd + tid; i < BK * W; i += NT) dst[i] = 0.0;  // rows past the chunk end
+    cp_async_commit();
+  };
+  auto gen_rows = [&](int stage, int kk) {
+    double* dst = sm + (stage * 2 + gh) * STAGE + gc;
+    const double* tb = tbuf + stage * (BK * W);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int k = kk * 4 + i;
+      const double* Tr = tb + k * W;
+      double v = Tr[off[0]];
+#pragma unroll
+      for (int d = 1; d < P; ++d) v = __dmul_rn(v, Tr[off[d]]);
       dst[k * SP] = v;
     }
   };
 
-  // ---- consumer role: 2 x 4 warp grid of 64 x 32 tiles ----
   const int wi = warp / 4, wj = warp % 4;
-  const bool active = !diag || (wj * WN + WN - 1 >= wi * WM);  // skip blocks strictly below diag
+  const bool active = !diag || (wj * WN + WN - 1 >= wi * WM);  // blocks strictly below the diagonal idle
   double acc[FM][FN][2];
 #pragma unroll
   for (int s = 0; s < FM; ++s)
@@ -136,13 +149,21 @@ gram_kernel(const double* __restrict__ T, const double* __restrict__ y, double m
     for (int t = 0; t < FN; ++t) acc[s][t][0] = acc[s][t][1] = 0.0;
 
   const int nchunks = int(ceil_div(tmax<int64_t>(r1 - r0, 0), BK));
-  if (nchunks > 0) generate(0, r0);
+  load_tab(0, r0);
+  cp_async_wait<0>();
+  __syncthreads();
+  load_tab(1, r0 + BK);
+#pragma unroll
+  for (int kk = 0; kk < BK / 4; ++kk) gen_rows(0, kk);
+  cp_async_wait<0>();
   __syncthreads();
   for (int n = 0; n < nchunks; ++n) {
-    if (n + 1 < nchunks) generate((n + 1) & 1, r0 + int64_t(n + 1) * BK);
+    const int cur = n & 1, nxt = cur ^ 1;
+    // table slot cur (chunk n) was consumed by the generation of chunk n one iteration ago
+    if (n + 2 < nchunks) load_tab(cur, r0 + int64_t(n + 2) * BK);
+    const double* As = sm + (cur * 2) * STAGE + (lane & 3) * SP + wi * WM + (lane >> 2);
+    const double* Bs = sm + (cur * 2 + 1) * STAGE + (lane & 3) * SP + wj * WN + (lane >> 2);
     if (active) {
-      const double* As = sm + ((n & 1) * 2) * STAGE + (lane & 3) * SP + wi * WM + (lane >> 2);
-      const double* Bs = sm + ((n & 1) * 2 + (diag ? 0 : 1)) * STAGE + (lane & 3) * SP + wj * WN + (lane >> 2);
 #pragma unroll
       for (int kk = 0; kk < BK / 4; ++kk) {
         double a[FM], bb[FN];
@@ -154,8 +175,13 @@ gram_kernel(const double* __restrict__ T, const double* __restrict__ y, double m
         for (int s = 0; s < FM; ++s)
 #pragma unroll
           for (int t = 0; t < FN; ++t) dmma_8x8x4(acc[s][t][0], acc[s][t][1], a[s], bb[t]);
+        gen_rows(nxt, kk);  // chunk n+1 (garbage past the last chunk, never read)
       }
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < BK / 4; ++kk) gen_rows(nxt, kk);
     }
+    cp_async_wait<0>();
     __syncthreads();
   }
 
@@ -171,24 +197,100 @@ gram_kernel(const double* __restrict__ T, const double* __restrict__ y, double m
       }
     }
   }
-  if (bad) raise_flag(flags, FAGP_FLAG_PHI_NONFINITE);
+}
+
+// Generic K1 for shapes outside the fast path (p > 8 or table rows too wide to stage):
+// runtime p, table entries read through L1, one barrier-separated phase per chunk.
+__global__ void __launch_bounds__(NT, 1)
+gram_kernel_generic(const double* __restrict__ T, int64_t N, BasisView b, Plan pl, double* __restrict__ ws) {
+  extern __shared__ double sm[];
+  int* col_off = reinterpret_cast<int*>(sm + 4 * STAGE);  // [p][NT], private per thread
+  const int M = b.M, p = b.p, pM = p * M, W = table_width(p, M);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int pair = blockIdx.x % pl.npairs;
+  const int chunk = blockIdx.x / pl.npairs;
+  int ti, tj;
+  pair_coords(pair, pl.Tt, ti, tj);
+  const bool diag = ti == tj;
+  const int64_t r0 = int64_t(chunk) * pl.chunk_rows;
+  const int64_t r1 = tmin<int64_t>(N, r0 + pl.chunk_rows);
+  const int gc = tid % BT, gh = tid / BT;
+  const int64_t gcol = int64_t(gh ? tj : ti) * BT + gc;
+  for (int d = 0; d < p; ++d) col_off[d * NT + tid] = col_offset(gcol, b.m, M, pM, d, p);
+
+  auto generate = [&](int64_t base) {
+    double* dst = sm + gh * STAGE + gc;
+    for (int k = 0; k < BK; ++k) {
+      const int64_t row = base + k;
+      double v = 0.0;
+      if (row < r1) {
+        const double* Tr = T + row * W;
+        v = __ldg(Tr + col_off[tid]);
+        for (int d = 1; d < p; ++d) v = __dmul_rn(v, __ldg(Tr + col_off[d * NT + tid]));
+      }
+      dst[k * SP] = v;
+    }
+  };
+  const int wi = warp / 4, wj = warp % 4;
+  const bool active = !diag || (wj * WN + WN - 1 >= wi * WM);
+  double acc[FM][FN][2];
+#pragma unroll
+  for (int s = 0; s < FM; ++s)
+#pragma unroll
+    for (int t = 0; t < FN; ++t) acc[s][t][0] = acc[s][t][1] = 0.0;
+  const int nchunks = int(ceil_div(tmax<int64_t>(r1 - r0, 0), BK));
+  for (int n = 0; n < nchunks; ++n) {
+    generate(r0 + int64_t(n) * BK);
+    __syncthreads();
+    if (active) {
+      const double* As = sm + (lane & 3) * SP + wi * WM + (lane >> 2);
+      const double* Bs = sm + STAGE + (lane & 3) * SP + wj * WN + (lane >> 2);
+#pragma unroll
+      for (int kk = 0; kk < BK / 4; ++kk) {
+        double a[FM], bb[FN];
+#pragma unroll
+        for (int s = 0; s < FM; ++s) a[s] = As[kk * 4 * SP + s * 8];
+#pragma unroll
+        for (int t = 0; t < FN; ++t) bb[t] = Bs[kk * 4 * SP + t * 8];
+#pragma unroll
+        for (int s = 0; s < FM; ++s)
+#pragma unroll
+          for (int t = 0; t < FN; ++t) dmma_8x8x4(acc[s][t][0], acc[s][t][1], a[s], bb[t]);
+      }
+    }
+    __syncthreads();
+  }
+  if (active) {
+    double* tile = ws + (size_t(chunk) * pl.npairs + pair) * size_t(BT * BT);
+#pragma unroll
+    for (int s = 0; s < FM; ++s) {
+      const int i = wi * WM + s * 8 + (lane >> 2);
+#pragma unroll
+      for (int t = 0; t < FN; ++t) {
+        const int j = wj * WN + t * 8 + 2 * (lane & 3);
+        *reinterpret_cast<double2*>(tile + i * BT + j) = make_double2(acc[s][t][0], acc[s][t][1]);
+      }
+    }
+  }
 }
 
 // K1b: packed[i, j] = sum_s ws[s][pair(i, j)][i % BT][j % BT] in chunk order.
-__global__ void gram_reduce_kernel(const double* __restrict__ ws, int64_t m, Plan pl,
-                                   double* __restrict__ packed) {
+__global__ void gram_reduce_kernel(const double* __restrict__ ws, int64_t m, Plan pl, double* __restrict__ packed,
+                                   uint32_t* flags) {
   const int64_t me = m + 1;
-  const int64_t i = blockIdx.y;
-  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (j < i || j >= me) return;
-  const int ti = int(i / BT), tj = int(j / BT);
-  const int pair = ti * pl.Tt - ti * (ti - 1) / 2 + (tj - ti);
-  const size_t off = size_t(i % BT) * BT + size_t(j % BT);
-  const size_t stride = size_t(pl.npairs) * BT * BT;
-  const double* src = ws + size_t(pair) * BT * BT + off;
-  double sum = 0.0;
-  for (int s = 0; s < pl.S; ++s) sum += src[s * stride];
-  packed[i * (2 * me - i - 1) / 2 + j] = sum;
+  for (int64_t i = blockIdx.y; i < me; i += gridDim.y) {
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j < i || j >= me) continue;
+    const int ti = int(i / BT), tj = int(j / BT);
+    const int pair = ti * pl.Tt - ti * (ti - 1) / 2 + (tj - ti);
+    const size_t off = size_t(i % BT) * BT + size_t(j % BT);
+    const size_t stride = size_t(pl.npairs) * BT * BT;
+    const double* src = ws + size_t(pair) * BT * BT + off;
+    double sum = 0.0;
+    for (int s = 0; s < pl.S; ++s) sum += src[s * stride];
+    packed[i * (2 * me - i - 1) / 2 + j] = sum;
+    if (i == j && i < m && not_finite(sum)) raise_flag(flags, FAGP_FLAG_PHI_NONFINITE);
+  }
 }
 
 }  // namespace gram
@@ -209,25 +311,46 @@ size_t fagp_gram_workspace_size(int64_t N, const fagp_basis* basis) {
   return size_t(pl.S) * pl.npairs * gram::BT * gram::BT * sizeof(double);
 }
 
-int fagp_gram(const double* T, const double* y, double mean_const, int64_t N, const fagp_basis* basis,
-              double* gram_ext_packed, void* workspace, size_t workspace_bytes, uint32_t* flags,
-              void* stream) {
+int fagp_gram(const double* T, int64_t N, const fagp_basis* basis, double* gram_ext_packed, void* workspace,
+              size_t workspace_bytes, uint32_t* flags, void* stream) {
   int st = check_basis(basis);
   if (st) return st;
-  if (N < 0 || gram_ext_packed == nullptr || (N > 0 && (T == nullptr || y == nullptr))) return FAGP_EINVAL;
+  if (N < 0 || gram_ext_packed == nullptr || (N > 0 && T == nullptr)) return FAGP_EINVAL;
   gram::Plan pl = gram::make_plan(N, basis->m);
   const size_t need = size_t(pl.S) * pl.npairs * gram::BT * gram::BT * sizeof(double);
   if (workspace == nullptr || workspace_bytes < need) return FAGP_EWORKSPACE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const size_t smem = gram::smem_bytes(basis->p);
-  FAGP_CUDA_TRY(cudaFuncSetAttribute(gram::gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  const int W = table_width(basis->p, basis->M);
   double* ws = static_cast<double*>(workspace);
-  gram::gram_kernel<<<unsigned(size_t(pl.S) * pl.npairs), gram::NT, smem, s>>>(T, y, mean_const, N, view(basis), pl,
-                                                                               ws, flags);
+  const unsigned nctas = unsigned(size_t(pl.S) * pl.npairs);
+  const size_t fsmem = gram::fast_smem_bytes(W);
+  if (basis->p <= 8 && fsmem <= gram::kMaxSmem) {
+    auto launch = [&](auto kern) -> int {
+      FAGP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fsmem)));
+      kern<<<nctas, gram::NT, fsmem, s>>>(T, N, view(basis), pl, ws);
+      return FAGP_OK;
+    };
+    int rc;
+    switch (basis->p) {
+      case 1: rc = launch(gram::gram_kernel_fast<1>); break;
+      case 2: rc = launch(gram::gram_kernel_fast<2>); break;
+      case 3: rc = launch(gram::gram_kernel_fast<3>); break;
+      case 4: rc = launch(gram::gram_kernel_fast<4>); break;
+      case 5: rc = launch(gram::gram_kernel_fast<5>); break;
+      case 6: rc = launch(gram::gram_kernel_fast<6>); break;
+      case 7: rc = launch(gram::gram_kernel_fast<7>); break;
+      default: rc = launch(gram::gram_kernel_fast<8>); break;
+    }
+    if (rc) return rc;
+  } else {
+    const size_t gsmem = size_t(4) * gram::STAGE * sizeof(double) + size_t(basis->p) * gram::NT * sizeof(int);
+    FAGP_CUDA_TRY(cudaFuncSetAttribute(gram::gram_kernel_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsmem)));
+    gram::gram_kernel_generic<<<nctas, gram::NT, gsmem, s>>>(T, N, view(basis), pl, ws);
+  }
   FAGP_LAUNCH_CHECK();
   const int64_t me = basis->m + 1;
-  dim3 grid(unsigned(ceil_div(me, 256)), unsigned(me));
-  gram::gram_reduce_kernel<<<grid, 256, 0, s>>>(ws, basis->m, pl, gram_ext_packed);
+  dim3 grid(unsigned(ceil_div(me, 256)), unsigned(tmin<int64_t>(me, 65535)));
+  gram::gram_reduce_kernel<<<grid, 256, 0, s>>>(ws, basis->m, pl, gram_ext_packed, flags);
   FAGP_LAUNCH_CHECK();
   return FAGP_OK;
 }

@@ -37,10 +37,10 @@ class PosteriorEngine:
         self.mean_const = float(mean_const)
         self.group = group
         self.want_var = want_var
-        m, pM = b.m, b.p * b.n
+        m, W = b.m, b.width
         e = lambda *shape: dev.empty(shape, device=self.device)  # noqa: E731
-        self.T = e(self.N, pM)
-        self.Ts = e(self.Ns, pM)
+        self.T = e(self.N, W)
+        self.Ts = e(self.Ns, W)
         self.packed = e(int(L.fagp_gram_packed_len(m)))
         self.gram_ws_bytes = int(L.fagp_gram_workspace_size(self.N, b.ref))
         self.gram_ws = e(max(1, self.gram_ws_bytes // 8))
@@ -64,19 +64,20 @@ class PosteriorEngine:
         return ctypes.c_void_p(self.flags.data_ptr() + 4 * k)
 
     # -- stages (each usable alone, e.g. for per-kernel timing) --------------------------
-    def stage_tables(self, X, Xs, stream=None):
+    def stage_tables(self, X, y, Xs, stream=None):
+        """K0 for train (with the residual column r = y - c) and test rows."""
         L, s, b = _lib.lib(), _lib.stream_handle(stream), self.basis
         if self.N:
-            _lib.check(L.fagp_basis_eval(_lib.ptr(X), self.N, b.ref, _lib.ptr(self.T), self._flag(0), s), "basis_eval")
+            _lib.check(L.fagp_basis_eval(_lib.ptr(X), self.N, b.ref, _lib.ptr(y), self.mean_const, _lib.ptr(self.T),
+                                         self._flag(0), s), "basis_eval")
         if self.Ns:
-            _lib.check(L.fagp_basis_eval(_lib.ptr(Xs), self.Ns, b.ref, _lib.ptr(self.Ts), self._flag(1), s),
+            _lib.check(L.fagp_basis_eval(_lib.ptr(Xs), self.Ns, b.ref, None, 0.0, _lib.ptr(self.Ts), self._flag(1), s),
                        "basis_eval")
 
-    def stage_gram(self, y, stream=None):
+    def stage_gram(self, stream=None):
         L, s, b = _lib.lib(), _lib.stream_handle(stream), self.basis
-        _lib.check(L.fagp_gram(_lib.ptr(self.T), _lib.ptr(y) if self.N else None, self.mean_const, self.N, b.ref,
-                               _lib.ptr(self.packed), _lib.ptr(self.gram_ws), self.gram_ws_bytes, self._flag(0), s),
-                   "gram")
+        _lib.check(L.fagp_gram(_lib.ptr(self.T), self.N, b.ref, _lib.ptr(self.packed), _lib.ptr(self.gram_ws),
+                               self.gram_ws_bytes, self._flag(0), s), "gram")
 
     def stage_reduce(self):
         if self.group is not None:
@@ -109,8 +110,8 @@ class PosteriorEngine:
     def run(self, X, y, Xs, fault_flip=False):
         """One posterior evaluation from device-resident inputs; returns device (mean, var)."""
         self.flags.zero_()
-        self.stage_tables(X, Xs)
-        self.stage_gram(y)
+        self.stage_tables(X, y, Xs)
+        self.stage_gram()
         self.stage_reduce()
         st = self.stage_factor()
         if st != _lib.FAGP_OK:

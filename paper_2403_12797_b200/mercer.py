@@ -155,6 +155,7 @@ class Basis:
         self.p = params.p
         self.m = self.n**self.p
         self.delta2_variant = delta2_variant
+        self.width = int(_lib.load().fagp_table_width(self.p, self.n))  # table row width W
         self.host_table = basis_table(params, n, delta2_variant)
         self.table = dev.to_device(self.host_table, device)
         self.struct = _lib.FagpBasis(self.p, self.n, self.m, self.table.data_ptr())
@@ -187,10 +188,10 @@ def eigenfunction_1d(i, x, params, delta2_variant=DELTA2_RHO_SQUARED):
         raise ValueError("eigenfunction_1d requires finite x")
     basis = Basis(ArdKernelParams((KernelParams1D(params.epsilon, params.rho),)), i, delta2_variant)
     xd = dev.to_device(xh.reshape(-1, 1))
-    T = dev.empty((xd.shape[0], i))
+    T = dev.empty((xd.shape[0], basis.width))
     L = _lib.lib()
-    _lib.check(L.fagp_basis_eval(_lib.ptr(xd), xd.shape[0], basis.ref, _lib.ptr(T), None, _lib.stream_handle()),
-               "eigenfunction_1d")
+    _lib.check(L.fagp_basis_eval(_lib.ptr(xd), xd.shape[0], basis.ref, None, 0.0, _lib.ptr(T), None,
+                                 _lib.stream_handle()), "eigenfunction_1d")
     val = dev.to_host(T[:, i - 1]).reshape(xh.shape)
     return val if val.ndim else float(val)
 
@@ -208,7 +209,7 @@ class EigenSystem:
     n: int
     delta2_variant: str
     X: object  # device tensor (N, p)
-    table: object  # device tensor (N, p*n): per-row 1-D eigenfunction values
+    table: object  # device tensor (N, W): per-row 1-D eigenfunction values (+ r, 1, 0)
     basis: Basis
     floor_rel: float = field(default=LAMBDA_FLOOR_REL, repr=False)
     _phi: np.ndarray | None = field(default=None, repr=False)
@@ -299,11 +300,12 @@ def eigensystem(X, params, n, backend=None, memory_cap=DEFAULT_MEMORY_CAP, delta
     _budget(N, n, p, memory_cap)
     basis = Basis(params, n, delta2_variant, device=Xd.device)
     L = _lib.lib()
-    table = dev.empty((N, p * n))
+    table = dev.empty((N, basis.width))
     flags = dev.zeros((1,), dtype="int32")
     s = _lib.stream_handle()
     if N > 0:
-        _lib.check(L.fagp_basis_eval(_lib.ptr(Xd), N, basis.ref, _lib.ptr(table), _lib.ptr(flags), s), "basis_eval")
+        _lib.check(L.fagp_basis_eval(_lib.ptr(Xd), N, basis.ref, None, 0.0, _lib.ptr(table), _lib.ptr(flags), s),
+                   "basis_eval")
     lam = dev.empty((basis.m,))
     _lib.check(L.fagp_eigenvalues(basis.ref, LAMBDA_FLOOR_REL, _lib.ptr(lam), None, None, s), "eigenvalues")
     if int(dev.to_host(flags)[0]) & _lib.FLAG_X_NONFINITE:

@@ -134,25 +134,27 @@ def _check_y(y, N):
     return yd
 
 
-def _stage_tables(basis, Xd, flag_ptr, s):
+def _stage_tables(basis, Xd, flag_ptr, s, yd=None, mean_const=0.0):
     N = int(Xd.shape[0])
-    T = dev.empty((N, basis.p * basis.n), device=Xd.device)
+    T = dev.empty((N, basis.width), device=Xd.device)
     if N > 0:
-        _lib.check(_lib.lib().fagp_basis_eval(_lib.ptr(Xd), N, basis.ref, _lib.ptr(T), flag_ptr, s), "basis_eval")
+        _lib.check(_lib.lib().fagp_basis_eval(_lib.ptr(Xd), N, basis.ref, _lib.ptr(yd), float(mean_const), _lib.ptr(T),
+                                              flag_ptr, s), "basis_eval")
     return T
 
 
-def gram_packed(basis, T, yd, mean_const, flag_ptr=None, stream=None):
-    """fagp_gram on a staged table: packed upper triangle of [Phi|r]^T[Phi|r] (device)."""
+def gram_packed(basis, T, yd=None, mean_const=0.0, flag_ptr=None, stream=None):
+    """fagp_gram on a table: packed upper triangle of [Phi|r]^T[Phi|r] (device).  The
+    table's residual column is (re)written from ``yd`` first (zero when ``yd`` is None)."""
     L = _lib.lib()
     s = _lib.stream_handle(stream)
     N = int(T.shape[0])
+    if N > 0:
+        _lib.check(L.fagp_set_residual(_lib.ptr(T), N, basis.ref, _lib.ptr(yd), float(mean_const), s), "set_residual")
     packed = dev.empty((int(L.fagp_gram_packed_len(basis.m)),), device=T.device)
     wsz = int(L.fagp_gram_workspace_size(N, basis.ref))
     ws = dev.empty((max(1, wsz // 8),), device=T.device)
-    ydp = _lib.ptr(yd) if N > 0 else None
-    _lib.check(L.fagp_gram(_lib.ptr(T), ydp, float(mean_const), N, basis.ref, _lib.ptr(packed), _lib.ptr(ws),
-                           wsz, flag_ptr, s), "gram")
+    _lib.check(L.fagp_gram(_lib.ptr(T), N, basis.ref, _lib.ptr(packed), _lib.ptr(ws), wsz, flag_ptr, s), "gram")
     return packed
 
 
@@ -383,8 +385,7 @@ class LambdaBarSolve:
         self.form = form
         self.noise_var = float(noise_var)
         self._es = es
-        zeros = dev.zeros((es.N,), device=es.table.device)
-        packed = gram_packed(es.basis, es.table, zeros, 0.0)
+        packed = gram_packed(es.basis, es.table, None, 0.0)
         f, st, piv = factor_packed(es.basis, packed, noise_var, 0.0, es.N, keep_gram=True)
         self._fit = f
         self._gram = f.G

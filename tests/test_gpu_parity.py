@@ -185,7 +185,7 @@ def test_eigenfunction_kats_on_device():
 
 
 @pytest.mark.parametrize("p,M,N,Ns", [(1, 1, 5, 3), (1, 7, 33, 129), (2, 3, 200, 257), (3, 4, 1000, 130),
-                                      (6, 2, 500, 64), (1, 130, 2000, 50)])
+                                      (6, 2, 500, 64), (1, 130, 2000, 50), (1, 200, 1500, 70)])
 def test_ragged_shapes_against_oracle(p, M, N, Ns):
     rng = np.random.default_rng(p * 1000 + M)
     X = rng.uniform(-1, 1, (N, p))
