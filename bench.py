@@ -64,7 +64,7 @@ def useful_flops(N, Ns, m):
 def launches_per_step(m):
     """Kernels of ours launched by one PosteriorEngine.run() (no jitter retry)."""
     nblk = -(-m // 32)
-    potrf = nblk + 2 * (nblk - 1)
+    potrf = nblk + (nblk - 1)  # fused diag+panel kernel per step, trailing GEMM between steps
     mp = 32
     while mp < m:
         mp *= 2
@@ -74,7 +74,7 @@ def launches_per_step(m):
         levels += 1
         h *= 2
     trtri = 1 + 1 + 2 * levels  # pad, diag_inv, 2 GEMMs per level
-    factor = 1 + 1 + potrf + 1 + 1 + 2 + 1 + trtri + 1  # build G/t, build A, potrf, zero, vec, trsv x2, vec, trtri, op
+    factor = 1 + 1 + potrf + 1 + trtri + 2 + 1  # build G/t, build A, potrf, zero upper, trtri, w GEMVs x2, operand
     return 2 + 2 + factor + 1  # basis_eval x2, gram + reduce, factor, predict
 
 

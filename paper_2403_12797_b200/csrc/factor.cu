@@ -153,62 +153,122 @@ __device__ __forceinline__ void warp_trinv(const double (*S)[33], double (*Xs)[3
   }
 }
 
-// Diagonal step of the blocked Cholesky: factor A[k0:k0+nb, k0:k0+nb] (lower) in place and
-// write inv(L11) (32x32, identity-padded) to Dinv.  Breakdown (pivot <= 0 or NaN, as in
-// LAPACK dpotrf2) records the 1-based global index in *info and stops.
-__global__ void chol_diag_kernel(double* A, int64_t lda, int64_t k0, int nb, int* info, double* Dinv) {
+// One step of the blocked right-looking Cholesky (NB = 32), one warp per CTA.  Every CTA
+// factors the 32x32 diagonal block A[k0:k0+nb, k0:k0+nb] redundantly in registers (lane i
+// holds row i; column j's multipliers are broadcast with shuffles), which costs ~1 us and
+// saves a launch + a grid-wide dependency.  CTA 0 writes L11; CTA b >= 1 solves panel
+// row-block b-1, L21 = A21 L11^{-T}, by forward substitution against L11 in shared memory.
+// A breakdown (pivot <= 0 or NaN, as LAPACK dpotrf2 tests it) records the 1-based global
+// column in *info; every later kernel then exits immediately.
+__global__ void __launch_bounds__(32) chol_panel_kernel(double* __restrict__ A, int64_t lda, int64_t m, int64_t k0,
+                                                        int nb, int* info) {
   if (*info) return;
-  __shared__ double S[32][33];
-  __shared__ double Xs[32][33];
+  __shared__ double Ls[32][33];
   const int lane = threadIdx.x;
-  for (int r = 0; r < 32; ++r)
-    S[r][lane] = (r < nb && lane < nb) ? A[(k0 + r) * lda + k0 + lane] : (r == lane ? 1.0 : 0.0);
-  __syncwarp();
-  for (int j = 0; j < nb; ++j) {
-    const double d = S[j][j];
-    if (!(d > 0.0)) {
-      if (lane == 0) atomicCAS(info, 0, int(k0 + j + 1));
+  double r[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c)
+    r[c] = (lane < nb && c < nb) ? (c <= lane ? A[(k0 + lane) * lda + k0 + c] : 0.0) : (lane == c ? 1.0 : 0.0);
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const double d = __shfl_sync(0xffffffffu, r[j], j);
+    if (!(d > 0.0)) {  // warp-uniform; padding pivots are exactly 1
+      if (blockIdx.x == 0 && lane == 0) atomicCAS(info, 0, int(k0 + j + 1));
       return;
     }
     const double ljj = sqrt(d);
-    __syncwarp();
-    if (lane == j) S[j][j] = ljj;
-    if (lane > j) S[lane][j] = S[lane][j] / ljj;
-    __syncwarp();
-    if (lane > j && lane < nb) {
-      const double lij = S[lane][j];
-      for (int l = j + 1; l <= lane; ++l) S[lane][l] -= lij * S[l][j];
+    if (lane == j) r[j] = ljj;
+    else if (lane > j) r[j] = r[j] / ljj;
+#pragma unroll
+    for (int k = j + 1; k < 32; ++k) {
+      const double lkj = __shfl_sync(0xffffffffu, r[j], k);
+      if (lane >= k) r[k] = fma(-r[j], lkj, r[k]);
     }
-    __syncwarp();
   }
-  for (int r = 0; r < nb; ++r)
-    if (lane <= r && lane < nb) A[(k0 + r) * lda + k0 + lane] = S[r][lane];
-  // zero the strictly upper entries of S beyond the factor (they still hold A values)
-  for (int r = 0; r < 32; ++r)
-    if (lane > r) S[r][lane] = 0.0;
+  if (blockIdx.x == 0) {
+    if (lane < nb) {
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        if (c <= lane && c < nb) A[(k0 + lane) * lda + k0 + c] = r[c];
+    }
+    return;
+  }
+#pragma unroll
+  for (int c = 0; c < 32; ++c) Ls[lane][c] = r[c];
   __syncwarp();
-  warp_trinv(S, Xs, lane);
-  __syncwarp();
-  for (int r = 0; r < 32; ++r) Dinv[r * 32 + lane] = Xs[r][lane];
+  const int64_t i0 = k0 + nb + int64_t(blockIdx.x - 1) * 32 + lane;
+  if (i0 >= m) return;
+  double* row = A + i0 * lda + k0;
+  double x[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) x[c] = c < nb ? row[c] : 0.0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    double v0 = x[j], v1 = 0.0;  // two partial sums shorten the dependency chain
+#pragma unroll
+    for (int l = 0; l < j; ++l) {
+      if (l & 1) v1 = fma(-x[l], Ls[j][l], v1);
+      else v0 = fma(-x[l], Ls[j][l], v0);
+    }
+    x[j] = (v0 + v1) / Ls[j][j];
+  }
+#pragma unroll
+  for (int c = 0; c < 32; ++c)
+    if (c < nb) row[c] = x[c];
 }
 
-int potrf_blocked(double* A, int64_t m, int64_t lda, int* info, double* Dinv, cudaStream_t s) {
+int potrf_blocked(double* A, int64_t m, int64_t lda, int* info, cudaStream_t s) {
   for (int64_t k0 = 0; k0 < m; k0 += 32) {
     const int nb = int(tmin<int64_t>(32, m - k0));
-    chol_diag_kernel<<<1, 32, 0, s>>>(A, lda, k0, nb, info, Dinv);
-    FAGP_LAUNCH_CHECK();
     const int64_t rest = m - k0 - nb;
+    chol_panel_kernel<<<unsigned(1 + ceil_div(rest, 32)), 32, 0, s>>>(A, lda, m, k0, nb, info);
+    FAGP_LAUNCH_CHECK();
     if (rest <= 0) break;
     double* A21 = A + (k0 + nb) * lda + k0;
-    GemmArgs pan{int(rest), nb, nb, 1.0, 0.0, A21, lda, 0, Dinv, 32, 0, A21, lda, 0, 0, info};
-    int st = gemm(true, pan, 1, s);
-    if (st) return st;
     double* A22 = A + (k0 + nb) * lda + (k0 + nb);
     GemmArgs upd{int(rest), int(rest), nb, -1.0, 1.0, A21, lda, 0, A21, lda, 0, A22, lda, 0, 1, info};
-    st = gemm(true, upd, 1, s);
+    int st = gemm(true, upd, 1, s);
     if (st) return st;
   }
   return FAGP_OK;
+}
+
+// w = V^T (V t), V = L^{-1} diag(s) taken from the TRTRI result X = L^{-1} (row stride mp):
+// w = S L^{-T} L^{-1} S t = s * A^{-1}(s * t)  (posterior.py:233-235), as two parallel
+// GEMVs instead of two sequential triangular solves.  Both use fixed summation orders.
+// y_k = sum_{j<=k} (X[k,j] s_j) t_j: one warp per row k, lanes stride over j.
+__global__ void vt_rows_kernel(const double* __restrict__ X, int64_t mp, const double* __restrict__ s,
+                               const double* __restrict__ t, int64_t m, double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k = int64_t(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (k >= m) return;
+  const double* Xk = X + k * mp;
+  double acc = 0.0;
+  for (int64_t j = lane; j <= k; j += 32) acc = fma(__dmul_rn(Xk[j], s[j]), t[j], acc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) y[k] = acc;
+}
+
+// w_j = sum_{k>=j} (X[k,j] s_j) y_k: 32 columns per CTA, 8 k-slices reduced in fixed order.
+__global__ void vt_cols_kernel(const double* __restrict__ X, int64_t mp, const double* __restrict__ s,
+                               const double* __restrict__ y, int64_t m, double* __restrict__ w) {
+  __shared__ double part[8][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int64_t j = int64_t(blockIdx.x) * 32 + tx;
+  double acc = 0.0;
+  if (j < m) {
+    const double sj = s[j];
+    for (int64_t k = j + ty; k < m; k += 8) acc = fma(__dmul_rn(X[k * mp + j], sj), y[k], acc);
+  }
+  part[ty][tx] = acc;
+  __syncthreads();
+  if (ty == 0 && j < m) {
+    double tot = part[0][tx];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) tot += part[q][tx];
+    w[j] = tot;
+  }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -542,9 +602,8 @@ int fagp_potrf(double* A, int64_t m, int32_t* info_dev, void* workspace, size_t 
   if (A == nullptr || m < 1 || info_dev == nullptr) return FAGP_EINVAL;
   if (workspace == nullptr || workspace_bytes < potrf_ws_bytes()) return FAGP_EWORKSPACE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  double* Dinv = reinterpret_cast<double*>(static_cast<char*>(workspace) + align256(sizeof(int)));
   FAGP_CUDA_TRY(cudaMemsetAsync(info_dev, 0, sizeof(int32_t), s));
-  return potrf_blocked(A, m, m, reinterpret_cast<int*>(info_dev), Dinv, s);
+  return potrf_blocked(A, m, m, reinterpret_cast<int*>(info_dev), s);
 }
 
 int fagp_potrs(const double* L, int64_t m, double* B, int64_t nrhs, void* stream) {
@@ -642,7 +701,7 @@ int fagp_factor(const double* packed, const double* sqrt_lam, double sigma2, int
     system_build_kernel<<<grid, 256, 0, s>>>(packed, sqrt_lam, sigma2, jit, m, L, nullptr, nullptr);
     FAGP_LAUNCH_CHECK();
     FAGP_CUDA_TRY(cudaMemsetAsync(ws.info, 0, sizeof(int), s));
-    int rc = potrf_blocked(L, m, m, ws.info, ws.Dinv, s);
+    int rc = potrf_blocked(L, m, m, ws.info, s);
     if (rc) return rc;
     FAGP_CUDA_TRY(cudaMemcpyAsync(&info_h, ws.info, sizeof(int), cudaMemcpyDeviceToHost, s));
     FAGP_CUDA_TRY(cudaStreamSynchronize(s));
@@ -655,22 +714,20 @@ int fagp_factor(const double* packed, const double* sqrt_lam, double sigma2, int
   }
   zero_upper_kernel<<<grid, 256, 0, s>>>(L, m);
   FAGP_LAUNCH_CHECK();
-  // w = s * A^{-1} (s * t)
-  const int vgrid = int(ceil_div(m, 256));
-  vec_mul_kernel<<<vgrid, 256, 0, s>>>(sqrt_lam, t, ws.vec, m);
-  FAGP_LAUNCH_CHECK();
-  trsv_lower_kernel<<<1, TS_NT, 0, s>>>(L, m, m, ws.vec, 1);
-  FAGP_LAUNCH_CHECK();
-  trsv_lower_trans_kernel<<<1, TS_NT, 0, s>>>(L, m, m, ws.vec, 1);
-  FAGP_LAUNCH_CHECK();
-  vec_mul_kernel<<<vgrid, 256, 0, s>>>(sqrt_lam, ws.vec, w, m);
-  FAGP_LAUNCH_CHECK();
-  if (predict_op) {
+  // V = L^{-1} diag(s) by TRTRI, then w = V^T (V t) = s * A^{-1}(s * t) and the predict operand
+  {
     int rc = trtri_padded(L, m, ws.Lp, ws.X, ws.Tmp, s);
     if (rc) return rc;
+  }
+  const int64_t mp = trtri_dim(m);
+  vt_rows_kernel<<<unsigned(ceil_div(m, 8)), 256, 0, s>>>(ws.X, mp, sqrt_lam, t, m, ws.vec);
+  FAGP_LAUNCH_CHECK();
+  vt_cols_kernel<<<unsigned(ceil_div(m, 32)), dim3(32, 8), 0, s>>>(ws.X, mp, sqrt_lam, ws.vec, m, w);
+  FAGP_LAUNCH_CHECK();
+  if (predict_op) {
     const int64_t pr = op_rows(m), pc = op_cols(m);
     dim3 g2(unsigned(ceil_div(pc, 32)), unsigned(ceil_div(pr, 32)));
-    predict_operand_kernel<<<g2, dim3(32, 8), 0, s>>>(ws.X, trtri_dim(m), sqrt_lam, w, m, predict_op, pr, pc);
+    predict_operand_kernel<<<g2, dim3(32, 8), 0, s>>>(ws.X, mp, sqrt_lam, w, m, predict_op, pr, pc);
     FAGP_LAUNCH_CHECK();
   }
   return FAGP_OK;

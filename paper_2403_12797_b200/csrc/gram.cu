@@ -21,39 +21,55 @@
 // K1b (gram_reduce_kernel): sums the split-K partials in chunk order (deterministic, no
 // atomics) and flags a non-finite diagonal (G_jj is non-finite iff a feature of column j
 // is), which keeps the per-element path check-free.
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 
 namespace fagp {
 namespace gram {
 
-constexpr int BT = 128;        // output tile edge
-constexpr int BK = 32;         // rows per pipeline stage
-constexpr int NT = 256;        // threads per CTA (8 warps)
-constexpr int SP = BT + 4;     // smem row stride in doubles; SP % 16 == 4 -> conflict-free fragments
-constexpr int WM = 64, WN = 32;
-constexpr int FM = WM / 8, FN = WN / 8;
-constexpr int STAGE = BK * SP;  // doubles per operand per stage
+constexpr int BK = 32;         // rows per pipeline stage (large / generic kernels)
 constexpr size_t kMaxSmem = 227 * 1024;
 
+// Tile configuration of the fast kernel: output tile BT x BT, warp grid WGM x WGN, NT = 2 BT
+// threads (one generated Phi column per thread), MINB CTAs per SM.
+template <int BT_, int WGM_, int WGN_, int MINB_, int BK_>
+struct Cfg {
+  static constexpr int BT = BT_, WGM = WGM_, WGN = WGN_, MINB = MINB_, BKC = BK_;
+  static constexpr int NT = 32 * WGM * WGN;
+  static constexpr int SP = BT + 4;  // SP % 16 == 4 -> conflict-free DMMA fragment loads
+  static constexpr int WM = BT / WGM, WN = BT / WGN, FM = WM / 8, FN = WN / 8;
+  static constexpr int STAGE = BKC * SP;  // doubles per operand per stage
+  static_assert(NT == 2 * BT, "one generated column per thread");
+  static_assert(SP % 16 == 4, "fragment bank mapping");
+};
+using CfgSmall = Cfg<64, 2, 2, 4, 16>;    // 64x64 tiles, 4 warps of 32x32, 16-row stages, 4 CTAs/SM
+using CfgLarge = Cfg<128, 2, 4, 1, 32>;   // 128x128 tiles, 8 warps of 64x32, 32-row stages, 1 CTA/SM
+
 struct Plan {
+  int BT;             // tile edge
+  int bk;             // rows per pipeline stage
   int Tt;             // tiles per side of the extended matrix
   int npairs;         // Tt (Tt + 1) / 2
   int S;              // row chunks (split-K)
   int64_t chunk_rows; // rows per chunk (multiple of BK)
 };
 
-inline Plan make_plan(int64_t N, int64_t m) {
+inline Plan make_plan(int64_t N, int64_t m, int BT, int ctas_per_sm, int bk) {
   Plan pl;
+  pl.BT = BT;
+  pl.bk = bk;
   pl.Tt = int(ceil_div(m + 1, BT));
   pl.npairs = pl.Tt * (pl.Tt + 1) / 2;
-  const int64_t max_chunks = tmax<int64_t>(1, ceil_div(N, BK));
-  const int sms = num_sms();
+  const int64_t max_chunks = tmax<int64_t>(1, ceil_div(N, bk));
+  const int64_t slots = int64_t(num_sms()) * ctas_per_sm;
   int64_t best_S = 1;
   double best_eff = -1.0;
   for (int64_t S = 1; S <= tmin<int64_t>(max_chunks, 4096); ++S) {
     const int64_t ctas = S * pl.npairs;
-    const double eff = double(ctas) / double(ceil_div(ctas, sms) * sms);
-    const bool enough = ctas >= 2 * sms || S == max_chunks;
+    const double eff = double(ctas) / double(ceil_div(ctas, slots) * slots);
+    const bool enough = ctas >= 2 * slots || S == max_chunks;
     if (enough && eff >= 0.96) {
       best_S = S;
       break;
@@ -63,7 +79,7 @@ inline Plan make_plan(int64_t N, int64_t m) {
       best_S = S;
     }
   }
-  pl.chunk_rows = round_up(tmax<int64_t>(1, ceil_div(tmax<int64_t>(N, 1), best_S)), BK);
+  pl.chunk_rows = round_up(tmax<int64_t>(1, ceil_div(tmax<int64_t>(N, 1), best_S)), bk);
   pl.S = int(tmax<int64_t>(1, ceil_div(N, pl.chunk_rows)));
   return pl;
 }
@@ -90,11 +106,16 @@ __device__ __forceinline__ int col_offset(int64_t col, int64_t m, int M, int pM,
   return table_col_one(pM);
 }
 
-inline size_t fast_smem_bytes(int W) { return size_t(4) * STAGE * sizeof(double) + size_t(2) * BK * W * sizeof(double); }
+template <class C>
+inline size_t fast_smem_bytes(int W) {
+  return size_t(4) * C::STAGE * sizeof(double) + size_t(2) * C::BKC * W * sizeof(double);
+}
 
-template <int P>
-__global__ void __launch_bounds__(NT, 1)
+template <int P, class C>
+__global__ void __launch_bounds__(C::NT, C::MINB)
 gram_kernel_fast(const double* __restrict__ T, int64_t N, BasisView b, Plan pl, double* __restrict__ ws) {
+  constexpr int BT = C::BT, NT = C::NT, SP = C::SP, STAGE = C::STAGE;
+  constexpr int WM = C::WM, WN = C::WN, FM = C::FM, FN = C::FN, BK = C::BKC;
   extern __shared__ double sm[];
   const int M = b.M, pM = P * M, W = table_width(P, M);
   double* tbuf = sm + 4 * STAGE;  // [2][BK][W] staged table rows
@@ -140,7 +161,7 @@ gram_kernel_fast(const double* __restrict__ T, int64_t N, BasisView b, Plan pl, 
     }
   };
 
-  const int wi = warp / 4, wj = warp % 4;
+  const int wi = warp / C::WGN, wj = warp % C::WGN;
   const bool active = !diag || (wj * WN + WN - 1 >= wi * WM);  // blocks strictly below the diagonal idle
   double acc[FM][FN][2];
 #pragma unroll
@@ -201,8 +222,11 @@ gram_kernel_fast(const double* __restrict__ T, int64_t N, BasisView b, Plan pl, 
 
 // Generic K1 for shapes outside the fast path (p > 8 or table rows too wide to stage):
 // runtime p, table entries read through L1, one barrier-separated phase per chunk.
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(CfgLarge::NT, 1)
 gram_kernel_generic(const double* __restrict__ T, int64_t N, BasisView b, Plan pl, double* __restrict__ ws) {
+  using C = CfgLarge;
+  constexpr int BT = C::BT, NT = C::NT, SP = C::SP, STAGE = C::STAGE;
+  constexpr int WM = C::WM, WN = C::WN, FM = C::FM, FN = C::FN;
   extern __shared__ double sm[];
   int* col_off = reinterpret_cast<int*>(sm + 4 * STAGE);  // [p][NT], private per thread
   const int M = b.M, p = b.p, pM = p * M, W = table_width(p, M);
@@ -278,6 +302,7 @@ gram_kernel_generic(const double* __restrict__ T, int64_t N, BasisView b, Plan p
 __global__ void gram_reduce_kernel(const double* __restrict__ ws, int64_t m, Plan pl, double* __restrict__ packed,
                                    uint32_t* flags) {
   const int64_t me = m + 1;
+  const int BT = pl.BT;
   for (int64_t i = blockIdx.y; i < me; i += gridDim.y) {
     const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j < i || j >= me) continue;
@@ -298,6 +323,48 @@ __global__ void gram_reduce_kernel(const double* __restrict__ ws, int64_t m, Pla
 
 using namespace fagp;
 
+namespace fagp {
+namespace gram {
+// Which kernel runs for a basis; the workspace size depends on it.
+struct Choice {
+  bool fast;
+  bool small;  // CfgSmall (else CfgLarge)
+  Plan plan;
+};
+inline Choice choose(int64_t N, const fagp_basis* b) {
+  const int W = table_width(b->p, b->M);
+  Choice c{};
+  c.fast = b->p <= 8 && fast_smem_bytes<CfgLarge>(W) <= kMaxSmem;
+  const char* cfg = getenv("FAGP_GRAM_CFG");  // tuning override: "large" | "small"
+  c.small = c.fast && fast_smem_bytes<CfgSmall>(W) * CfgSmall::MINB <= 228 * 1024 - CfgSmall::MINB * 1024 &&
+            !(cfg && strcmp(cfg, "large") == 0);
+  c.plan = c.small ? make_plan(N, b->m, CfgSmall::BT, CfgSmall::MINB, CfgSmall::BKC)
+                    : make_plan(N, b->m, CfgLarge::BT, 1, CfgLarge::BKC);
+  return c;
+}
+template <int P, class C>
+int launch_fast(const double* T, int64_t N, const fagp_basis* basis, const Plan& pl, double* ws, cudaStream_t s) {
+  const size_t smem = fast_smem_bytes<C>(table_width(basis->p, basis->M));
+  FAGP_CUDA_TRY(cudaFuncSetAttribute(gram_kernel_fast<P, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  gram_kernel_fast<P, C><<<unsigned(size_t(pl.S) * pl.npairs), C::NT, smem, s>>>(T, N, view(basis), pl, ws);
+  return FAGP_OK;
+}
+template <class C>
+int dispatch_fast(const double* T, int64_t N, const fagp_basis* basis, const Plan& pl, double* ws, cudaStream_t s) {
+  switch (basis->p) {
+    case 1: return launch_fast<1, C>(T, N, basis, pl, ws, s);
+    case 2: return launch_fast<2, C>(T, N, basis, pl, ws, s);
+    case 3: return launch_fast<3, C>(T, N, basis, pl, ws, s);
+    case 4: return launch_fast<4, C>(T, N, basis, pl, ws, s);
+    case 5: return launch_fast<5, C>(T, N, basis, pl, ws, s);
+    case 6: return launch_fast<6, C>(T, N, basis, pl, ws, s);
+    case 7: return launch_fast<7, C>(T, N, basis, pl, ws, s);
+    default: return launch_fast<8, C>(T, N, basis, pl, ws, s);
+  }
+}
+}  // namespace gram
+}  // namespace fagp
+
 extern "C" {
 
 int64_t fagp_gram_packed_len(int64_t m) {
@@ -307,8 +374,8 @@ int64_t fagp_gram_packed_len(int64_t m) {
 
 size_t fagp_gram_workspace_size(int64_t N, const fagp_basis* basis) {
   if (check_basis(basis) != FAGP_OK || N < 0) return 0;
-  gram::Plan pl = gram::make_plan(N, basis->m);
-  return size_t(pl.S) * pl.npairs * gram::BT * gram::BT * sizeof(double);
+  const gram::Plan pl = gram::choose(N, basis).plan;
+  return size_t(pl.S) * pl.npairs * pl.BT * pl.BT * sizeof(double);
 }
 
 int fagp_gram(const double* T, int64_t N, const fagp_basis* basis, double* gram_ext_packed, void* workspace,
@@ -316,37 +383,22 @@ int fagp_gram(const double* T, int64_t N, const fagp_basis* basis, double* gram_
   int st = check_basis(basis);
   if (st) return st;
   if (N < 0 || gram_ext_packed == nullptr || (N > 0 && T == nullptr)) return FAGP_EINVAL;
-  gram::Plan pl = gram::make_plan(N, basis->m);
-  const size_t need = size_t(pl.S) * pl.npairs * gram::BT * gram::BT * sizeof(double);
+  const gram::Choice ch = gram::choose(N, basis);
+  const gram::Plan pl = ch.plan;
+  const size_t need = size_t(pl.S) * pl.npairs * pl.BT * pl.BT * sizeof(double);
   if (workspace == nullptr || workspace_bytes < need) return FAGP_EWORKSPACE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int W = table_width(basis->p, basis->M);
   double* ws = static_cast<double*>(workspace);
-  const unsigned nctas = unsigned(size_t(pl.S) * pl.npairs);
-  const size_t fsmem = gram::fast_smem_bytes(W);
-  if (basis->p <= 8 && fsmem <= gram::kMaxSmem) {
-    auto launch = [&](auto kern) -> int {
-      FAGP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fsmem)));
-      kern<<<nctas, gram::NT, fsmem, s>>>(T, N, view(basis), pl, ws);
-      return FAGP_OK;
-    };
-    int rc;
-    switch (basis->p) {
-      case 1: rc = launch(gram::gram_kernel_fast<1>); break;
-      case 2: rc = launch(gram::gram_kernel_fast<2>); break;
-      case 3: rc = launch(gram::gram_kernel_fast<3>); break;
-      case 4: rc = launch(gram::gram_kernel_fast<4>); break;
-      case 5: rc = launch(gram::gram_kernel_fast<5>); break;
-      case 6: rc = launch(gram::gram_kernel_fast<6>); break;
-      case 7: rc = launch(gram::gram_kernel_fast<7>); break;
-      default: rc = launch(gram::gram_kernel_fast<8>); break;
-    }
-    if (rc) return rc;
+  int rc = FAGP_OK;
+  if (ch.fast) {
+    rc = ch.small ? gram::dispatch_fast<gram::CfgSmall>(T, N, basis, pl, ws, s)
+                  : gram::dispatch_fast<gram::CfgLarge>(T, N, basis, pl, ws, s);
   } else {
-    const size_t gsmem = size_t(4) * gram::STAGE * sizeof(double) + size_t(basis->p) * gram::NT * sizeof(int);
+    const size_t gsmem = size_t(4) * gram::CfgLarge::STAGE * sizeof(double) + size_t(basis->p) * gram::CfgLarge::NT * sizeof(int);
     FAGP_CUDA_TRY(cudaFuncSetAttribute(gram::gram_kernel_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsmem)));
-    gram::gram_kernel_generic<<<nctas, gram::NT, gsmem, s>>>(T, N, view(basis), pl, ws);
+    gram::gram_kernel_generic<<<unsigned(size_t(pl.S) * pl.npairs), gram::CfgLarge::NT, gsmem, s>>>(T, N, view(basis), pl, ws);
   }
+  if (rc) return rc;
   FAGP_LAUNCH_CHECK();
   const int64_t me = basis->m + 1;
   dim3 grid(unsigned(ceil_div(me, 256)), unsigned(tmin<int64_t>(me, 65535)));

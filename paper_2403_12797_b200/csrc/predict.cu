@@ -15,20 +15,39 @@
 // per-row registers; the final lane/warp reduction is in a fixed order (deterministic,
 // no atomics) and each row's mean and var are single coalesced 8-byte stores.  A
 // non-finite phi*_i shows up as a non-finite mean_i / var_i and raises the flag.
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 
 namespace fagp {
 namespace pred {
 
-constexpr int BM = 128, BN = 128, BK = 32, NT = 256;
-constexpr int ASP = BK + 4;  // 36 % 16 == 4
-constexpr int BSP = BN + 4;  // 132 % 16 == 4
-constexpr int WM = 64, WN = 32, FM = WM / 8, FN = WN / 8;
-constexpr int A_STAGE = BM * ASP, B_STAGE = BK * BSP;
+constexpr int BK = 32;  // K rows per step (the predict operand's rows are padded to 32)
 constexpr int OP_COL_ALIGN = 128;
-constexpr size_t BASE_SMEM = size_t(2) * (A_STAGE + B_STAGE) * sizeof(double) + size_t(4) * BM * sizeof(double);
 constexpr size_t kMaxSmem = 227 * 1024;
-inline size_t fast_smem_bytes(int W) { return BASE_SMEM + size_t(BM) * W * sizeof(double); }
+
+// Tile configuration: BM test rows x BN output columns per step, warp grid WGM x WGN.
+template <int BM_, int BN_, int WGM_, int WGN_, int MINB_>
+struct Cfg {
+  static constexpr int BM = BM_, BN = BN_, WGM = WGM_, WGN = WGN_, MINB = MINB_;
+  static constexpr int NT = 32 * WGM * WGN;
+  static constexpr int ASP = BK + 4;  // 36 % 16 == 4
+  static constexpr int BSP = BN + 4;  // % 16 == 4
+  static constexpr int WM = BM / WGM, WN = BN / WGN, FM = WM / 8, FN = WN / 8;
+  static constexpr int A_STAGE = BM * ASP, B_STAGE = BK * BSP;
+  static constexpr int GROWS = NT / BK;             // generator row groups
+  static constexpr int GPER = BM * BK / NT;         // generated elements per thread per step
+  static constexpr int GPERKK = GPER / (BK / 4);    // ... per DMMA k-step
+  static constexpr size_t BASE_SMEM = size_t(2) * (A_STAGE + B_STAGE) * sizeof(double) + size_t(WGN) * BM * sizeof(double);
+  static_assert(BSP % 16 == 4 && ASP % 16 == 4, "fragment bank mapping");
+  static_assert(GPERKK * (BK / 4) == GPER, "generation split");
+};
+using CfgSmall = Cfg<64, 64, 2, 2, 2>;     // 4 warps of 32x32, 2 CTAs/SM (default)
+using CfgLarge = Cfg<128, 128, 2, 4, 1>;   // 8 warps of 64x32, 1 CTA/SM
+
+template <class C>
+inline size_t fast_smem_bytes(int W) { return C::BASE_SMEM + size_t(C::BM) * W * sizeof(double); }
 
 // Digit offsets of K column j for factor d (feature), or the zero entry for j >= m.
 __device__ __forceinline__ int kcol_offset(int64_t j, int64_t m, int M, int pM, int d, int p) {
@@ -41,33 +60,35 @@ __device__ __forceinline__ int kcol_offset(int64_t j, int64_t m, int M, int pM, 
 }
 
 // fold column tile c0 of the accumulators into the per-row sums / mean registers
-__device__ __forceinline__ void fold_tile(const double (&acc)[FM][FN][2], double (&vsum)[FM], double (&mval)[FM],
-                                          int64_t c0, int64_t m, int wj, int lane) {
+template <class C>
+__device__ __forceinline__ void fold_tile(const double (&acc)[C::FM][C::FN][2], double (&vsum)[C::FM],
+                                          double (&mval)[C::FM], int64_t c0, int64_t m, int wj, int lane) {
 #pragma unroll
-  for (int t = 0; t < FN; ++t) {
+  for (int t = 0; t < C::FN; ++t) {
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-      const int64_t k = c0 + wj * WN + t * 8 + 2 * (lane & 3) + e;
+      const int64_t k = c0 + wj * C::WN + t * 8 + 2 * (lane & 3) + e;
       if (k < m) {
 #pragma unroll
-        for (int s = 0; s < FM; ++s) vsum[s] = fma(acc[s][t][e], acc[s][t][e], vsum[s]);
+        for (int s = 0; s < C::FM; ++s) vsum[s] = fma(acc[s][t][e], acc[s][t][e], vsum[s]);
       } else if (k == m) {
 #pragma unroll
-        for (int s = 0; s < FM; ++s) mval[s] = acc[s][t][e];
+        for (int s = 0; s < C::FM; ++s) mval[s] = acc[s][t][e];
       }
     }
   }
 }
 
-// Final fixed-order reduction: lanes sharing a row, then the 4 warp columns.
-__device__ __forceinline__ void finish_rows(double (&vsum)[FM], const double (&mval)[FM], double* red, double* mbuf,
-                                            int64_t m, int wi, int wj, int lane, int tid, int64_t row0, int64_t Ns,
-                                            double sigma2, double mean_const, double* mean, double* var,
+// Final fixed-order reduction: lanes sharing a row, then the WGN warp columns.
+template <class C>
+__device__ __forceinline__ void finish_rows(double (&vsum)[C::FM], const double (&mval)[C::FM], double* red,
+                                            double* mbuf, int64_t m, int wi, int wj, int lane, int tid, int64_t row0,
+                                            int64_t Ns, double sigma2, double mean_const, double* mean, double* var,
                                             uint32_t* flags) {
-  const int mwarp = int((m % BN) / WN);
-  const int mlane = int((m % WN) % 8) / 2;
+  const int mwarp = int((m % C::BN) / C::WN);
+  const int mlane = int((m % C::WN) % 8) / 2;
 #pragma unroll
-  for (int s = 0; s < FM; ++s) {
+  for (int s = 0; s < C::FM; ++s) {
     double v = vsum[s];
     v += __shfl_xor_sync(0xffffffffu, v, 1);
     v += __shfl_xor_sync(0xffffffffu, v, 2);
@@ -75,18 +96,20 @@ __device__ __forceinline__ void finish_rows(double (&vsum)[FM], const double (&m
   }
   if ((lane & 3) == 0) {
 #pragma unroll
-    for (int s = 0; s < FM; ++s) red[wj * BM + wi * WM + s * 8 + (lane >> 2)] = vsum[s];
+    for (int s = 0; s < C::FM; ++s) red[wj * C::BM + wi * C::WM + s * 8 + (lane >> 2)] = vsum[s];
   }
   if (wj == mwarp && (lane & 3) == mlane) {
 #pragma unroll
-    for (int s = 0; s < FM; ++s) mbuf[wi * WM + s * 8 + (lane >> 2)] = mval[s];
+    for (int s = 0; s < C::FM; ++s) mbuf[wi * C::WM + s * 8 + (lane >> 2)] = mval[s];
   }
   __syncthreads();
-  if (tid < BM) {
-    const int64_t row = row0 + tid;
+  for (int r = tid; r < C::BM; r += C::NT) {
+    const int64_t row = row0 + r;
     if (row < Ns) {
-      const double tot = ((red[tid] + red[BM + tid]) + red[2 * BM + tid]) + red[3 * BM + tid];
-      const double vv = sigma2 * tot, mm = mean_const + mbuf[tid];
+      double tot = red[r];
+#pragma unroll
+      for (int w = 1; w < C::WGN; ++w) tot += red[w * C::BM + r];
+      const double vv = sigma2 * tot, mm = mean_const + mbuf[r];
       if (var) var[row] = vv;
       mean[row] = mm;
       if (not_finite(vv) || not_finite(mm)) raise_flag(flags, FAGP_FLAG_PHI_NONFINITE);
@@ -94,19 +117,21 @@ __device__ __forceinline__ void finish_rows(double (&vsum)[FM], const double (&m
   }
 }
 
-template <int P>
-__global__ void __launch_bounds__(NT, 1)
+template <int P, class C>
+__global__ void __launch_bounds__(C::NT, C::MINB)
 predict_kernel_fast(const double* __restrict__ Ts, int64_t Ns, BasisView b, const double* __restrict__ Pop,
                     int64_t pc, double sigma2, double mean_const, double* __restrict__ mean,
                     double* __restrict__ var, uint32_t* flags) {
+  constexpr int BM = C::BM, BN = C::BN, NT = C::NT, ASP = C::ASP, BSP = C::BSP;
+  constexpr int WM = C::WM, WN = C::WN, FM = C::FM, FN = C::FN, A_STAGE = C::A_STAGE, B_STAGE = C::B_STAGE;
   extern __shared__ double sm[];
   double* As = sm;                             // [2][BM][ASP]
   double* Bs = sm + 2 * A_STAGE;               // [2][BK][BSP]
-  double* red = sm + 2 * (A_STAGE + B_STAGE);  // [4][BM]
+  double* red = sm + 2 * (A_STAGE + B_STAGE);  // [WGN][BM]
   const int M = b.M, pM = P * M, W = table_width(P, M);
-  double* tsm = red + 4 * BM;  // [BM][W]
+  double* tsm = red + C::WGN * BM;  // [BM][W]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wi = warp / 4, wj = warp % 4;
+  const int wi = warp / C::WGN, wj = warp % C::WGN;
   const int64_t row0 = int64_t(blockIdx.x) * BM;
   const int64_t m = b.m;
   const int Tn = int(ceil_div(m + 1, BN));
@@ -117,7 +142,7 @@ predict_kernel_fast(const double* __restrict__ Ts, int64_t Ns, BasisView b, cons
     for (int i = nd + tid; i < BM * W; i += NT) tsm[i] = 0.0;  // rows past N*
     cp_async_commit();
   }
-  const int gk = tid % BK, gr0 = tid / BK;  // generator: K column gk, rows gr0 + 8 q, q < 16
+  const int gk = tid % BK, gr0 = tid / BK;  // generator: K column gk, rows gr0 + GROWS q
 
   auto nk_of = [&](int c) { return int(round_up(tmin<int64_t>(m, int64_t(c) * BN + BN), BK) / BK); };
   auto offsets = [&](int64_t j0, int (&off)[P]) {
@@ -127,8 +152,8 @@ predict_kernel_fast(const double* __restrict__ Ts, int64_t Ns, BasisView b, cons
   auto gen_rows = [&](int stage, const int (&off)[P], int q0) {
     double* dst = As + stage * A_STAGE + gk;
 #pragma unroll
-    for (int qi = 0; qi < 2; ++qi) {
-      const int r = gr0 + 8 * (q0 + qi);
+    for (int qi = 0; qi < C::GPERKK; ++qi) {
+      const int r = gr0 + C::GROWS * (q0 + qi);
       const double* Tr = tsm + r * W;
       double v = Tr[off[0]];
 #pragma unroll
@@ -163,7 +188,7 @@ predict_kernel_fast(const double* __restrict__ Ts, int64_t Ns, BasisView b, cons
     int off[P];
     offsets(0, off);
 #pragma unroll
-    for (int q0 = 0; q0 < 16; q0 += 2) gen_rows(0, off, q0);
+    for (int kk = 0; kk < BK / 4; ++kk) gen_rows(0, off, kk * C::GPERKK);
   }
   cp_async_wait<0>();
   __syncthreads();
@@ -179,25 +204,32 @@ predict_kernel_fast(const double* __restrict__ Ts, int64_t Ns, BasisView b, cons
     if (has_next) load_b(buf ^ 1, int64_t(n2) * BK, int64_t(c2) * BN);
     int off[P];
     offsets(int64_t(n2) * BK, off);  // past the last step: harmless garbage into the spare buffer
+    // V^T is upper triangular: a K chunk lying entirely below this warp's columns is zero
+    const bool live = int64_t(n) * BK <= int64_t(c) * BN + wj * WN + WN - 1;
     const double* Ab = As + buf * A_STAGE + (wi * WM + (lane >> 2)) * ASP + (lane & 3);
     const double* Bb = Bs + buf * B_STAGE + (lane & 3) * BSP + wj * WN + (lane >> 2);
+    if (live) {
 #pragma unroll
-    for (int kk = 0; kk < BK / 4; ++kk) {
-      double a[FM], bb[FN];
+      for (int kk = 0; kk < BK / 4; ++kk) {
+        double a[FM], bb[FN];
 #pragma unroll
-      for (int s = 0; s < FM; ++s) a[s] = Ab[s * 8 * ASP + kk * 4];
+        for (int s = 0; s < FM; ++s) a[s] = Ab[s * 8 * ASP + kk * 4];
 #pragma unroll
-      for (int t = 0; t < FN; ++t) bb[t] = Bb[kk * 4 * BSP + t * 8];
+        for (int t = 0; t < FN; ++t) bb[t] = Bb[kk * 4 * BSP + t * 8];
 #pragma unroll
-      for (int s = 0; s < FM; ++s)
+        for (int s = 0; s < FM; ++s)
 #pragma unroll
-        for (int t = 0; t < FN; ++t) dmma_8x8x4(acc[s][t][0], acc[s][t][1], a[s], bb[t]);
-      gen_rows(buf ^ 1, off, kk * 2);
+          for (int t = 0; t < FN; ++t) dmma_8x8x4(acc[s][t][0], acc[s][t][1], a[s], bb[t]);
+        gen_rows(buf ^ 1, off, kk * C::GPERKK);
+      }
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < BK / 4; ++kk) gen_rows(buf ^ 1, off, kk * C::GPERKK);
     }
     cp_async_wait<0>();
     __syncthreads();
     if (n2 == 0 || !has_next) {
-      fold_tile(acc, vsum, mval, int64_t(c) * BN, m, wj, lane);
+      fold_tile<C>(acc, vsum, mval, int64_t(c) * BN, m, wj, lane);
 #pragma unroll
       for (int s = 0; s < FM; ++s)
 #pragma unroll
@@ -209,15 +241,18 @@ predict_kernel_fast(const double* __restrict__ Ts, int64_t Ns, BasisView b, cons
     nk = nk_of(c);
     buf ^= 1;
   }
-  finish_rows(vsum, mval, red, As, m, wi, wj, lane, tid, row0, Ns, sigma2, mean_const, mean, var, flags);
+  finish_rows<C>(vsum, mval, red, As, m, wi, wj, lane, tid, row0, Ns, sigma2, mean_const, mean, var, flags);
 }
 
 // Generic K5 (p > 8 or table rows too wide to stage): runtime p, table through L1, one
 // barrier-separated generation phase per step.
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(CfgLarge::NT, 1)
 predict_kernel_generic(const double* __restrict__ Ts, int64_t Ns, BasisView b, const double* __restrict__ Pop,
                        int64_t pc, double sigma2, double mean_const, double* __restrict__ mean,
                        double* __restrict__ var, uint32_t* flags) {
+  using C = CfgLarge;
+  constexpr int BM = C::BM, BN = C::BN, NT = C::NT, ASP = C::ASP, BSP = C::BSP;
+  constexpr int WM = C::WM, WN = C::WN, FM = C::FM, FN = C::FN, A_STAGE = C::A_STAGE, B_STAGE = C::B_STAGE;
   extern __shared__ double sm[];
   double* As = sm;
   double* Bs = sm + A_STAGE;
@@ -278,15 +313,43 @@ predict_kernel_generic(const double* __restrict__ Ts, int64_t Ns, BasisView b, c
       }
       __syncthreads();
     }
-    fold_tile(acc, vsum, mval, c0, m, wj, lane);
+    fold_tile<C>(acc, vsum, mval, c0, m, wj, lane);
   }
-  finish_rows(vsum, mval, red, As, m, wi, wj, lane, tid, row0, Ns, sigma2, mean_const, mean, var, flags);
+  finish_rows<C>(vsum, mval, red, As, m, wi, wj, lane, tid, row0, Ns, sigma2, mean_const, mean, var, flags);
 }
 
 }  // namespace pred
 }  // namespace fagp
 
 using namespace fagp;
+
+namespace fagp {
+namespace pred {
+template <int P, class C>
+int launch_fast(const double* Ts, int64_t Ns, const fagp_basis* basis, const double* op, int64_t pc, double sigma2,
+                double c, double* mean, double* var, uint32_t* flags, cudaStream_t s) {
+  const size_t smem = fast_smem_bytes<C>(table_width(basis->p, basis->M));
+  FAGP_CUDA_TRY(cudaFuncSetAttribute(predict_kernel_fast<P, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  predict_kernel_fast<P, C><<<unsigned(ceil_div(Ns, C::BM)), C::NT, smem, s>>>(Ts, Ns, view(basis), op, pc, sigma2, c,
+                                                                              mean, var, flags);
+  return FAGP_OK;
+}
+template <class C>
+int dispatch_fast(const double* Ts, int64_t Ns, const fagp_basis* basis, const double* op, int64_t pc, double sigma2,
+                  double c, double* mean, double* var, uint32_t* flags, cudaStream_t s) {
+  switch (basis->p) {
+    case 1: return launch_fast<1, C>(Ts, Ns, basis, op, pc, sigma2, c, mean, var, flags, s);
+    case 2: return launch_fast<2, C>(Ts, Ns, basis, op, pc, sigma2, c, mean, var, flags, s);
+    case 3: return launch_fast<3, C>(Ts, Ns, basis, op, pc, sigma2, c, mean, var, flags, s);
+    case 4: return launch_fast<4, C>(Ts, Ns, basis, op, pc, sigma2, c, mean, var, flags, s);
+    case 5: return launch_fast<5, C>(Ts, Ns, basis, op, pc, sigma2, c, mean, var, flags, s);
+    case 6: return launch_fast<6, C>(Ts, Ns, basis, op, pc, sigma2, c, mean, var, flags, s);
+    case 7: return launch_fast<7, C>(Ts, Ns, basis, op, pc, sigma2, c, mean, var, flags, s);
+    default: return launch_fast<8, C>(Ts, Ns, basis, op, pc, sigma2, c, mean, var, flags, s);
+  }
+}
+}  // namespace pred
+}  // namespace fagp
 
 extern "C" {
 
@@ -298,34 +361,24 @@ int fagp_predict(const double* Ts, int64_t Ns, const fagp_basis* basis, const do
   if (Ns == 0) return FAGP_OK;
   const int64_t pc = round_up(basis->m + 1, pred::OP_COL_ALIGN);
   const int W = table_width(basis->p, basis->M);
-  const int64_t grid = ceil_div(Ns, pred::BM);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const size_t fsmem = pred::fast_smem_bytes(W);
-  if (basis->p <= 8 && fsmem <= pred::kMaxSmem) {
-    auto launch = [&](auto kern) -> int {
-      FAGP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fsmem)));
-      kern<<<unsigned(grid), pred::NT, fsmem, s>>>(Ts, Ns, view(basis), predict_op, pc, sigma2, mean_const, mean,
-                                                   var, flags);
-      return FAGP_OK;
-    };
-    int rc;
-    switch (basis->p) {
-      case 1: rc = launch(pred::predict_kernel_fast<1>); break;
-      case 2: rc = launch(pred::predict_kernel_fast<2>); break;
-      case 3: rc = launch(pred::predict_kernel_fast<3>); break;
-      case 4: rc = launch(pred::predict_kernel_fast<4>); break;
-      case 5: rc = launch(pred::predict_kernel_fast<5>); break;
-      case 6: rc = launch(pred::predict_kernel_fast<6>); break;
-      case 7: rc = launch(pred::predict_kernel_fast<7>); break;
-      default: rc = launch(pred::predict_kernel_fast<8>); break;
-    }
-    if (rc) return rc;
+  const char* cfg = getenv("FAGP_PREDICT_CFG");  // tuning override: "large" | "small"
+  const bool small_ok = pred::fast_smem_bytes<pred::CfgSmall>(W) * pred::CfgSmall::MINB <=
+                        228 * 1024 - 1024 * pred::CfgSmall::MINB;
+  const bool large_ok = pred::fast_smem_bytes<pred::CfgLarge>(W) <= pred::kMaxSmem;
+  int rc = FAGP_OK;
+  if (basis->p <= 8 && small_ok && !(cfg && strcmp(cfg, "large") == 0)) {
+    rc = pred::dispatch_fast<pred::CfgSmall>(Ts, Ns, basis, predict_op, pc, sigma2, mean_const, mean, var, flags, s);
+  } else if (basis->p <= 8 && large_ok) {
+    rc = pred::dispatch_fast<pred::CfgLarge>(Ts, Ns, basis, predict_op, pc, sigma2, mean_const, mean, var, flags, s);
   } else {
     FAGP_CUDA_TRY(cudaFuncSetAttribute(pred::predict_kernel_generic, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(pred::BASE_SMEM)));
-    pred::predict_kernel_generic<<<unsigned(grid), pred::NT, pred::BASE_SMEM, s>>>(
-        Ts, Ns, view(basis), predict_op, pc, sigma2, mean_const, mean, var, flags);
+                                       int(pred::CfgLarge::BASE_SMEM)));
+    pred::predict_kernel_generic<<<unsigned(ceil_div(Ns, pred::CfgLarge::BM)), pred::CfgLarge::NT,
+                                   pred::CfgLarge::BASE_SMEM, s>>>(Ts, Ns, view(basis), predict_op, pc, sigma2,
+                                                                   mean_const, mean, var, flags);
   }
+  if (rc) return rc;
   FAGP_LAUNCH_CHECK();
   return FAGP_OK;
 }
