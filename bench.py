@@ -61,7 +61,7 @@ def useful_flops(N, Ns, m):
     return N * m * (m + 1) + 2 * N * m + 2 * m**3 / 3 + 2 * Ns * m + Ns * m * (m + 1) + 2 * Ns * m
 
 
-def launches_per_step(m):
+def launches_per_step(m, pair):
     """Kernels of ours launched by one PosteriorEngine.run() (no jitter retry)."""
     nblk = -(-m // 32)
     potrf = nblk + (nblk - 1)  # fused diag+panel kernel per step, trailing GEMM between steps
@@ -74,7 +74,11 @@ def launches_per_step(m):
         levels += 1
         h *= 2
     trtri = 1 + 1 + 2 * levels  # pad, diag_inv, 2 GEMMs per level
-    factor = 1 + 1 + potrf + 1 + trtri + 2 + 1  # build G/t, build A, potrf, zero upper, trtri, w GEMVs x2, operand
+    if pair:
+        # t copy, build A, potrf, zero upper, trtri, w GEMVs x2, D = X^T X, Ct, w copy
+        factor = 1 + 1 + potrf + 1 + trtri + 2 + 1 + 1 + 1
+        return 2 + 2 + factor + 2  # basis_eval x2, pair GEMM + reduce, factor, var + mean
+    factor = 1 + 1 + potrf + 1 + trtri + 2 + 1  # build G/t, build A, potrf, zero upper, trtri, GEMVs, operand
     return 2 + 2 + factor + 1  # basis_eval x2, gram + reduce, factor, predict
 
 
@@ -304,20 +308,31 @@ def main():
 
     # ---- roofline of the dominant kernel (per launch, this rank's shard) ----
     n_loc, ns_loc = X.shape[0], Xs.shape[0]
-    gram_flops = n_loc * m * (m + 1) + 2 * n_loc * m
-    pred_flops = ns_loc * m * (m + 1) + 4 * ns_loc * m
+    pair = p >= 2
+    P = M * (M + 1) // 2
+    if pair:  # pair form: the GEMM over the P^p distinct Gram / variance entries (+ t, mean)
+        gram_flops = 2 * n_loc * P**p + 2 * n_loc * m
+        pred_flops = 2 * ns_loc * P**p + 2 * ns_loc * m
+    else:
+        gram_flops = n_loc * m * (m + 1) + 2 * n_loc * m
+        pred_flops = ns_loc * m * (m + 1) + 4 * ns_loc * m
+    ref_gram = n_loc * m * (m + 1) + 2 * n_loc * m  # SURVEY.md §8d counts (reference algorithm)
+    ref_pred = ns_loc * m * (m + 1) + 4 * ns_loc * m
     g_ms, p_ms = statistics.mean(gram_ms), statistics.mean(pred_ms)
     peak, peak_src = fp64_peak()
     if g_ms >= p_ms:
-        dom, dflops, dms = "gram_kernel (fagp_gram: K1 + K1b reduce)", gram_flops, g_ms
+        dom, dflops, rflops, dms = "fagp_gram (pair-form DMMA GEMM + reduce + t)" if pair else \
+            "fagp_gram (fused SYRK + reduce)", gram_flops, ref_gram, g_ms
         traffic = ncu_traffic("gram_kernel")
     else:
-        dom, dflops, dms = "predict_kernel (fagp_predict: K5)", pred_flops, p_ms
+        dom, dflops, rflops, dms = "fagp_predict (pair-form variance GEMM + mean)" if pair else \
+            "fagp_predict (fused triangular GEMM)", pred_flops, ref_pred, p_ms
         traffic = ncu_traffic("predict_kernel")
     achieved = dflops / (dms / 1e3) / 1e12
     roofline = {"bound": "tensor", "kernel": dom, "achieved": round(achieved, 3), "peak": peak, "unit": "TFLOP/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                "flops_per_launch": dflops}
+                "flops_per_launch": dflops, "algorithm": "pair form (P^p distinct entries)" if pair else "direct",
+                "reference_equivalent_tflops": round(rflops / (dms / 1e3) / 1e12, 3)}
     step_tf = useful_flops(N, Ns, m) / world / (ms / 1e3) / 1e12
 
     # ---- end to end through the public API (pinned host in, host numpy out) ----
@@ -362,10 +377,10 @@ def main():
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator)",
                "config": config_dict(args, world), "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
-               "clocks": clk.summary(), "gpu_launches": launches_per_step(m) * args.steps,
+               "clocks": clk.summary(), "gpu_launches": launches_per_step(m, p >= 2) * args.steps,
                "phases_ms": {"tables": round(statistics.mean(tab_ms), 3), "gram": round(g_ms, 3),
                              "allreduce+factor": round(statistics.mean(factor_ms), 3), "predict": round(p_ms, 3)},
-               "step_tflops_useful": round(step_tf, 3), "step_frac_of_peak": round(step_tf / peak, 4),
+               "step_reference_equivalent_tflops": round(step_tf, 3),
                "jitter": eng.jitter.value, "lib": str(_lib.LIB_PATH.name)}
         print(json.dumps(out), flush=True)
     if world > 1:

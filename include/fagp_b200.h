@@ -116,38 +116,47 @@ int fagp_find_nonfinite(const double* T, int64_t N, const fagp_basis* basis, int
 
 /* Fused feature generation + Gram contraction on FP64 tensor cores (DMMA).
  * Replaces `backend.gemm(phi, phi, transpose_a=True)` (posterior.py:168) and
- * `backend.gemm(phi, y - c, transpose_a=True)` (posterior.py:229,233):
- *   gram_ext = [Phi | r]^T [Phi | r],  r = y - mean_const,
- * returned as the packed upper triangle of the (m+1) x (m+1) matrix, row-major:
- * element (i, j), i <= j, at i*(2(m+1) - i - 1)/2 + j.  Column m holds t = Phi^T r.
- * Phi is never written to HBM.  Deterministic for fixed (N, basis): fixed split-K tree,
- * no floating-point atomics.  T comes from fagp_basis_eval(X, y, mean_const).  Sets
- * FAGP_FLAG_PHI_NONFINITE when a feature is not finite (detected on the Gram diagonal). */
-int64_t fagp_gram_packed_len(int64_t m);
+ * `backend.gemm(phi, y - c, transpose_a=True)` (posterior.py:229,233), with Phi never
+ * written to HBM.  The output `gram` (fagp_gram_len(basis) doubles) is a compressed form
+ * of G = Phi^T Phi and t = Phi^T (y - c), read by fagp_factor / fagp_gram_unpack:
+ *  - p >= 2 ("pair form"): [H | t].  G[(a),(a')] = sum_r prod_d phi_d,a_d phi_d,a'_d depends
+ *    only on the unordered pair {a_d, a'_d} of every dimension, so G has (M(M+1)/2)^p distinct
+ *    entries H[pi_0, ..., pi_{p-1}] (pi = pair index, first dimension slowest), computed as
+ *    one rectangular DMMA GEMM over the rows; t follows (m entries, CUDA cores).
+ *  - p == 1: the packed upper triangle of [Phi | r]^T [Phi | r] ((m+1)(m+2)/2, row-major;
+ *    column m holds t), from a fused SYRK.
+ * This buffer is also the only data multi-GPU callers all-reduce (sum over row shards).
+ * Deterministic for fixed (N, basis): fixed split-K trees, no floating-point atomics.
+ * T comes from fagp_basis_eval(X, y, mean_const).  Sets FAGP_FLAG_PHI_NONFINITE when a
+ * feature is not finite (detected on the Gram entries). */
+int64_t fagp_gram_len(const fagp_basis* basis);
 size_t fagp_gram_workspace_size(int64_t N, const fagp_basis* basis);
-int fagp_gram(const double* T, int64_t N, const fagp_basis* basis, double* gram_ext_packed,
-              void* workspace, size_t workspace_bytes, uint32_t* flags, void* stream);
+int fagp_gram(const double* T, int64_t N, const fagp_basis* basis, double* gram, void* workspace,
+              size_t workspace_bytes, uint32_t* flags, void* stream);
+
+/* Expand a `gram` buffer into the full symmetric G (m x m, nullable) and t (m, nullable). */
+int fagp_gram_unpack(const double* gram, const fagp_basis* basis, double* G, double* t, void* stream);
 
 /* ---- (3) Cholesky factorisation and solves ----------------------------------------- */
-/* Scaled system A = (s_i G_ij) s_j + sigma2 I (posterior.py:171-174) from the packed Gram,
+/* Scaled system A = (s_i G_ij) s_j + sigma2 I (posterior.py:171-174) from the `gram` buffer,
  * its Cholesky factor with the reference's jitter schedule [0, b, 10b, 100b],
- * b = 1e-12 trace(A)/m (backend.py:154-189), the mean weights
- * w = s * A^{-1}(s * t) (posterior.py:233-235), and V = L^{-1} diag(s) written
- * transposed into the predict operand.  Synchronises `stream` once per attempt.
- * Outputs (device): L (m x m, lower; upper part zeroed), G (m x m symmetric, nullable),
- * t (m), w (m), predict_op (fagp_predict_operand_len(m) doubles; its mean column is
- * filled with w).  Host outputs: *jitter (the jitter that succeeded), *pivot_index
- * (1-based LAPACK-style leading minor on ENOTPD, else 0). */
+ * b = 1e-12 trace(A)/m (backend.py:154-189), V = L^{-1} diag(s) (TRTRI), the mean weights
+ * w = V^T V t = s * A^{-1}(s * t) (posterior.py:233-235) and the predict operand
+ * (pair form: [Ct | w] with Ct the pair-folded S A^{-1} S; p == 1: [V^T | w]).
+ * Synchronises `stream` once per attempt.  Outputs (device): L (m x m, lower; upper part
+ * zeroed), G (m x m symmetric, nullable), t (m), w (m), predict_op
+ * (fagp_predict_operand_len(basis) doubles, nullable).  Host outputs: *jitter (the jitter
+ * that succeeded), *pivot_index (1-based LAPACK-style leading minor on ENOTPD, else 0). */
 size_t fagp_factor_workspace_size(int64_t m);
-int64_t fagp_predict_operand_len(int64_t m);
-int fagp_factor(const double* gram_ext_packed, const double* sqrt_lam, double sigma2, int64_t m,
-                int32_t jitter_attempts, double* L, double* G, double* t, double* w,
-                double* predict_op, double* jitter, int32_t* pivot_index, void* workspace,
-                size_t workspace_bytes, void* stream);
+int64_t fagp_predict_operand_len(const fagp_basis* basis);
+int fagp_factor(const double* gram, const fagp_basis* basis, const double* sqrt_lam, double sigma2,
+                int32_t jitter_attempts, double* L, double* G, double* t, double* w, double* predict_op,
+                double* jitter, int32_t* pivot_index, void* workspace, size_t workspace_bytes,
+                void* stream);
 
-/* Overwrite the mean column of the predict operand with w (used after the reference's
- * fault-injection hook flips w, posterior.py:245-246). */
-int fagp_set_mean_weights(double* predict_op, const double* w, int64_t m, void* stream);
+/* Overwrite the mean weights stored in the predict operand with w (used after the
+ * reference's fault-injection hook flips w, posterior.py:245-246). */
+int fagp_set_mean_weights(double* predict_op, const double* w, const fagp_basis* basis, void* stream);
 
 /* Plain lower Cholesky of a symmetric m x m matrix, in place, no jitter: the single
  * dpotrf call inside SpdFactor (backend.py:172).  *info_dev (device int32) receives 0 or
@@ -173,10 +182,12 @@ int fagp_trtri(const double* L, const double* s, int64_t m, double* V, void* wor
                size_t workspace_bytes, void* stream);
 
 /* ---- (4) predictive mean and variance ---------------------------------------------- */
-/* Fused Phi*-generation + FP64 DMMA contraction with [V^T | w] + row reduction:
- *   mean[i] = mean_const + Phi*_i . w                   (posterior.py:247)
- *   var[i]  = sigma2 * || V phi*_i ||^2                 (= diag of posterior.py:249-263,
+/*   mean[i] = mean_const + Phi*_i . w                   (posterior.py:247)
+ *   var[i]  = sigma2 * phi*_i^T (S A^{-1} S) phi*_i      (= diag of posterior.py:249-263,
  *                                                          the variance cli.py:222 reports)
+ * Pair form (p >= 2): var = sigma2 sum_pi Ct[pi] prod_d q_d[i, pi_d] as a DMMA GEMM over the
+ * pair combos with a fused q-product epilogue; mean by nested per-dimension sums.
+ * p == 1: fused Phi*-generation + DMMA contraction with [V^T | w] + row sums of squares.
  * Ts = fagp_basis_eval(Xstar).  var may be NULL (mean only). */
 int fagp_predict(const double* Ts, int64_t Ns, const fagp_basis* basis, const double* predict_op,
                  double sigma2, double mean_const, double* mean, double* var, uint32_t* flags,

@@ -64,13 +64,14 @@ SIGNATURES = {
     "fagp_set_residual": (ctypes.c_int, [_P, _I64, _BASIS, _P, _D, _P]),
     "fagp_features": (ctypes.c_int, [_P, _I64, _BASIS, _P, _P, _P]),
     "fagp_find_nonfinite": (ctypes.c_int, [_P, _I64, _BASIS, _P, _P]),
-    "fagp_gram_packed_len": (_I64, [_I64]),
+    "fagp_gram_len": (_I64, [_BASIS]),
+    "fagp_gram_unpack": (ctypes.c_int, [_P, _BASIS, _P, _P, _P]),
     "fagp_gram_workspace_size": (_SZ, [_I64, _BASIS]),
     "fagp_gram": (ctypes.c_int, [_P, _I64, _BASIS, _P, _P, _SZ, _P, _P]),
     "fagp_factor_workspace_size": (_SZ, [_I64]),
-    "fagp_predict_operand_len": (_I64, [_I64]),
-    "fagp_factor": (ctypes.c_int, [_P, _P, _D, _I64, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
-    "fagp_set_mean_weights": (ctypes.c_int, [_P, _P, _I64, _P]),
+    "fagp_predict_operand_len": (_I64, [_BASIS]),
+    "fagp_factor": (ctypes.c_int, [_P, _BASIS, _P, _D, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "fagp_set_mean_weights": (ctypes.c_int, [_P, _P, _BASIS, _P]),
     "fagp_potrf_workspace_size": (_SZ, [_I64]),
     "fagp_potrf": (ctypes.c_int, [_P, _I64, _P, _P, _SZ, _P]),
     "fagp_potrs": (ctypes.c_int, [_P, _I64, _P, _I64, _P]),

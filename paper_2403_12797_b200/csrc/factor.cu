@@ -17,6 +17,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "pair.cuh"
 
 namespace fagp {
 namespace la {
@@ -550,6 +551,7 @@ struct FactorWs {
   double* Lp;      // mp2^2
   double* X;       // mp2^2
   double* Tmp;     // mp2^2 / 4
+  double* D;       // m x m: X^T X for the pair-form predict operand
   size_t bytes;
 };
 
@@ -572,6 +574,7 @@ inline FactorWs carve(void* base, int64_t m) {
   w.Lp = reinterpret_cast<double*>(take(size_t(mp) * mp * sizeof(double)));
   w.X = reinterpret_cast<double*>(take(size_t(mp) * mp * sizeof(double)));
   w.Tmp = reinterpret_cast<double*>(take(size_t(mp) * mp / 4 * sizeof(double) + sizeof(double)));
+  w.D = reinterpret_cast<double*>(take(size_t(m) * m * sizeof(double)));
   w.bytes = off;
   return w;
 }
@@ -591,9 +594,23 @@ size_t fagp_factor_workspace_size(int64_t m) {
   return carve(nullptr, m).bytes;
 }
 
-int64_t fagp_predict_operand_len(int64_t m) {
-  if (m < 1) return -1;
-  return op_rows(m) * op_cols(m);
+int64_t fagp_predict_operand_len(const fagp_basis* basis) {
+  if (check_basis(basis) != FAGP_OK) return -1;
+  if (pairk::enabled(basis->p, basis->M)) return pairk::predict_op_len(basis);
+  return op_rows(basis->m) * op_cols(basis->m);
+}
+
+int fagp_gram_unpack(const double* gram, const fagp_basis* basis, double* G, double* t, void* stream) {
+  int st = check_basis(basis);
+  if (st) return st;
+  if (gram == nullptr) return FAGP_EINVAL;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (pairk::enabled(basis->p, basis->M)) return pairk::system(gram, nullptr, 0.0, 0.0, basis, nullptr, G, t, s);
+  const int64_t m = basis->m;
+  const int grid = int(tmin<int64_t>(ceil_div(m * m, 256), 8 * num_sms()));
+  system_build_kernel<<<grid, 256, 0, s>>>(gram, nullptr, 0.0, 0.0, m, nullptr, G, t);
+  FAGP_LAUNCH_CHECK();
+  return FAGP_OK;
 }
 
 size_t fagp_potrf_workspace_size(int64_t m) { return m < 1 ? 0 : potrf_ws_bytes(); }
@@ -650,18 +667,29 @@ int fagp_dgemm(int32_t trans_a, int32_t trans_b, int64_t M, int64_t N, int64_t K
   return gemm(trans_b != 0, g, 1, static_cast<cudaStream_t>(stream), trans_a != 0);
 }
 
-int fagp_set_mean_weights(double* predict_op, const double* w, int64_t m, void* stream) {
-  if (predict_op == nullptr || w == nullptr || m < 1) return FAGP_EINVAL;
+int fagp_set_mean_weights(double* predict_op, const double* w, const fagp_basis* basis, void* stream) {
+  int st = check_basis(basis);
+  if (st) return st;
+  if (predict_op == nullptr || w == nullptr) return FAGP_EINVAL;
+  if (pairk::enabled(basis->p, basis->M))
+    return pairk::set_weights(predict_op, w, basis, static_cast<cudaStream_t>(stream));
+  const int64_t m = basis->m;
   set_mean_weights_kernel<<<unsigned(ceil_div(m, 256)), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       predict_op, w, m, op_cols(m));
   FAGP_LAUNCH_CHECK();
   return FAGP_OK;
 }
 
-int fagp_factor(const double* packed, const double* sqrt_lam, double sigma2, int64_t m, int32_t jitter_attempts,
-                double* L, double* G, double* t, double* w, double* predict_op, double* jitter_out,
-                int32_t* pivot_out, void* workspace, size_t workspace_bytes, void* stream) {
-  if (packed == nullptr || sqrt_lam == nullptr || L == nullptr || t == nullptr || w == nullptr || m < 1 ||
+int fagp_factor(const double* packed, const fagp_basis* basis, const double* sqrt_lam, double sigma2,
+                int32_t jitter_attempts, double* L, double* G, double* t, double* w, double* predict_op,
+                double* jitter_out, int32_t* pivot_out, void* workspace, size_t workspace_bytes, void* stream) {
+  {
+    int st = check_basis(basis);
+    if (st) return st;
+  }
+  const int64_t m = basis->m;
+  const bool pm = pairk::enabled(basis->p, basis->M);
+  if (packed == nullptr || sqrt_lam == nullptr || L == nullptr || t == nullptr || w == nullptr ||
       jitter_attempts < 0)
     return FAGP_EINVAL;
   if (!(sigma2 > 0.0) || !std::isfinite(sigma2)) return FAGP_EINVAL;
@@ -673,8 +701,16 @@ int fagp_factor(const double* packed, const double* sqrt_lam, double sigma2, int
   if (jitter_out) *jitter_out = 0.0;
 
   // G and t once (A is rebuilt per attempt below)
-  system_build_kernel<<<grid, 256, 0, s>>>(packed, sqrt_lam, sigma2, 0.0, m, nullptr, G, t);
-  FAGP_LAUNCH_CHECK();
+  auto build = [&](double jit, double* A_, double* G_, double* t_) -> int {
+    if (pm) return pairk::system(packed, sqrt_lam, sigma2, jit, basis, A_, G_, t_, s);
+    system_build_kernel<<<grid, 256, 0, s>>>(packed, sqrt_lam, sigma2, jit, m, A_, G_, t_);
+    FAGP_LAUNCH_CHECK();
+    return FAGP_OK;
+  };
+  {
+    int rc = build(0.0, nullptr, G, t);
+    if (rc) return rc;
+  }
 
   double base = 0.0;
   bool have_base = false;
@@ -684,8 +720,8 @@ int fagp_factor(const double* packed, const double* sqrt_lam, double sigma2, int
     if (attempt > 0) {
       if (!have_base) {
         // trace of the un-jittered A, in numpy's summation order (np.trace)
-        system_build_kernel<<<grid, 256, 0, s>>>(packed, sqrt_lam, sigma2, 0.0, m, L, nullptr, nullptr);
-        FAGP_LAUNCH_CHECK();
+        int rc0 = build(0.0, L, nullptr, nullptr);
+        if (rc0) return rc0;
         trace_kernel<<<1, 256, 0, s>>>(L, m, ws.vec, ws.scalar);
         FAGP_LAUNCH_CHECK();
         double tr = 0.0;
@@ -698,8 +734,10 @@ int fagp_factor(const double* packed, const double* sqrt_lam, double sigma2, int
       for (int k = 1; k < attempt; ++k) p10 *= 10.0;
       jit = base * p10;
     }
-    system_build_kernel<<<grid, 256, 0, s>>>(packed, sqrt_lam, sigma2, jit, m, L, nullptr, nullptr);
-    FAGP_LAUNCH_CHECK();
+    {
+      int rc1 = build(jit, L, nullptr, nullptr);
+      if (rc1) return rc1;
+    }
     FAGP_CUDA_TRY(cudaMemsetAsync(ws.info, 0, sizeof(int), s));
     int rc = potrf_blocked(L, m, m, ws.info, s);
     if (rc) return rc;
@@ -725,10 +763,19 @@ int fagp_factor(const double* packed, const double* sqrt_lam, double sigma2, int
   vt_cols_kernel<<<unsigned(ceil_div(m, 32)), dim3(32, 8), 0, s>>>(ws.X, mp, sqrt_lam, ws.vec, m, w);
   FAGP_LAUNCH_CHECK();
   if (predict_op) {
-    const int64_t pr = op_rows(m), pc = op_cols(m);
-    dim3 g2(unsigned(ceil_div(pc, 32)), unsigned(ceil_div(pr, 32)));
-    predict_operand_kernel<<<g2, dim3(32, 8), 0, s>>>(ws.X, mp, sqrt_lam, w, m, predict_op, pr, pc);
-    FAGP_LAUNCH_CHECK();
+    if (pm) {
+      // D = X^T X (X = L^{-1}, lower), then the pair-folded Ct = fold(S D S) and w
+      GemmArgs g{int(m), int(m), int(m), 1.0, 0.0, ws.X, mp, 0, ws.X, mp, 0, ws.D, m, 0, 0, nullptr};
+      int rc = gemm(false, g, 1, s, true);
+      if (rc) return rc;
+      rc = pairk::build_predict_op(ws.D, sqrt_lam, w, basis, predict_op, s);
+      if (rc) return rc;
+    } else {
+      const int64_t pr = op_rows(m), pc = op_cols(m);
+      dim3 g2(unsigned(ceil_div(pc, 32)), unsigned(ceil_div(pr, 32)));
+      predict_operand_kernel<<<g2, dim3(32, 8), 0, s>>>(ws.X, mp, sqrt_lam, w, m, predict_op, pr, pc);
+      FAGP_LAUNCH_CHECK();
+    }
   }
   return FAGP_OK;
 }

@@ -25,6 +25,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "pair.cuh"
 
 namespace fagp {
 namespace gram {
@@ -367,13 +368,15 @@ int dispatch_fast(const double* T, int64_t N, const fagp_basis* basis, const Pla
 
 extern "C" {
 
-int64_t fagp_gram_packed_len(int64_t m) {
-  if (m < 1) return -1;
-  return (m + 1) * (m + 2) / 2;
+int64_t fagp_gram_len(const fagp_basis* basis) {
+  if (check_basis(basis) != FAGP_OK) return -1;
+  if (pairk::enabled(basis->p, basis->M)) return pairk::gram_len(basis);
+  return (basis->m + 1) * (basis->m + 2) / 2;
 }
 
 size_t fagp_gram_workspace_size(int64_t N, const fagp_basis* basis) {
   if (check_basis(basis) != FAGP_OK || N < 0) return 0;
+  if (pairk::enabled(basis->p, basis->M)) return pairk::gram_workspace(N, basis);
   const gram::Plan pl = gram::choose(N, basis).plan;
   return size_t(pl.S) * pl.npairs * pl.BT * pl.BT * sizeof(double);
 }
@@ -383,6 +386,8 @@ int fagp_gram(const double* T, int64_t N, const fagp_basis* basis, double* gram_
   int st = check_basis(basis);
   if (st) return st;
   if (N < 0 || gram_ext_packed == nullptr || (N > 0 && T == nullptr)) return FAGP_EINVAL;
+  if (pairk::enabled(basis->p, basis->M))
+    return pairk::gram(T, N, basis, gram_ext_packed, workspace, workspace_bytes, flags, static_cast<cudaStream_t>(stream));
   const gram::Choice ch = gram::choose(N, basis);
   const gram::Plan pl = ch.plan;
   const size_t need = size_t(pl.S) * pl.npairs * pl.BT * pl.BT * sizeof(double);

@@ -19,6 +19,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "pair.cuh"
 
 namespace fagp {
 namespace pred {
@@ -359,6 +360,9 @@ int fagp_predict(const double* Ts, int64_t Ns, const fagp_basis* basis, const do
   if (st) return st;
   if (Ns < 0 || predict_op == nullptr || (Ns > 0 && (Ts == nullptr || mean == nullptr))) return FAGP_EINVAL;
   if (Ns == 0) return FAGP_OK;
+  if (pairk::enabled(basis->p, basis->M))
+    return pairk::predict(Ts, Ns, basis, predict_op, sigma2, mean_const, mean, var, flags,
+                          static_cast<cudaStream_t>(stream));
   const int64_t pc = round_up(basis->m + 1, pred::OP_COL_ALIGN);
   const int W = table_width(basis->p, basis->M);
   cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -41,14 +41,14 @@ class PosteriorEngine:
         e = lambda *shape: dev.empty(shape, device=self.device)  # noqa: E731
         self.T = e(self.N, W)
         self.Ts = e(self.Ns, W)
-        self.packed = e(int(L.fagp_gram_packed_len(m)))
+        self.packed = e(int(L.fagp_gram_len(b.ref)))
         self.gram_ws_bytes = int(L.fagp_gram_workspace_size(self.N, b.ref))
         self.gram_ws = e(max(1, self.gram_ws_bytes // 8))
         self.lam, self.lam_floored, self.sqrt_lam = e(m), e(m), e(m)
         self.L = e(m, m)
         self.G = e(m, m) if keep_gram else None
         self.t, self.w = e(m), e(m)
-        self.predict_op = e(int(L.fagp_predict_operand_len(m)))
+        self.predict_op = e(int(L.fagp_predict_operand_len(b.ref)))
         self.factor_ws_bytes = int(L.fagp_factor_workspace_size(m))
         self.factor_ws = e(max(1, self.factor_ws_bytes // 8))
         self.mean = e(self.Ns)
@@ -87,7 +87,7 @@ class PosteriorEngine:
 
     def stage_factor(self, stream=None):
         L, s, b = _lib.lib(), _lib.stream_handle(stream), self.basis
-        self.status = L.fagp_factor(_lib.ptr(self.packed), _lib.ptr(self.sqrt_lam), self.noise_var, b.m,
+        self.status = L.fagp_factor(_lib.ptr(self.packed), b.ref, _lib.ptr(self.sqrt_lam), self.noise_var,
                                     JITTER_ATTEMPTS, _lib.ptr(self.L), _lib.ptr(self.G), _lib.ptr(self.t),
                                     _lib.ptr(self.w), _lib.ptr(self.predict_op), ctypes.byref(self.jitter),
                                     ctypes.byref(self.pivot), _lib.ptr(self.factor_ws), self.factor_ws_bytes, s)
@@ -96,7 +96,7 @@ class PosteriorEngine:
         return self.status
 
     def set_mean_weights(self, stream=None):
-        _lib.check(_lib.lib().fagp_set_mean_weights(_lib.ptr(self.predict_op), _lib.ptr(self.w), self.basis.m,
+        _lib.check(_lib.lib().fagp_set_mean_weights(_lib.ptr(self.predict_op), _lib.ptr(self.w), self.basis.ref,
                                                     _lib.stream_handle(stream)), "set_mean_weights")
 
     def stage_predict(self, stream=None):

@@ -151,7 +151,7 @@ def gram_packed(basis, T, yd=None, mean_const=0.0, flag_ptr=None, stream=None):
     N = int(T.shape[0])
     if N > 0:
         _lib.check(L.fagp_set_residual(_lib.ptr(T), N, basis.ref, _lib.ptr(yd), float(mean_const), s), "set_residual")
-    packed = dev.empty((int(L.fagp_gram_packed_len(basis.m)),), device=T.device)
+    packed = dev.empty((int(L.fagp_gram_len(basis.ref)),), device=T.device)
     wsz = int(L.fagp_gram_workspace_size(N, basis.ref))
     ws = dev.empty((max(1, wsz // 8),), device=T.device)
     _lib.check(L.fagp_gram(_lib.ptr(T), N, basis.ref, _lib.ptr(packed), _lib.ptr(ws), wsz, flag_ptr, s), "gram")
@@ -173,17 +173,26 @@ def factor_packed(basis, packed, noise_var, mean_const, N, keep_gram=False, stre
     G = dev.empty((m, m), device=device) if keep_gram else None
     t = dev.empty((m,), device=device)
     w = dev.empty((m,), device=device)
-    P = dev.empty((int(L.fagp_predict_operand_len(m)),), device=device)
+    P = dev.empty((int(L.fagp_predict_operand_len(basis.ref)),), device=device)
     wsz = int(L.fagp_factor_workspace_size(m))
     ws = dev.empty((max(1, wsz // 8),), device=device)
     jit = ctypes.c_double(0.0)
     piv = ctypes.c_int32(0)
-    st = L.fagp_factor(_lib.ptr(packed), _lib.ptr(sq), float(noise_var), m, JITTER_ATTEMPTS, _lib.ptr(Lf),
+    st = L.fagp_factor(_lib.ptr(packed), basis.ref, _lib.ptr(sq), float(noise_var), JITTER_ATTEMPTS, _lib.ptr(Lf),
                        _lib.ptr(G), _lib.ptr(t), _lib.ptr(w), _lib.ptr(P), ctypes.byref(jit), ctypes.byref(piv),
                        _lib.ptr(ws), wsz, s)
     f = Fit(basis=basis, noise_var=float(noise_var), mean_const=float(mean_const), N=N, lam=lam, lam_floored=lam_f,
             sqrt_lam=sq, packed=packed, L=Lf, t=t, w=w, predict_op=P, jitter=float(jit.value), G=G)
     return f, st, int(piv.value)
+
+
+def gram_unpack(basis, packed):
+    """Full symmetric G (m x m) and t (m) from a `gram` buffer (device tensors)."""
+    G = dev.empty((basis.m, basis.m), device=packed.device)
+    t = dev.empty((basis.m,), device=packed.device)
+    _lib.check(_lib.lib().fagp_gram_unpack(_lib.ptr(packed), basis.ref, _lib.ptr(G), _lib.ptr(t),
+                                           _lib.stream_handle()), "gram_unpack")
+    return G, t
 
 
 def _raise_factor(st, piv, m):
@@ -197,7 +206,7 @@ def _raise_factor(st, piv, m):
 def _apply_fault(f, stream=None):
     if _FAULT_FLIP_MEAN_SIGN:
         f.w.neg_()
-        _lib.check(_lib.lib().fagp_set_mean_weights(_lib.ptr(f.predict_op), _lib.ptr(f.w), f.m,
+        _lib.check(_lib.lib().fagp_set_mean_weights(_lib.ptr(f.predict_op), _lib.ptr(f.w), f.basis.ref,
                                                     _lib.stream_handle(stream)), "set_mean_weights")
 
 

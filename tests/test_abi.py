@@ -37,11 +37,17 @@ def test_host_only_entry_points():
     assert lib.fagp_abi_version() == _lib.ABI_VERSION
     assert lib.fagp_strerror(_lib.FAGP_ENOTPD) == b"matrix is not positive definite"
     assert lib.fagp_basis_table_len(3, 10) == 3 * 3 + 30
-    assert lib.fagp_gram_packed_len(1000) == 1001 * 1002 // 2
-    assert lib.fagp_predict_operand_len(1000) == 1024 * 1024
+    b3 = _lib.FagpBasis(3, 10, 1000, 8)  # table pointer is not dereferenced by host-only calls
+    assert lib.fagp_gram_len(ctypes.byref(b3)) == 55**3 + 1000  # pair form [H | t]
+    b1 = _lib.FagpBasis(1, 10, 10, 8)
+    assert lib.fagp_gram_len(ctypes.byref(b1)) == 11 * 12 // 2  # p == 1: packed [Phi | r] SYRK
+    assert lib.fagp_predict_operand_len(ctypes.byref(b1)) == 32 * 128
+    assert lib.fagp_predict_operand_len(ctypes.byref(b3)) >= 55**3 + 1000
     assert lib.fagp_factor_workspace_size(1000) > 0
+    assert lib.fagp_table_width(3, 10) == 34
     b = _lib.FagpBasis(3, 10, 1000, None)
     assert lib.fagp_gram_workspace_size(1000000, ctypes.byref(b)) == 0  # null table is rejected
+    assert lib.fagp_gram_workspace_size(1000000, ctypes.byref(b3)) > 0
     buf = (ctypes.c_int64 * 24)()
     assert lib.fagp_multi_indices(2, 3, buf) == 0
     assert list(buf)[:6] == [1, 1, 1, 1, 1, 2]

@@ -15,7 +15,7 @@ import fagp_oracle as O
 import paper_2403_12797_b200 as F
 from conftest import CASE_NAMES, rel_err, scaled_err
 from paper_2403_12797_b200 import _device as dev
-from paper_2403_12797_b200.posterior import _stage_tables, factor_packed, gram_packed
+from paper_2403_12797_b200.posterior import _stage_tables, factor_packed, gram_packed, gram_unpack
 
 pytestmark = pytest.mark.gpu
 
@@ -23,13 +23,9 @@ MEAN_VAR_RTOL = 1e-9
 GRAM_TOL = 1e-12
 
 
-def unpack(packed, m):
-    me = m + 1
-    full = np.zeros((me, me))
-    iu = np.triu_indices(me)
-    full[iu] = packed
-    full = full + np.triu(full, 1).T
-    return full[:m, :m], full[:m, m]
+def unpack(basis, packed):
+    G, t = gram_unpack(basis, packed)
+    return dev.to_host(G), dev.to_host(t)
 
 
 def test_library_is_the_cuda_extension():
@@ -55,8 +51,7 @@ def test_gram_and_t_parity(cases, name):
     basis = F.Basis(c.kernel(), c.M, c.variant)
     X = dev.to_device(c.X)
     T = _stage_tables(basis, X, None, None)
-    packed = dev.to_host(gram_packed(basis, T, dev.to_device(c.y), c.mean_const))
-    G, t = unpack(packed, basis.m)
+    G, t = unpack(basis, gram_packed(basis, T, dev.to_device(c.y), c.mean_const))
     assert scaled_err(t, c.ref["t"]) <= GRAM_TOL
     assert scaled_err(np.diag(G), c.ref["G_diag"]) <= GRAM_TOL
     rows = [0, 1, basis.m // 2, basis.m - 1]
@@ -71,7 +66,9 @@ def test_gram_and_t_parity(cases, name):
 def test_eigenvalues_bit_exact(cases, name):
     c = cases[name]
     basis = F.Basis(c.kernel(), c.M, c.variant)
-    f, st, _ = factor_packed(basis, dev.zeros((int(basis.m + 1) * (basis.m + 2) // 2,)), c.noise_var, 0.0, 0)
+    from paper_2403_12797_b200 import _lib
+
+    f, st, _ = factor_packed(basis, dev.zeros((int(_lib.lib().fagp_gram_len(basis.ref)),)), c.noise_var, 0.0, 0)
     assert np.array_equal(dev.to_host(f.lam), c.ref["lam"])
     assert np.array_equal(dev.to_host(f.lam_floored), c.ref["lam_floored"])
     assert np.array_equal(dev.to_host(f.sqrt_lam), np.sqrt(c.ref["lam_floored"]))
@@ -110,7 +107,7 @@ def test_weights_match_oracle(cases):
     T = _stage_tables(basis, dev.to_device(c.X), None, None)
     packed = gram_packed(basis, T, dev.to_device(c.y), c.mean_const)
     f, st, _ = factor_packed(basis, packed, c.noise_var, c.mean_const, c.N)
-    G, t = unpack(dev.to_host(packed), basis.m)
+    G, t = unpack(basis, packed)
     o = O.factor(G, t, c.ref["lam"], c.noise_var)
     assert scaled_err(dev.to_host(f.w), o["w"]) < 1e-10
     Lg = dev.to_host(f.L)
