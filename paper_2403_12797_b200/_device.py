@@ -51,13 +51,55 @@ def to_device(a, device=None, dtype="float64"):
 
 
 def to_host(t):
-    """CUDA tensor -> numpy (synchronising copy)."""
-    return t.detach().cpu().numpy()
+    """CUDA tensor -> numpy.  Large results land in page-locked memory from torch's pinned
+    caching allocator (DMA at full link speed, no first-touch page faults); the returned array
+    keeps that buffer alive, and it returns to the cache when the array is dropped."""
+    torch = _torch()
+    t = t.detach()
+    if not t.is_cuda or t.numel() * t.element_size() < (1 << 20):
+        return t.cpu().numpy()
+    out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    out.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    return out.numpy()
+
+
+def upload_async(a, device=None):
+    """Start the H2D copy of a host tensor/array on a side stream; returns (device tensor,
+    event).  Pinned sources copy asynchronously; the caller waits on the event."""
+    torch = _torch()
+    dev = device_of(device)
+    if isinstance(a, torch.Tensor) and a.is_cuda:
+        return to_device(a, dev), None
+    main = torch.cuda.current_stream(dev)
+    side = torch.cuda.Stream(device=dev)
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        if isinstance(a, torch.Tensor):
+            src = a.to(dtype=torch.float64).contiguous()
+        else:
+            src = torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64)))
+        d = src.to(dev, non_blocking=src.is_pinned())
+        ev = torch.cuda.Event()
+        ev.record(side)
+    d.record_stream(main)
+    return d, ev
 
 
 def is_tensor(a):
     torch = _torch()
     return isinstance(a, torch.Tensor)
+
+
+def points_shape(X, p, name):
+    """Validate an (N, p) point set's shape without copying it (posterior.py:93-97)."""
+    torch = _torch()
+    if isinstance(X, torch.Tensor):
+        shape = tuple(X.shape) if X.dim() == 2 else ((1, X.shape[0]) if X.dim() == 1 and X.numel() else (0, p))
+    else:
+        shape = np.atleast_2d(np.asarray(X, dtype=float)).shape
+    if len(shape) != 2 or shape[1] != p:
+        raise ValueError(f"{name} has {shape[-1]} columns, expected p={p}")
 
 
 def points(X, p, name):

@@ -155,67 +155,65 @@ __device__ __forceinline__ void warp_trinv(const double (*S)[33], double (*Xs)[3
 }
 
 // One step of the blocked right-looking Cholesky (NB = 32), one warp per CTA.  Every CTA
-// factors the 32x32 diagonal block A[k0:k0+nb, k0:k0+nb] redundantly in registers (lane i
-// holds row i; column j's multipliers are broadcast with shuffles), which costs ~1 us and
-// saves a launch + a grid-wide dependency.  CTA 0 writes L11; CTA b >= 1 solves panel
-// row-block b-1, L21 = A21 L11^{-T}, by forward substitution against L11 in shared memory.
-// A breakdown (pivot <= 0 or NaN, as LAPACK dpotrf2 tests it) records the 1-based global
-// column in *info; every later kernel then exits immediately.
+// factors the 32x32 diagonal block A[k0:k0+nb, k0:k0+nb] redundantly (lane i owns row i of
+// a shared-memory copy; the loops are runtime-uniform so the SASS stays small enough for the
+// instruction cache), which costs a few us and saves a launch plus a grid-wide dependency.
+// CTA 0 writes L11; CTA b >= 1 solves panel row-block b-1, L21 = A21 L11^{-T}, by forward
+// substitution.  A breakdown (pivot <= 0 or NaN, as LAPACK dpotrf2 tests it) records the
+// 1-based global column in *info; every later kernel then exits immediately.
 __global__ void __launch_bounds__(32) chol_panel_kernel(double* __restrict__ A, int64_t lda, int64_t m, int64_t k0,
                                                         int nb, int* info) {
   if (*info) return;
-  __shared__ double Ls[32][33];
+  __shared__ double Ls[32][33];  // L11 (for the panel solve)
+  __shared__ double dinv[32];
   const int lane = threadIdx.x;
+  // Lane i holds the not-yet-factored part of row i in registers, shifted so that r[0] is
+  // always the current column j: every register index is a compile-time constant while the
+  // j loop stays rolled (small SASS, no shared-memory aliasing in the update).
   double r[32];
 #pragma unroll
   for (int c = 0; c < 32; ++c)
     r[c] = (lane < nb && c < nb) ? (c <= lane ? A[(k0 + lane) * lda + k0 + c] : 0.0) : (lane == c ? 1.0 : 0.0);
-#pragma unroll
+#pragma unroll 1
   for (int j = 0; j < 32; ++j) {
-    const double d = __shfl_sync(0xffffffffu, r[j], j);
+    const double d = __shfl_sync(0xffffffffu, r[0], j);
     if (!(d > 0.0)) {  // warp-uniform; padding pivots are exactly 1
       if (blockIdx.x == 0 && lane == 0) atomicCAS(info, 0, int(k0 + j + 1));
       return;
     }
     const double ljj = sqrt(d);
-    if (lane == j) r[j] = ljj;
-    else if (lane > j) r[j] = r[j] / ljj;
+    const double inv = 1.0 / ljj;
+    const double lij = lane == j ? ljj : (lane > j ? r[0] * inv : 0.0);
+    Ls[lane][j] = lij;
+    if (lane == j) dinv[j] = inv;
+    // trailing update of this lane's row: a_{i, j+k} -= l_ij l_{j+k, j}, then shift left
 #pragma unroll
-    for (int k = j + 1; k < 32; ++k) {
-      const double lkj = __shfl_sync(0xffffffffu, r[j], k);
-      if (lane >= k) r[k] = fma(-r[j], lkj, r[k]);
+    for (int k = 1; k < 32; ++k) {
+      const double lkj = __shfl_sync(0xffffffffu, lij, (j + k) & 31);
+      r[k - 1] = (lane >= j + k && j + k < 32) ? fma(-lij, lkj, r[k]) : r[k];
     }
+    r[31] = 0.0;
   }
+  __syncwarp();
   if (blockIdx.x == 0) {
-    if (lane < nb) {
-#pragma unroll
-      for (int c = 0; c < 32; ++c)
-        if (c <= lane && c < nb) A[(k0 + lane) * lda + k0 + c] = r[c];
-    }
+    if (lane < nb)
+      for (int c = 0; c <= lane; ++c) A[(k0 + lane) * lda + k0 + c] = Ls[lane][c];
     return;
   }
-#pragma unroll
-  for (int c = 0; c < 32; ++c) Ls[lane][c] = r[c];
-  __syncwarp();
+  // panel row: x L11^T = a, right-looking with the same shifted-register scheme
   const int64_t i0 = k0 + nb + int64_t(blockIdx.x - 1) * 32 + lane;
-  if (i0 >= m) return;
-  double* row = A + i0 * lda + k0;
-  double x[32];
+  const bool solve = i0 < m;
+  double* row = A + (solve ? i0 : 0) * lda + k0;
 #pragma unroll
-  for (int c = 0; c < 32; ++c) x[c] = c < nb ? row[c] : 0.0;
+  for (int c = 0; c < 32; ++c) r[c] = (solve && c < nb) ? row[c] : 0.0;
+#pragma unroll 1
+  for (int j = 0; j < nb; ++j) {
+    const double xj = r[0] * dinv[j];
+    if (solve) row[j] = xj;
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    double v0 = x[j], v1 = 0.0;  // two partial sums shorten the dependency chain
-#pragma unroll
-    for (int l = 0; l < j; ++l) {
-      if (l & 1) v1 = fma(-x[l], Ls[j][l], v1);
-      else v0 = fma(-x[l], Ls[j][l], v0);
-    }
-    x[j] = (v0 + v1) / Ls[j][j];
+    for (int k = 1; k < 32; ++k) r[k - 1] = (j + k < 32) ? fma(-xj, Ls[(j + k) & 31][j], r[k]) : r[k];
+    r[31] = 0.0;
   }
-#pragma unroll
-  for (int c = 0; c < 32; ++c)
-    if (c < nb) row[c] = x[c];
 }
 
 int potrf_blocked(double* A, int64_t m, int64_t lda, int* info, cudaStream_t s) {

@@ -128,17 +128,19 @@ pair_gram_kernel(const double* __restrict__ T, int64_t N, BasisView b, PairPlan 
   const int64_t r0 = int64_t(chunk) * pl.chunk_rows;
   const int64_t r1 = tmin<int64_t>(N, r0 + pl.chunk_rows);
 
-  // generator role: A column tid; B column tid (first GBN threads)
+  // generator role: A column tid (4 rows per k-step); B column tid % GBN for the first
+  // 2 GBN threads, which split each k-step's 4 rows in halves (balances the warps)
   int offA[FA], offB[FB];
-  const bool genB = tid < GBN;
+  const bool genB = tid < 2 * GBN;
+  const int bcol = tid % GBN, bhalf = tid / GBN;
   if (tile < npair) {
     const int ta = tile / pl.gtB, tb = tile % pl.gtB;
     combo_offsets<FA>(int64_t(ta) * GBM + tid, pl.GA, 0, M, pl.P, pM, offA);
-    combo_offsets<FB>(int64_t(tb) * GBN + tid, pl.GB, pl.pL, M, pl.P, pM, offB);
+    combo_offsets<FB>(int64_t(tb) * GBN + bcol, pl.GB, pl.pL, M, pl.P, pM, offB);
   } else {
     const int ta = (tile - npair) / pl.stB, tb = (tile - npair) % pl.stB;
     single_offsets<FA>(int64_t(ta) * GBM + tid, pl.SA, 0, M, pM, false, offA);
-    single_offsets<FB>(int64_t(tb) * GBN + tid, pl.SB, pl.pL, M, pM, true, offB);
+    single_offsets<FB>(int64_t(tb) * GBN + bcol, pl.SB, pl.pL, M, pM, true, offB);
   }
 
   auto load_tab = [&](int slot, int64_t base) {
@@ -160,11 +162,16 @@ pair_gram_kernel(const double* __restrict__ T, int64_t N, BasisView b, PairPlan 
 #pragma unroll
       for (int f = 1; f < FA; ++f) v = __dmul_rn(v, Tr[offA[f]]);
       As[stage * GA_STAGE + k * GSPA + tid] = v;
-      if (genB) {
+    }
+    if (genB) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int k = kk * 4 + bhalf * 2 + i;
+        const double* Tr = tb_ + k * W;
         double u = Tr[offB[0]];
 #pragma unroll
         for (int f = 1; f < FB; ++f) u = __dmul_rn(u, Tr[offB[f]]);
-        Bs[stage * GB_STAGE + k * GSPB + tid] = u;
+        Bs[stage * GB_STAGE + k * GSPB + bcol] = u;
       }
     }
   };

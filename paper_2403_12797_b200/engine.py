@@ -66,10 +66,17 @@ class PosteriorEngine:
     # -- stages (each usable alone, e.g. for per-kernel timing) --------------------------
     def stage_tables(self, X, y, Xs, stream=None):
         """K0 for train (with the residual column r = y - c) and test rows."""
+        self.stage_train_table(X, y, stream)
+        self.stage_test_table(Xs, stream)
+
+    def stage_train_table(self, X, y, stream=None):
         L, s, b = _lib.lib(), _lib.stream_handle(stream), self.basis
         if self.N:
             _lib.check(L.fagp_basis_eval(_lib.ptr(X), self.N, b.ref, _lib.ptr(y), self.mean_const, _lib.ptr(self.T),
                                          self._flag(0), s), "basis_eval")
+
+    def stage_test_table(self, Xs, stream=None):
+        L, s, b = _lib.lib(), _lib.stream_handle(stream), self.basis
         if self.Ns:
             _lib.check(L.fagp_basis_eval(_lib.ptr(Xs), self.Ns, b.ref, None, 0.0, _lib.ptr(self.Ts), self._flag(1), s),
                        "basis_eval")
@@ -107,13 +114,21 @@ class PosteriorEngine:
                        "predict")
 
     # -- the whole step -------------------------------------------------------------------
-    def run(self, X, y, Xs, fault_flip=False):
-        """One posterior evaluation from device-resident inputs; returns device (mean, var)."""
+    def run(self, X, y, Xs, fault_flip=False, xs_ready=None):
+        """One posterior evaluation from device-resident inputs; returns device (mean, var).
+
+        The test table is evaluated after the factorisation, so an X* upload still in
+        flight on another stream (``xs_ready``: its event) overlaps the Gram contraction."""
+        import torch
+
         self.flags.zero_()
-        self.stage_tables(X, y, Xs)
+        self.stage_train_table(X, y)
         self.stage_gram()
         self.stage_reduce()
         st = self.stage_factor()
+        if xs_ready is not None:
+            torch.cuda.current_stream().wait_event(xs_ready)
+        self.stage_test_table(Xs)
         if st != _lib.FAGP_OK:
             self.raise_errors(X, Xs, factor_failed=True)
         if fault_flip:

@@ -333,14 +333,17 @@ def fagp_posterior(train, Xstar, model, backend=None, want_cov=False, method="sc
     kernel = as_ard(model.kernel)
     p = kernel.p
     X = dev.points(train.X, p, "train.X")
-    Xs = dev.points(Xstar, p, "Xstar")
+    dev.points_shape(Xstar, p, "Xstar")
+    Xs, xs_ready = dev.upload_async(Xstar if dev.is_tensor(Xstar) else np.atleast_2d(np.asarray(Xstar, dtype=float)),
+                                    X.device)
+    Xs = Xs.reshape(-1, p)
     N, Ns = int(X.shape[0]), int(Xs.shape[0])
     yd = _check_y(train.y, N)
     _budget(N, model.n_eigen, p, memory_cap)
     _budget(Ns, model.n_eigen, p, memory_cap)
     eng = PosteriorEngine(kernel, model.n_eigen, N, Ns, model.noise_var, model.mean_const, delta2_variant,
                           device=X.device, group=group, want_var=want_var)
-    mean, var = eng.run(X, yd, Xs, fault_flip=_FAULT_FLIP_MEAN_SIGN)
+    mean, var = eng.run(X, yd, Xs, fault_flip=_FAULT_FLIP_MEAN_SIGN, xs_ready=xs_ready)
     eng.check(X, Xs)
     cov = None
     if want_cov:
