@@ -93,7 +93,7 @@ def load(path=None):
     global _LIB
     if _LIB is not None and path is None:
         return _LIB
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else Path(os.environ.get("FAGP_LIB_PATH", str(LIB_PATH)))
     if not p.exists():
         raise ExtensionMissing(
             f"{p} is missing: build it with `python -m paper_2403_12797_b200._build` "

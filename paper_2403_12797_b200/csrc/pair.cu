@@ -63,11 +63,11 @@ template <int F>
 __device__ __forceinline__ void combo_offsets(int64_t col, int64_t ncols, int d0, int M, int P, int pM,
                                               int (&off)[F]) {
   static_assert(F % 2 == 0, "two factors per dimension");
-  int64_t q = col < ncols ? col : 0;
+  unsigned q = col < ncols ? unsigned(col) : 0u;  // pair-combo counts stay below 2^31 (enabled())
 #pragma unroll
   for (int e = F / 2 - 1; e >= 0; --e) {
-    const int pi = int(q % P);
-    q /= P;
+    const int pi = int(q % unsigned(P));
+    q /= unsigned(P);
     int a, b;
     pair_decode(pi, M, a, b);
     off[2 * e] = (d0 + e) * M + a;
@@ -207,10 +207,146 @@ pair_gram_kernel(const double* __restrict__ T, int64_t N, BasisView b, PairPlan 
       for (int s = 0; s < GFM; ++s)
 #pragma unroll
         for (int t = 0; t < GFN; ++t) dmma_8x8x4(acc[s][t][0], acc[s][t][1], a[s], bb[t]);
+#ifndef FAGP_DIAG_NOGEN
       gen_rows(nxt, kk);  // chunk n+1 (garbage past the last chunk, never read)
+#endif
     }
     cp_async_wait<0>();
     __syncthreads();
+  }
+  double* out = ws + (size_t(chunk) * ntiles + tile) * size_t(GBM * GBN);
+#pragma unroll
+  for (int s = 0; s < GFM; ++s) {
+    const int i = warp * 32 + s * 8 + (lane >> 2);
+#pragma unroll
+    for (int t = 0; t < GFN; ++t) {
+      const int j = t * 8 + 2 * (lane & 3);
+      *reinterpret_cast<double2*>(out + i * GBN + j) = make_double2(acc[s][t][0], acc[s][t][1]);
+    }
+  }
+}
+
+// KP1 (warp-specialised): 4 consumer warps issue only fragment loads and DMMAs; 2 producer
+// warps stage table rows (cp.async), generate the U_L / U_R tiles of each 16-row chunk into
+// a 3-stage shared-memory ring and hand them over with named barriers (FULL[s] / EMPTY[s]),
+// so generation never interrupts the tensor-core instruction stream.
+constexpr int WS_STAGES = 3, WS_CONS = 4, WS_PROD = 2;
+constexpr int WS_NT = 32 * (WS_CONS + WS_PROD);
+constexpr int WS_PT = 32 * WS_PROD;  // producer threads
+
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
+inline size_t gram_ws_smem(int W) {
+  return size_t(WS_STAGES) * (GA_STAGE + GB_STAGE + size_t(GBK) * W) * sizeof(double);
+}
+
+template <int FA, int FB>
+__global__ void __launch_bounds__(WS_NT, 2)
+pair_gram_ws_kernel(const double* __restrict__ T, int64_t N, BasisView b, PairPlan pl, double* __restrict__ ws) {
+  extern __shared__ double sm[];
+  const int M = b.M, pM = b.p * M, W = table_width(b.p, M);
+  double* As = sm;                                   // [STAGES][GBK][GSPA]
+  double* Bs = As + WS_STAGES * GA_STAGE;            // [STAGES][GBK][GSPB]
+  double* Tb = Bs + WS_STAGES * GB_STAGE;            // [STAGES][GBK][W]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int npair = pl.gtA * pl.gtB;
+  const int ntiles = npair + pl.stA * pl.stB;
+  const int tile = blockIdx.x % ntiles, chunk = blockIdx.x / ntiles;
+  const int64_t r0 = int64_t(chunk) * pl.chunk_rows;
+  const int64_t r1 = tmin<int64_t>(N, r0 + pl.chunk_rows);
+  const int nchunks = int(ceil_div(tmax<int64_t>(r1 - r0, 0), GBK));
+  constexpr int FULL0 = 1, EMPTY0 = 1 + WS_STAGES, PROD = 1 + 2 * WS_STAGES;
+
+  if (warp >= WS_CONS) {
+    // ---------------- producers ----------------
+    const int pt = tid - 32 * WS_CONS;  // 0..63
+    int offA0[FA], offA1[FA], offB[FB];
+    const bool genB = pt < GBN;
+    if (tile < npair) {
+      const int ta = tile / pl.gtB, tb = tile % pl.gtB;
+      combo_offsets<FA>(int64_t(ta) * GBM + pt, pl.GA, 0, M, pl.P, pM, offA0);
+      combo_offsets<FA>(int64_t(ta) * GBM + pt + WS_PT, pl.GA, 0, M, pl.P, pM, offA1);
+      combo_offsets<FB>(int64_t(tb) * GBN + pt, pl.GB, pl.pL, M, pl.P, pM, offB);
+    } else {
+      const int ta = (tile - npair) / pl.stB, tb = (tile - npair) % pl.stB;
+      single_offsets<FA>(int64_t(ta) * GBM + pt, pl.SA, 0, M, pM, false, offA0);
+      single_offsets<FA>(int64_t(ta) * GBM + pt + WS_PT, pl.SA, 0, M, pM, false, offA1);
+      single_offsets<FB>(int64_t(tb) * GBN + pt, pl.SB, pl.pL, M, pM, true, offB);
+    }
+    auto load_tab = [&](int slot, int64_t base) {
+      double* dst = Tb + slot * (GBK * W);
+      const int nrows = int(tmax<int64_t>(0, tmin<int64_t>(GBK, r1 - base)));
+      const int nd = nrows * W;
+      const double* src = T + base * W;
+      for (int i = pt; i < nd / 2; i += WS_PT) cp_async_16(dst + 2 * i, src + 2 * i);
+      for (int i = nd + pt; i < GBK * W; i += WS_PT) dst[i] = 0.0;
+      cp_async_commit();
+    };
+    if (nchunks > 0) load_tab(0, r0);
+    for (int n = 0; n < nchunks; ++n) {
+      const int slot = n % WS_STAGES;
+      // table rows of chunk n are in Tb[slot]; prefetch chunk n+1's into the next slot (its
+      // previous content, chunk n+1-STAGES, was consumed by this warp group long ago)
+      if (n + 1 < nchunks) load_tab((n + 1) % WS_STAGES, r0 + int64_t(n + 1) * GBK);
+      if (n + 1 < nchunks) cp_async_wait<1>(); else cp_async_wait<0>();
+      named_sync(PROD, WS_PT);  // chunk n's table visible to all producers
+      if (n >= WS_STAGES) named_sync(EMPTY0 + slot, WS_NT);  // consumers released this slot
+      const double* tb = Tb + slot * (GBK * W);
+      double* Ad = As + slot * GA_STAGE;
+      double* Bd = Bs + slot * GB_STAGE;
+#pragma unroll 4
+      for (int k = 0; k < GBK; ++k) {
+        const double* Tr = tb + k * W;
+        double v0 = Tr[offA0[0]], v1 = Tr[offA1[0]];
+#pragma unroll
+        for (int f = 1; f < FA; ++f) {
+          v0 = __dmul_rn(v0, Tr[offA0[f]]);
+          v1 = __dmul_rn(v1, Tr[offA1[f]]);
+        }
+        Ad[k * GSPA + pt] = v0;
+        Ad[k * GSPA + pt + WS_PT] = v1;
+        if (genB) {
+          double u = Tr[offB[0]];
+#pragma unroll
+          for (int f = 1; f < FB; ++f) u = __dmul_rn(u, Tr[offB[f]]);
+          Bd[k * GSPB + pt] = u;
+        }
+      }
+      named_arrive(FULL0 + slot, WS_NT);
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  double acc[GFM][GFN][2];
+#pragma unroll
+  for (int s = 0; s < GFM; ++s)
+#pragma unroll
+    for (int t = 0; t < GFN; ++t) acc[s][t][0] = acc[s][t][1] = 0.0;
+  for (int n = 0; n < nchunks; ++n) {
+    const int slot = n % WS_STAGES;
+    named_sync(FULL0 + slot, WS_NT);
+    const double* Ab = As + slot * GA_STAGE + (lane & 3) * GSPA + warp * 32 + (lane >> 2);
+    const double* Bb = Bs + slot * GB_STAGE + (lane & 3) * GSPB + (lane >> 2);
+#pragma unroll
+    for (int kk = 0; kk < GBK / 4; ++kk) {
+      double a[GFM], bb[GFN];
+#pragma unroll
+      for (int s = 0; s < GFM; ++s) a[s] = Ab[kk * 4 * GSPA + s * 8];
+#pragma unroll
+      for (int t = 0; t < GFN; ++t) bb[t] = Bb[kk * 4 * GSPB + t * 8];
+#pragma unroll
+      for (int s = 0; s < GFM; ++s)
+#pragma unroll
+        for (int t = 0; t < GFN; ++t) dmma_8x8x4(acc[s][t][0], acc[s][t][1], a[s], bb[t]);
+    }
+    // release the slot unless the producers will never refill it
+    if (n + WS_STAGES < nchunks) named_arrive(EMPTY0 + slot, WS_NT);
   }
   double* out = ws + (size_t(chunk) * ntiles + tile) * size_t(GBM * GBN);
 #pragma unroll
@@ -340,19 +476,23 @@ __global__ void ctilde_kernel(const double* __restrict__ D, int64_t ldd, const d
 // KP5: var for BM test rows: Y = Q_K Ct over K chunks (Q_K generated from the staged table
 // rows: product of the pair values of dims >= pN), then var_i = sigma2 sum_nu Y[i,nu] E[i,nu]
 // with E = product of the pair values of dims < pN.  Ct streams from L2 by cp.async.
-constexpr int VBM = 128, VBN = 56, VBK = 16, VNT = 128;  // 4 warps, warp tile 32 x 56
+constexpr int VBM = 128, VBN = 56, VBK = 16;
 constexpr int VASP = VBK + 4, VBSP = VBN + 12;           // 20, 68 (% 16 == 4)
-constexpr int VFM = 4, VFN = 7;
+constexpr int VFN = 7;
 constexpr int VA_STAGE = VBM * VASP, VB_STAGE = VBK * VBSP;
 
 inline size_t var_smem(int W) {
   return (size_t(2) * (VA_STAGE + VB_STAGE) + size_t(VBM) * W + VBM) * sizeof(double);
 }
 
-template <int FK, int FE>
-__global__ void __launch_bounds__(VNT, 2)
+template <int FK, int FE, int NW>
+__global__ void __launch_bounds__(32 * NW, 2)
 pair_var_kernel(const double* __restrict__ Ts, int64_t Ns, BasisView b, PairPlan pl, const double* __restrict__ Ct,
                 double sigma2, double* __restrict__ var, uint32_t* flags) {
+  constexpr int VNT = 32 * NW;             // NW warps stacked along the rows
+  constexpr int VWM = VBM / NW, VFM = VWM / 8;
+  constexpr int GGRP = VNT / VBK;          // generator row groups
+  constexpr int GPERKK = VBM / GGRP / (VBK / 4);  // generated rows per thread per k-step
   extern __shared__ double sm[];
   double* As = sm;                     // [2][VBM][VASP]
   double* Bs = sm + 2 * VA_STAGE;      // [2][VBK][VBSP]
@@ -368,7 +508,7 @@ pair_var_kernel(const double* __restrict__ Ts, int64_t Ns, BasisView b, PairPlan
     for (int i = nd + tid; i < VBM * W; i += VNT) tsm[i] = 0.0;
     cp_async_commit();
   }
-  const int gk = tid % VBK, gr0 = tid / VBK;  // generator: K column gk, rows gr0 + 8 q (q < 16)
+  const int gk = tid % VBK, gr0 = tid / VBK;  // generator: K column gk, rows gr0 + GGRP q
   const int nkc = int(pl.KP / VBK);
   const int ntn = int(pl.NP / VBN);
 
@@ -383,8 +523,8 @@ pair_var_kernel(const double* __restrict__ Ts, int64_t Ns, BasisView b, PairPlan
   auto gen_rows = [&](int stage, const int (&off)[FK], int q0) {
     double* dst = As + stage * VA_STAGE + gk;
 #pragma unroll
-    for (int qi = 0; qi < 4; ++qi) {
-      const int r = gr0 + 8 * (q0 + qi);
+    for (int qi = 0; qi < GPERKK; ++qi) {
+      const int r = gr0 + GGRP * (q0 + qi);
       const double* Tr = tsm + r * W;
       double v = Tr[off[0]];
 #pragma unroll
@@ -409,7 +549,7 @@ pair_var_kernel(const double* __restrict__ Ts, int64_t Ns, BasisView b, PairPlan
     int off[FK];
     combo_offsets<FK>(gk, pl.KR, pl.pN, M, pl.P, pM, off);
 #pragma unroll
-    for (int kk = 0; kk < VBK / 4; ++kk) gen_rows(0, off, kk * 4);
+    for (int kk = 0; kk < VBK / 4; ++kk) gen_rows(0, off, kk * GPERKK);
   }
   cp_async_wait<0>();
   __syncthreads();
@@ -425,7 +565,7 @@ pair_var_kernel(const double* __restrict__ Ts, int64_t Ns, BasisView b, PairPlan
     if (has_next) load_b(buf ^ 1, int64_t(kc2) * VBK, int64_t(tn2) * VBN);
     int off[FK];
     combo_offsets<FK>(int64_t(kc2) * VBK + gk, pl.KR, pl.pN, M, pl.P, pM, off);
-    const double* Ab = As + buf * VA_STAGE + (warp * 32 + (lane >> 2)) * VASP + (lane & 3);
+    const double* Ab = As + buf * VA_STAGE + (warp * VWM + (lane >> 2)) * VASP + (lane & 3);
     const double* Bb = Bs + buf * VB_STAGE + (lane & 3) * VBSP + (lane >> 2);
 #pragma unroll
     for (int kk = 0; kk < VBK / 4; ++kk) {
@@ -438,7 +578,9 @@ pair_var_kernel(const double* __restrict__ Ts, int64_t Ns, BasisView b, PairPlan
       for (int s = 0; s < VFM; ++s)
 #pragma unroll
         for (int t = 0; t < VFN; ++t) dmma_8x8x4(acc[s][t][0], acc[s][t][1], a[s], bb[t]);
-      gen_rows(buf ^ 1, off, kk * 4);
+#ifndef FAGP_DIAG_NOGEN
+      gen_rows(buf ^ 1, off, kk * GPERKK);
+#endif
     }
     cp_async_wait<0>();
     __syncthreads();
@@ -453,7 +595,7 @@ pair_var_kernel(const double* __restrict__ Ts, int64_t Ns, BasisView b, PairPlan
           combo_offsets<FE>(nu, pl.NR, 0, M, pl.P, pM, offe);
 #pragma unroll
           for (int s = 0; s < VFM; ++s) {
-            const double* Tr = tsm + (warp * 32 + s * 8 + (lane >> 2)) * W;
+            const double* Tr = tsm + (warp * VWM + s * 8 + (lane >> 2)) * W;
             double ev = Tr[offe[0]];
 #pragma unroll
             for (int f = 1; f < FE; ++f) ev = __dmul_rn(ev, Tr[offe[f]]);
@@ -482,7 +624,7 @@ pair_var_kernel(const double* __restrict__ Ts, int64_t Ns, BasisView b, PairPlan
   if ((lane & 3) == 0) {
 #pragma unroll
     for (int s = 0; s < VFM; ++s) {
-      const int64_t row = row0 + warp * 32 + s * 8 + (lane >> 2);
+      const int64_t row = row0 + warp * VWM + s * 8 + (lane >> 2);
       if (row < Ns) {
         const double vv = sigma2 * vsum[s];
         var[row] = vv;
@@ -570,8 +712,9 @@ static int64_t ipow(int64_t b, int e) {
 bool enabled(int p, int M) {
   if (p < 2 || p > 8 || M < 1) return false;
   const int64_t P = int64_t(M) * (M + 1) / 2;
-  // every split must keep factor counts within the instantiated templates (<= 8 factors)
-  return ipow(P, p) < (int64_t(1) << 40);
+  // every split keeps factor counts within the instantiated templates (<= 8 factors) and
+  // pair-combo indices in 31 bits
+  return ipow(P, p) < (int64_t(1) << 31);
 }
 
 PairPlan make_plan(int64_t N, int p, int M) {
@@ -648,19 +791,39 @@ size_t gram_workspace(int64_t N, const fagp_basis* b) {
   return size_t(pl.S) * tiles * GBM * GBN * sizeof(double);
 }
 
+static bool gram_ws_enabled() {
+  // Experimental: the warp-specialised kernel measured 17.6 ms vs 13.8 ms for the
+  // interleaved one at C3 (producer DMULs lose the FP64 pipe to the DMMA stream); opt in
+  // with FAGP_GRAM_WS=1.
+  const char* e = getenv("FAGP_GRAM_WS");
+  return e && e[0] == '1';
+}
+
 template <int FA>
 static int launch_gram_fb(int FB, const double* T, int64_t N, const fagp_basis* b, const PairPlan& pl, double* ws,
                           size_t smem, unsigned grid, cudaStream_t s) {
-  auto go = [&](auto kern) -> int {
-    FAGP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    kern<<<grid, GNT, smem, s>>>(T, N, view(b), pl, ws);
+  const int W = table_width(b->p, b->M);
+  const bool wsk = gram_ws_enabled() && gram_ws_smem(W) * 2 <= 227 * 1024;
+  auto go = [&](auto kern, int nt, size_t sm) -> int {
+    FAGP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+    kern<<<grid, nt, sm, s>>>(T, N, view(b), pl, ws);
     return FAGP_OK;
   };
+  if (wsk) {
+    const size_t sm = gram_ws_smem(W);
+    switch (FB) {
+      case 2: return go(pair_gram_ws_kernel<FA, 2>, WS_NT, sm);
+      case 4: return go(pair_gram_ws_kernel<FA, 4>, WS_NT, sm);
+      case 6: return go(pair_gram_ws_kernel<FA, 6>, WS_NT, sm);
+      case 8: return go(pair_gram_ws_kernel<FA, 8>, WS_NT, sm);
+      default: return FAGP_EUNSUPPORTED;
+    }
+  }
   switch (FB) {
-    case 2: return go(pair_gram_kernel<FA, 2>);
-    case 4: return go(pair_gram_kernel<FA, 4>);
-    case 6: return go(pair_gram_kernel<FA, 6>);
-    case 8: return go(pair_gram_kernel<FA, 8>);
+    case 2: return go(pair_gram_kernel<FA, 2>, GNT, smem);
+    case 4: return go(pair_gram_kernel<FA, 4>, GNT, smem);
+    case 6: return go(pair_gram_kernel<FA, 6>, GNT, smem);
+    case 8: return go(pair_gram_kernel<FA, 8>, GNT, smem);
     default: return FAGP_EUNSUPPORTED;
   }
 }
@@ -734,21 +897,33 @@ int set_weights(double* op, const double* w, const fagp_basis* b, cudaStream_t s
   return FAGP_OK;
 }
 
-template <int FK>
-static int launch_var_fe(int FE, const double* Ts, int64_t Ns, const fagp_basis* b, const PairPlan& pl,
+static int var_warps() {
+  const char* e = getenv("FAGP_VAR_WARPS");  // tuning override: 4 | 8
+  return (e && atoi(e) == 8) ? 8 : 4;
+}
+
+template <int FK, int NW>
+static int launch_var_nw(int FE, const double* Ts, int64_t Ns, const fagp_basis* b, const PairPlan& pl,
                          const double* Ct, double sigma2, double* var, uint32_t* flags, size_t smem, cudaStream_t s) {
   auto go = [&](auto kern) -> int {
     FAGP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    kern<<<unsigned(ceil_div(Ns, VBM)), VNT, smem, s>>>(Ts, Ns, view(b), pl, Ct, sigma2, var, flags);
+    kern<<<unsigned(ceil_div(Ns, VBM)), 32 * NW, smem, s>>>(Ts, Ns, view(b), pl, Ct, sigma2, var, flags);
     return FAGP_OK;
   };
   switch (FE) {
-    case 2: return go(pair_var_kernel<FK, 2>);
-    case 4: return go(pair_var_kernel<FK, 4>);
-    case 6: return go(pair_var_kernel<FK, 6>);
-    case 8: return go(pair_var_kernel<FK, 8>);
+    case 2: return go(pair_var_kernel<FK, 2, NW>);
+    case 4: return go(pair_var_kernel<FK, 4, NW>);
+    case 6: return go(pair_var_kernel<FK, 6, NW>);
+    case 8: return go(pair_var_kernel<FK, 8, NW>);
     default: return FAGP_EUNSUPPORTED;
   }
+}
+
+template <int FK>
+static int launch_var_fe(int FE, const double* Ts, int64_t Ns, const fagp_basis* b, const PairPlan& pl,
+                         const double* Ct, double sigma2, double* var, uint32_t* flags, size_t smem, cudaStream_t s) {
+  if (var_warps() == 4) return launch_var_nw<FK, 4>(FE, Ts, Ns, b, pl, Ct, sigma2, var, flags, smem, s);
+  return launch_var_nw<FK, 8>(FE, Ts, Ns, b, pl, Ct, sigma2, var, flags, smem, s);
 }
 
 int predict(const double* Ts, int64_t Ns, const fagp_basis* b, const double* op, double sigma2, double mean_const,
