@@ -90,6 +90,14 @@ def main():
     mm = 0.5 * (mm + mm.T)
     out["spd/near_singular"] = mm
     out["spd/near_singular_jitter"] = np.array(SpdFactor(mm).jitter)
+    # CSV schema of the bench / plotdata files (the reference's own golden headers)
+    from fagp.bench import PLOTDATA_HEADER, RESULTS_HEADER
+
+    out["headers/results"] = np.array(RESULTS_HEADER)
+    out["headers/plotdata"] = np.array(PLOTDATA_HEADER)
+    gold = Path("/root/reference/pkg/tests/golden")
+    assert (gold / "results_header.txt").read_text().strip() == RESULTS_HEADER
+    assert (gold / "plotdata_header.txt").read_text().strip() == PLOTDATA_HEADER
     np.savez_compressed(OUT, **out)
     print("wrote", OUT, OUT.stat().st_size, "bytes", file=sys.stderr)
 
