@@ -193,6 +193,54 @@ int fagp_predict(const double* Ts, int64_t Ns, const fagp_basis* basis, const do
                  double sigma2, double mean_const, double* mean, double* var, uint32_t* flags,
                  void* stream);
 
+/* ---- (6) method="literal": the reference's cross-check route ---------------------------
+ * posterior.py:236-244 (mean through t1..t5) and 256-260 (inner covariance).  Built from
+ * the Gram/predict kernels above plus these pieces; the Python host (posterior.py in this
+ * package) strings them together exactly as the reference's expressions are ordered. */
+
+/* y = mean_const + Phi x over the rows of a table (backend.gemm(phi, x), posterior.py:241,247).
+ * Phi generated on chip from T; any 1 <= p <= 8.  Sets FAGP_FLAG_PHI_NONFINITE on a
+ * non-finite output. */
+int fagp_phi_matvec(const double* T, int64_t N, const fagp_basis* basis, const double* x,
+                    double mean_const, double* y, uint32_t* flags, void* stream);
+
+/* out = Phi^T v (backend.gemm(phi, v, transpose_a=True), posterior.py:240,243).  Writes v
+ * into T's residual column (T is modified), then runs the Gram kernel's t-tiles only. */
+size_t fagp_phi_tmatvec_workspace_size(int64_t N, const fagp_basis* basis);
+int fagp_phi_tmatvec(double* T, int64_t N, const fagp_basis* basis, const double* v, double* out,
+                     void* workspace, size_t workspace_bytes, void* stream);
+
+/* Elementwise vector ops, numpy rounding (one IEEE op per numpy operator). */
+#define FAGP_VEC_DIV 0        /* out = x / alpha         t1 = r / sigma2 (posterior.py:239) */
+#define FAGP_VEC_SUB_DIV 1    /* out = x - y / alpha     t5 = t1 - t4 / sigma2 (:242)       */
+#define FAGP_VEC_MUL 2        /* out = x * y             w = lam_f * u (:244)               */
+#define FAGP_VEC_SUB 3        /* out = x - y             mid = g - g @ solve(g) (:258)      */
+#define FAGP_VEC_SUB_SCALAR 4 /* out = x - alpha         r = y - mean_const (:229)          */
+int fagp_vec_op(int32_t op, int64_t n, const double* x, const double* y, double alpha, double* out,
+                void* stream);
+
+/* LambdaBarSolve.matrix (posterior.py:184-188): 0.5 (B + B^T), B = diag(1/lam_f) + G/sigma2.
+ * G, out: m x m (distinct buffers). */
+int fagp_lambda_bar(const double* G, const double* lam_f, int64_t m, double sigma2, double* out,
+                    void* stream);
+
+/* inner = 0.5 (A + A^T), A = diag(lam_f) - lam_f[:, None] * mid * lam_f[None, :]
+ * (posterior.py:259-261).  mid, inner: m x m (distinct buffers). */
+int fagp_literal_inner(const double* mid, const double* lam_f, int64_t m, double* inner,
+                       void* stream);
+
+/* A fagp_predict operand (fagp_predict_operand_len doubles) for an explicit inner matrix:
+ * fagp_predict(..., sigma2 = 1.0, ...) then returns var_i = phi*_i^T inner phi*_i and
+ * mean_i = mean_const + phi*_i . w.  Pair form (2 <= p <= 8) only: FAGP_EUNSUPPORTED
+ * otherwise (use fagp_features + fagp_dgemm + fagp_rowdot), returned before the pointer
+ * checks so a call with NULL pointers probes the form. */
+int fagp_inner_operand(const double* inner, const double* w, const fagp_basis* basis,
+                       double* predict_op, void* stream);
+
+/* out[i] = sum_j A[i, j] B[i, j] (A, B: n x k) -- diag(Phi* inner Phi*^T) from
+ * B = Phi* inner (posterior.py:262, cli.py:222). */
+int fagp_rowdot(const double* A, const double* B, int64_t n, int64_t k, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -186,6 +186,34 @@ def posterior(X, y, Xs, eps, rho, n, noise_var, mean_const=0.0, variant=DELTA2_R
     return {"G": G, "t": t, "lam": lam, "mean": mean, "var": var, **fitd}
 
 
+def posterior_literal(X, y, Xs, eps, rho, n, noise_var, mean_const=0.0, variant=DELTA2_RHO_SQUARED):
+    """method="literal" (posterior.py:176, 184-188, 236-247, 256-262): LamBar factorized
+    directly, mean through t1..t5, var = diag(Phi* inner Phi*^T)."""
+    eps = list(eps)
+    rho = list(rho)
+    phi = assemble_phi(X, eps, rho, n, variant)
+    phis = assemble_phi(Xs, eps, rho, n, variant)
+    lam_f = lam_floored(eigenvalues(eps, rho, n, variant))
+    G = phi.T @ phi
+    lb = np.diag(1.0 / lam_f) + G / noise_var
+    lb = 0.5 * (lb + lb.T)
+    L, jit = spd_factor(lb)
+
+    def solve(b):
+        return sla.cho_solve((L, True), b, check_finite=False)
+
+    t1 = (np.asarray(y, dtype=float) - mean_const) / noise_var
+    t4 = phi @ solve(phi.T @ t1)
+    w = lam_f * (phi.T @ (t1 - t4 / noise_var))
+    mean = mean_const + phis @ w
+    g = G / noise_var
+    mid = g - g @ solve(g)
+    inner = np.diag(lam_f) - lam_f[:, None] * mid * lam_f[None, :]
+    inner = 0.5 * (inner + inner.T)
+    var = np.einsum("ij,ij->i", phis @ inner, phis)
+    return {"mean": mean, "var": var, "w": w, "inner": inner, "lambda_bar": lb, "jitter": jit}
+
+
 def useful_flops(N, Ns, m):
     """Algorithmic flop count of the path."""
     return N * m * (m + 1) + 2 * N * m + m**3 / 3 + m**3 / 3 + 2 * Ns * m + Ns * m * (m + 1) + 2 * Ns * m

@@ -86,6 +86,12 @@ def upload_async(a, device=None):
     return d, ev
 
 
+def wait_upload(ev):
+    """Make the current stream wait for an upload_async event (None: nothing pending)."""
+    if ev is not None:
+        _torch().cuda.current_stream().wait_event(ev)
+
+
 def is_tensor(a):
     torch = _torch()
     return isinstance(a, torch.Tensor)

@@ -79,6 +79,14 @@ SIGNATURES = {
     "fagp_trtri_workspace_size": (_SZ, [_I64]),
     "fagp_trtri": (ctypes.c_int, [_P, _P, _I64, _P, _P, _SZ, _P]),
     "fagp_predict": (ctypes.c_int, [_P, _I64, _BASIS, _P, _D, _D, _P, _P, _P, _P]),
+    "fagp_phi_matvec": (ctypes.c_int, [_P, _I64, _BASIS, _P, _D, _P, _P, _P]),
+    "fagp_phi_tmatvec_workspace_size": (ctypes.c_size_t, [_I64, _BASIS]),
+    "fagp_phi_tmatvec": (ctypes.c_int, [_P, _I64, _BASIS, _P, _P, _P, ctypes.c_size_t, _P]),
+    "fagp_vec_op": (ctypes.c_int, [ctypes.c_int32, _I64, _P, _P, _D, _P, _P]),
+    "fagp_lambda_bar": (ctypes.c_int, [_P, _P, _I64, _D, _P, _P]),
+    "fagp_literal_inner": (ctypes.c_int, [_P, _P, _I64, _P, _P]),
+    "fagp_inner_operand": (ctypes.c_int, [_P, _P, _BASIS, _P, _P]),
+    "fagp_rowdot": (ctypes.c_int, [_P, _P, _I64, _I64, _P, _P]),
 }
 
 _LIB = None
@@ -159,3 +167,10 @@ def stream_handle(stream=None):
 
     s = stream if stream is not None else torch.cuda.current_stream()
     return ctypes.c_void_p(s.cuda_stream)
+
+# fagp_vec_op codes (include/fagp_b200.h)
+VEC_DIV = 0
+VEC_SUB_DIV = 1
+VEC_MUL = 2
+VEC_SUB = 3
+VEC_SUB_SCALAR = 4

@@ -412,4 +412,32 @@ int fagp_gram(const double* T, int64_t N, const fagp_basis* basis, double* gram_
   return FAGP_OK;
 }
 
+size_t fagp_phi_tmatvec_workspace_size(int64_t N, const fagp_basis* basis) {
+  if (check_basis(basis) != FAGP_OK || N < 0) return 0;
+  if (pairk::enabled(basis->p, basis->M)) return pairk::tmatvec_workspace(N, basis);
+  // direct form: the packed [G | t] Gram and its workspace (p = 1: the SYRK is the cheap part)
+  return fagp_gram_workspace_size(N, basis) + size_t(round_up(fagp_gram_len(basis), 2)) * sizeof(double);
+}
+
+int fagp_phi_tmatvec(double* T, int64_t N, const fagp_basis* basis, const double* v, double* out, void* workspace,
+                     size_t workspace_bytes, void* stream) {
+  int st = check_basis(basis);
+  if (st) return st;
+  if (N < 0 || out == nullptr || (N > 0 && (T == nullptr || v == nullptr))) return FAGP_EINVAL;
+  if (workspace == nullptr || workspace_bytes < fagp_phi_tmatvec_workspace_size(N, basis)) return FAGP_EWORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (N == 0) {
+    FAGP_CUDA_TRY(cudaMemsetAsync(out, 0, size_t(basis->m) * sizeof(double), s));
+    return FAGP_OK;
+  }
+  st = fagp_set_residual(T, N, basis, v, 0.0, stream);
+  if (st) return st;
+  if (pairk::enabled(basis->p, basis->M)) return pairk::tmatvec(T, N, basis, out, workspace, workspace_bytes, s);
+  const size_t gws = fagp_gram_workspace_size(N, basis);
+  double* packed = reinterpret_cast<double*>(static_cast<char*>(workspace) + gws);
+  st = fagp_gram(T, N, basis, packed, workspace, gws, nullptr, stream);
+  if (st) return st;
+  return fagp_gram_unpack(packed, basis, nullptr, out, stream);
+}
+
 }  // extern "C"

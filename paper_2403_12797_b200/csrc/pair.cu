@@ -123,8 +123,7 @@ pair_gram_kernel(const double* __restrict__ T, int64_t N, BasisView b, PairPlan 
   const int M = b.M, pM = b.p * M, W = table_width(b.p, M);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int npair = pl.gtA * pl.gtB;
-  const int ntiles = npair + pl.stA * pl.stB;
-  const int tile = blockIdx.x % ntiles, chunk = blockIdx.x / ntiles;
+  const int tile = pl.tile0 + int(blockIdx.x % pl.nrun), chunk = int(blockIdx.x / pl.nrun);
   const int64_t r0 = int64_t(chunk) * pl.chunk_rows;
   const int64_t r1 = tmin<int64_t>(N, r0 + pl.chunk_rows);
 
@@ -214,7 +213,7 @@ pair_gram_kernel(const double* __restrict__ T, int64_t N, BasisView b, PairPlan 
     cp_async_wait<0>();
     __syncthreads();
   }
-  double* out = ws + (size_t(chunk) * ntiles + tile) * size_t(GBM * GBN);
+  double* out = ws + (size_t(chunk) * pl.nrun + (tile - pl.tile0)) * size_t(GBM * GBN);
 #pragma unroll
   for (int s = 0; s < GFM; ++s) {
     const int i = warp * 32 + s * 8 + (lane >> 2);
@@ -255,8 +254,7 @@ pair_gram_ws_kernel(const double* __restrict__ T, int64_t N, BasisView b, PairPl
   double* Tb = Bs + WS_STAGES * GB_STAGE;            // [STAGES][GBK][W]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int npair = pl.gtA * pl.gtB;
-  const int ntiles = npair + pl.stA * pl.stB;
-  const int tile = blockIdx.x % ntiles, chunk = blockIdx.x / ntiles;
+  const int tile = pl.tile0 + int(blockIdx.x % pl.nrun), chunk = int(blockIdx.x / pl.nrun);
   const int64_t r0 = int64_t(chunk) * pl.chunk_rows;
   const int64_t r1 = tmin<int64_t>(N, r0 + pl.chunk_rows);
   const int nchunks = int(ceil_div(tmax<int64_t>(r1 - r0, 0), GBK));
@@ -348,7 +346,7 @@ pair_gram_ws_kernel(const double* __restrict__ T, int64_t N, BasisView b, PairPl
     // release the slot unless the producers will never refill it
     if (n + WS_STAGES < nchunks) named_arrive(EMPTY0 + slot, WS_NT);
   }
-  double* out = ws + (size_t(chunk) * ntiles + tile) * size_t(GBM * GBN);
+  double* out = ws + (size_t(chunk) * pl.nrun + (tile - pl.tile0)) * size_t(GBM * GBN);
 #pragma unroll
   for (int s = 0; s < GFM; ++s) {
     const int i = warp * 32 + s * 8 + (lane >> 2);
@@ -366,10 +364,11 @@ __global__ void pair_gram_reduce_kernel(const double* __restrict__ ws, PairPlan 
                                         uint32_t* flags) {
   const int64_t nH = pl.GA * pl.GB, nt = pl.SA * pl.SB;
   const int npair = pl.gtA * pl.gtB;
-  const int ntiles = npair + pl.stA * pl.stB;
-  const size_t stride = size_t(ntiles) * GBM * GBN;
+  const size_t stride = size_t(pl.nrun) * GBM * GBN;
+  const int64_t e0 = pl.tile0 > 0 ? nH : 0;  // t-only runs produce just t
   bool bad = false;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < nH + nt; e += int64_t(gridDim.x) * blockDim.x) {
+  for (int64_t e = e0 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < nH + nt;
+       e += int64_t(gridDim.x) * blockDim.x) {
     int tile;
     int64_t lam, rho;
     if (e < nH) {
@@ -382,10 +381,10 @@ __global__ void pair_gram_reduce_kernel(const double* __restrict__ ws, PairPlan 
       rho = q - lam * pl.SB;
       tile = npair + int(lam / GBM) * pl.stB + int(rho / GBN);
     }
-    const double* src = ws + size_t(tile) * GBM * GBN + size_t(lam % GBM) * GBN + size_t(rho % GBN);
+    const double* src = ws + size_t(tile - pl.tile0) * GBM * GBN + size_t(lam % GBM) * GBN + size_t(rho % GBN);
     double sum = 0.0;
     for (int s = 0; s < pl.S; ++s) sum += src[s * stride];
-    out[e] = sum;
+    out[e - e0] = sum;
     bad |= not_finite(sum);
   }
   if (bad) raise_flag(flags, FAGP_FLAG_PHI_NONFINITE);
@@ -465,7 +464,7 @@ __global__ void ctilde_kernel(const double* __restrict__ D, int64_t ldd, const d
           j = j * M + x;
           jj = jj * M + y;
         }
-        v += __dmul_rn(__dmul_rn(s[j], D[j * ldd + jj]), s[jj]);
+        v += s ? __dmul_rn(__dmul_rn(s[j], D[j * ldd + jj]), s[jj]) : D[j * ldd + jj];
       }
     }
     Ct[e] = v;
@@ -717,7 +716,7 @@ bool enabled(int p, int M) {
   return ipow(P, p) < (int64_t(1) << 31);
 }
 
-PairPlan make_plan(int64_t N, int p, int M) {
+PairPlan make_plan(int64_t N, int p, int M, bool t_only) {
   PairPlan pl{};
   pl.P = M * (M + 1) / 2;
   pl.Hlen = ipow(pl.P, p);
@@ -760,8 +759,10 @@ PairPlan make_plan(int64_t N, int p, int M) {
   pl.KR = ipow(pl.P, p - pl.pN);
   pl.NP = round_up(pl.NR, 56);
   pl.KP = round_up(pl.KR, 16);
-  // split-K over rows: 3 CTAs per SM
-  const int64_t tiles = int64_t(pl.gtA) * pl.gtB + int64_t(pl.stA) * pl.stB;
+  // tiles launched, then split-K over rows: 3 CTAs per SM
+  pl.tile0 = t_only ? pl.gtA * pl.gtB : 0;
+  pl.nrun = (t_only ? 0 : pl.gtA * pl.gtB) + pl.stA * pl.stB;
+  const int64_t tiles = pl.nrun;
   const int64_t max_chunks = tmax<int64_t>(1, ceil_div(N, 16));
   const int64_t slots = int64_t(num_sms()) * 3;
   int64_t bestS = 1;
@@ -787,8 +788,12 @@ int64_t gram_len(const fagp_basis* b) { return make_plan(0, b->p, b->M).Hlen + b
 
 size_t gram_workspace(int64_t N, const fagp_basis* b) {
   const PairPlan pl = make_plan(N, b->p, b->M);
-  const size_t tiles = size_t(pl.gtA) * pl.gtB + size_t(pl.stA) * pl.stB;
-  return size_t(pl.S) * tiles * GBM * GBN * sizeof(double);
+  return size_t(pl.S) * pl.nrun * GBM * GBN * sizeof(double);
+}
+
+size_t tmatvec_workspace(int64_t N, const fagp_basis* b) {
+  const PairPlan pl = make_plan(N, b->p, b->M, true);
+  return size_t(pl.S) * pl.nrun * GBM * GBN * sizeof(double);
 }
 
 static bool gram_ws_enabled() {
@@ -828,16 +833,12 @@ static int launch_gram_fb(int FB, const double* T, int64_t N, const fagp_basis* 
   }
 }
 
-int gram(const double* T, int64_t N, const fagp_basis* b, double* out, void* ws_, size_t ws_bytes, uint32_t* flags,
-         cudaStream_t s) {
-  const PairPlan pl = make_plan(N, b->p, b->M);
-  if (ws_ == nullptr || ws_bytes < gram_workspace(N, b)) return FAGP_EWORKSPACE;
+static int run_gram(const PairPlan& pl, const double* T, int64_t N, const fagp_basis* b, double* out, double* ws,
+                    uint32_t* flags, cudaStream_t s) {
   const int W = table_width(b->p, b->M);
-  const size_t tiles = size_t(pl.gtA) * pl.gtB + size_t(pl.stA) * pl.stB;
-  double* ws = static_cast<double*>(ws_);
   const size_t smem = gram_smem(W);
   if (smem > 227 * 1024) return FAGP_EUNSUPPORTED;
-  const unsigned grid = unsigned(size_t(pl.S) * tiles);
+  const unsigned grid = unsigned(size_t(pl.S) * pl.nrun);
   const int FA = 2 * pl.pL, FB = 2 * (b->p - pl.pL);
   int rc;
   switch (FA) {
@@ -853,6 +854,17 @@ int gram(const double* T, int64_t N, const fagp_basis* b, double* out, void* ws_
       ws, pl, out, flags);
   FAGP_LAUNCH_CHECK();
   return FAGP_OK;
+}
+
+int gram(const double* T, int64_t N, const fagp_basis* b, double* out, void* ws, size_t ws_bytes, uint32_t* flags,
+         cudaStream_t s) {
+  if (ws == nullptr || ws_bytes < gram_workspace(N, b)) return FAGP_EWORKSPACE;
+  return run_gram(make_plan(N, b->p, b->M), T, N, b, out, static_cast<double*>(ws), flags, s);
+}
+
+int tmatvec(const double* T, int64_t N, const fagp_basis* b, double* t, void* ws, size_t ws_bytes, cudaStream_t s) {
+  if (ws == nullptr || ws_bytes < tmatvec_workspace(N, b)) return FAGP_EWORKSPACE;
+  return run_gram(make_plan(N, b->p, b->M, true), T, N, b, t, static_cast<double*>(ws), nullptr, s);
 }
 
 __global__ void copy_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t n) {
@@ -917,6 +929,34 @@ static int launch_var_nw(int FE, const double* Ts, int64_t Ns, const fagp_basis*
     case 8: return go(pair_var_kernel<FK, 8, NW>);
     default: return FAGP_EUNSUPPORTED;
   }
+}
+
+int matvec(const double* T, int64_t N, const fagp_basis* b, const double* x, double c, double* y, uint32_t* flags,
+           cudaStream_t s) {
+  if (N == 0) return FAGP_OK;
+  const int W = table_width(b->p, b->M);
+  const size_t msmem = (size_t(b->m) + size_t(MNT) * (W | 1)) * sizeof(double);
+  if (msmem > 227 * 1024) return FAGP_EUNSUPPORTED;
+  auto go = [&](auto kern) -> int {
+    FAGP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(msmem)));
+    kern<<<unsigned(ceil_div(N, MNT)), MNT, msmem, s>>>(T, N, view(b), x, c, y, flags);
+    return FAGP_OK;
+  };
+  int rc;
+  switch (b->p) {
+    case 1: rc = go(mean_kernel<1>); break;
+    case 2: rc = go(mean_kernel<2>); break;
+    case 3: rc = go(mean_kernel<3>); break;
+    case 4: rc = go(mean_kernel<4>); break;
+    case 5: rc = go(mean_kernel<5>); break;
+    case 6: rc = go(mean_kernel<6>); break;
+    case 7: rc = go(mean_kernel<7>); break;
+    case 8: rc = go(mean_kernel<8>); break;
+    default: rc = FAGP_EUNSUPPORTED;
+  }
+  if (rc) return rc;
+  FAGP_LAUNCH_CHECK();
+  return FAGP_OK;
 }
 
 template <int FK>

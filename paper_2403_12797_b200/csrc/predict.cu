@@ -354,6 +354,15 @@ int dispatch_fast(const double* Ts, int64_t Ns, const fagp_basis* basis, const d
 
 extern "C" {
 
+int fagp_phi_matvec(const double* T, int64_t N, const fagp_basis* basis, const double* x, double mean_const,
+                    double* out, uint32_t* flags, void* stream) {
+  int st = check_basis(basis);
+  if (st) return st;
+  if (N < 0 || (N > 0 && (T == nullptr || x == nullptr || out == nullptr))) return FAGP_EINVAL;
+  if (basis->p > 8) return FAGP_EUNSUPPORTED;
+  return pairk::matvec(T, N, basis, x, mean_const, out, flags, static_cast<cudaStream_t>(stream));
+}
+
 int fagp_predict(const double* Ts, int64_t Ns, const fagp_basis* basis, const double* predict_op, double sigma2,
                  double mean_const, double* mean, double* var, uint32_t* flags, void* stream) {
   int st = check_basis(basis);

@@ -10,6 +10,9 @@ call into libfagp_b200.so on the current CUDA stream:
     fagp_factor                                A, Cholesky+jitter, w, V        (posterior.py:171-175,234-235)
     fagp_predict                               mean, var, fused               (posterior.py:247,249-263)
 
+``method="literal"`` (the reference's cross-check route, posterior.py:236-244, 256-260) runs
+on the device too: see :mod:`literal`.
+
 ``PosteriorResult`` gains ``var`` (the per-point predictive variance, i.e. the diagonal of
 the reference's covariance that `fagp predict` reports, cli.py:222).  The full N* x N*
 covariance (``want_cov=True``) is formed from the same factor for modest N*.
@@ -26,6 +29,7 @@ from . import _device as dev
 from . import _lib
 from .errors import NumericalError
 from .kernels import as_ard
+from .literal import lambda_bar_matrix, literal_posterior
 from .mercer import (
     DEFAULT_MEMORY_CAP,
     DELTA2_RHO_SQUARED,
@@ -328,8 +332,6 @@ def fagp_posterior(train, Xstar, model, backend=None, want_cov=False, method="sc
         raise ValueError("model.n_eigen must be set for the fast posterior")
     if method not in ("scaled", "literal"):
         raise ValueError(f"form must be 'scaled' or 'literal', got {method!r}")
-    if method == "literal":
-        raise NotImplementedError("method='literal' is not on the GPU path yet; use method='scaled'")
     kernel = as_ard(model.kernel)
     p = kernel.p
     X = dev.points(train.X, p, "train.X")
@@ -341,6 +343,19 @@ def fagp_posterior(train, Xstar, model, backend=None, want_cov=False, method="sc
     yd = _check_y(train.y, N)
     _budget(N, model.n_eigen, p, memory_cap)
     _budget(Ns, model.n_eigen, p, memory_cap)
+    if method == "literal":
+        if group is not None:
+            raise ValueError("method='literal' does not shard (group must be None)")
+        dev.wait_upload(xs_ready)
+        basis = Basis(kernel, model.n_eigen, delta2_variant, device=X.device)
+        flags = _Flags(X.device)
+        s = _lib.stream_handle()
+        T = _stage_tables(basis, X, flags.ptr(0), s)
+        Ts = _stage_tables(basis, Xs, flags.ptr(1), s)
+        mean, var, cov = literal_posterior(basis, T, Ts, yd, model.noise_var, model.mean_const, want_var=want_var,
+                                           want_cov=want_cov, fault_flip=_FAULT_FLIP_MEAN_SIGN, X=X, Xs=Xs,
+                                           flags=flags)
+        return _result(mean, var, cov, return_device)
     eng = PosteriorEngine(kernel, model.n_eigen, N, Ns, model.noise_var, model.mean_const, delta2_variant,
                           device=X.device, group=group, want_var=want_var)
     mean, var = eng.run(X, yd, Xs, fault_flip=_FAULT_FLIP_MEAN_SIGN, xs_ready=xs_ready)
@@ -351,6 +366,10 @@ def fagp_posterior(train, Xstar, model, backend=None, want_cov=False, method="sc
                 lam_floored=eng.lam_floored, sqrt_lam=eng.sqrt_lam, packed=eng.packed, L=eng.L, t=eng.t, w=eng.w,
                 predict_op=eng.predict_op, jitter=float(eng.jitter.value))
         cov = _covariance(f, eng.Ts)
+    return _result(mean, var, cov, return_device)
+
+
+def _result(mean, var, cov, return_device):
     if return_device:
         return PosteriorResult(mean=mean, cov=cov, var=var)
     return PosteriorResult(mean=dev.to_host(mean), cov=None if cov is None else dev.to_host(cov),
@@ -368,7 +387,10 @@ def fagp_posterior_from_eigensystems(es, es_star, y, model, backend=None, want_c
     if method not in ("scaled", "literal"):
         raise ValueError(f"form must be 'scaled' or 'literal', got {method!r}")
     if method == "literal":
-        raise NotImplementedError("method='literal' is not on the GPU path yet; use method='scaled'")
+        # the tables are the eigensystems' own; phi_tmatvec rewrites only the residual column
+        mean, var, cov = literal_posterior(es.basis, es.table, es_star.table, yd, model.noise_var, model.mean_const,
+                                           want_var=want_var, want_cov=want_cov, fault_flip=_FAULT_FLIP_MEAN_SIGN)
+        return _result(mean, var, cov, return_device)
     packed = gram_packed(es.basis, es.table, yd, model.mean_const)
     f, st, piv = factor_packed(es.basis, packed, model.noise_var, model.mean_const, es.N)
     if st != _lib.FAGP_OK:
@@ -376,10 +398,7 @@ def fagp_posterior_from_eigensystems(es, es_star, y, model, backend=None, want_c
     _apply_fault(f)
     mean, var = predict_device(f, es_star.table, want_var=want_var)
     cov = _covariance(f, es_star.table) if want_cov else None
-    if return_device:
-        return PosteriorResult(mean=mean, cov=cov, var=var)
-    return PosteriorResult(mean=dev.to_host(mean), cov=None if cov is None else dev.to_host(cov),
-                           var=None if var is None else dev.to_host(var))
+    return _result(mean, var, cov, return_device)
 
 
 class LambdaBarSolve:
@@ -419,11 +438,7 @@ class LambdaBarSolve:
         return self._es.size
 
     def _matrix_device(self):
-        import torch
-
-        lam_f = self._fit.lam_floored
-        mtx = torch.diag(1.0 / lam_f) + self._gram / self.noise_var
-        return 0.5 * (mtx + mtx.T)
+        return lambda_bar_matrix(self._gram, self._fit.lam_floored, self.noise_var)
 
     @property
     def matrix(self):

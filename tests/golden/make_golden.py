@@ -37,6 +37,8 @@ CASES = {
     "c5s": (5, 6, 600, 80, None, None, 0.0025, 0.0, "rho_squared", False),
 }
 
+LITERAL_CASES = ("c1", "lin2", "ard4", "p1m40", "c5s")
+
 
 def digest(a):
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
@@ -79,6 +81,11 @@ def main():
         out[pre + "phi_head"] = es.phi[:8].copy()
         if full_g:
             out[pre + "G"] = G
+        if name in LITERAL_CASES:  # the cross-check route (posterior.py:236-244, 256-260)
+            lit = fagp_posterior(ds, Xs, model, want_cov=True, method="literal", delta2_variant=var_kind,
+                                 memory_cap=1 << 40)
+            out[pre + "literal_mean"] = lit.mean
+            out[pre + "literal_var"] = np.diag(lit.cov).copy()
         print(name, "m =", es.size, "mean[0] =", res.mean[0], file=sys.stderr)
     # multi-index enumerations (bit-exact check)
     for n, p in [(1, 1), (3, 1), (2, 2), (4, 3), (10, 3), (8, 4), (6, 5), (3, 7)]:

@@ -98,11 +98,11 @@ def test_predict_cli_matches_oracle(tmp_path):
 def test_bench_cli_rows(tmp_path):
     out = tmp_path / "r.csv"
     rc = cli.main(["bench", "--out", str(out), "--reps", "2", "--dims", "1,2", "--n-samples", "2000",
-                   "--n-test", "100", "--memory-cap", str(1 << 22), "--quiet"])
+                   "--n-test", "100", "--memory-cap", str(1 << 21), "--quiet"])
     assert rc == cli.EXIT_OK
     rows = cli.read_results_csv(out)
     skips = [r for r in rows if r[4] == cli.SKIP_PHASE]
     timed = [r for r in rows if r[4] != cli.SKIP_PHASE]
     assert timed and all(r[0] == "cuda" and r[5] >= 0 for r in timed)
-    assert skips  # p=2, n=11 at N=2000 exceeds a 4 MiB cap as in the reference's sentinel logic
+    assert skips  # p=1, n=128 at N=2000 (2.18 MB estimate) exceeds a 2 MiB cap: the reference's sentinel
     assert cli.main(["plotdata", "--results", str(out), "--out-dir", str(tmp_path)]) == cli.EXIT_OK

@@ -82,3 +82,17 @@ def test_spd_factor_jitter_and_pivot(golden):
 def test_useful_flops_c3():
     assert O.useful_flops(10**6, 10**6, 1000) == pytest.approx(2.0087e12, rel=1e-4)
     assert math.isclose(O.useful_flops(1000, 1000, 10), 2.807e5, rel_tol=1e-3)
+
+
+LITERAL_CASES = ["c1", "lin2", "ard4", "p1m40", "c5s"]
+
+
+@pytest.mark.parametrize("name", LITERAL_CASES)
+def test_oracle_literal_matches_reference(cases, name):
+    """method='literal' restatement against the reference's own literal outputs."""
+    c = cases[name]
+    out = O.posterior_literal(c.X, c.y, c.Xs, c.eps, c.rho, c.M, c.noise_var, c.mean_const, c.variant)
+    assert scaled_err(out["mean"], c.ref["literal_mean"]) < 1e-12
+    # the reference takes diag(cov) after cov = Phi* inner Phi*^T; the restatement forms only
+    # the diagonal (same products, different summation order) -- ill-conditioned route
+    assert scaled_err(out["var"], c.ref["literal_var"]) < 1e-9
