@@ -61,7 +61,7 @@ def useful_flops(N, Ns, m):
     return N * m * (m + 1) + 2 * N * m + 2 * m**3 / 3 + 2 * Ns * m + Ns * m * (m + 1) + 2 * Ns * m
 
 
-def launches_per_step(m, pair):
+def launches_per_step(m, pair, p=1):
     """Kernels of ours launched by one PosteriorEngine.run() (no jitter retry)."""
     nblk = -(-m // 32)
     potrf = nblk + (nblk - 1)  # fused diag+panel kernel per step, trailing GEMM between steps
@@ -75,9 +75,10 @@ def launches_per_step(m, pair):
         h *= 2
     trtri = 1 + 1 + 2 * levels  # pad, diag_inv, 2 GEMMs per level
     if pair:
-        # t copy, build A, potrf, zero upper, trtri, w GEMVs x2, D = X^T X, Ct, w copy
-        factor = 1 + 1 + potrf + 1 + trtri + 2 + 1 + 1 + 1
-        return 2 + 2 + factor + 2  # basis_eval x2, pair GEMM + reduce, factor, var + mean
+        # K -> H expansion (p mode products), t copy, build A, potrf, zero upper, trtri, w GEMVs x2,
+        # D = X^T X, Ct, Ct -> C'' (p mode products), scatter, w copy
+        factor = p + 1 + 1 + potrf + 1 + trtri + 2 + 1 + 1 + p + 1 + 1
+        return 2 + 2 + factor + 2  # basis_eval x2, modal GEMM + reduce, factor, var + mean
     factor = 1 + 1 + potrf + 1 + trtri + 2 + 1  # build G/t, build A, potrf, zero upper, trtri, GEMVs, operand
     return 2 + 2 + factor + 1  # basis_eval x2, gram + reduce, factor, predict
 
@@ -308,11 +309,11 @@ def main():
 
     # ---- roofline of the dominant kernel (per launch, this rank's shard) ----
     n_loc, ns_loc = X.shape[0], Xs.shape[0]
-    pair = p >= 2
-    P = M * (M + 1) // 2
-    if pair:  # pair form: the GEMM over the P^p distinct Gram / variance entries (+ t, mean)
-        gram_flops = 2 * n_loc * P**p + 2 * n_loc * m
-        pred_flops = 2 * ns_loc * P**p + 2 * ns_loc * m
+    pair = 2 <= p <= 8
+    Lm = 2 * M - 1
+    if pair:  # modal form: the GEMM over the L^p modal Gram / variance entries (+ t, mean)
+        gram_flops = 2 * n_loc * Lm**p + 2 * n_loc * m
+        pred_flops = 2 * ns_loc * Lm**p + 2 * ns_loc * m
     else:
         gram_flops = n_loc * m * (m + 1) + 2 * n_loc * m
         pred_flops = ns_loc * m * (m + 1) + 4 * ns_loc * m
@@ -321,17 +322,17 @@ def main():
     g_ms, p_ms = statistics.mean(gram_ms), statistics.mean(pred_ms)
     peak, peak_src = fp64_peak()
     if g_ms >= p_ms:
-        dom, dflops, rflops, dms = "fagp_gram (pair-form DMMA GEMM + reduce + t)" if pair else \
+        dom, dflops, rflops, dms = "fagp_gram (modal DMMA GEMM + reduce + t)" if pair else \
             "fagp_gram (fused SYRK + reduce)", gram_flops, ref_gram, g_ms
         traffic = ncu_traffic("gram_kernel")
     else:
-        dom, dflops, rflops, dms = "fagp_predict (pair-form variance GEMM + mean)" if pair else \
+        dom, dflops, rflops, dms = "fagp_predict (modal variance GEMM + mean)" if pair else \
             "fagp_predict (fused triangular GEMM)", pred_flops, ref_pred, p_ms
         traffic = ncu_traffic("predict_kernel")
     achieved = dflops / (dms / 1e3) / 1e12
     roofline = {"bound": "tensor", "kernel": dom, "achieved": round(achieved, 3), "peak": peak, "unit": "TFLOP/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                "flops_per_launch": dflops, "algorithm": "pair form (P^p distinct entries)" if pair else "direct",
+                "flops_per_launch": dflops, "algorithm": "modal form (L^p = (2M-1)^p entries)" if pair else "direct",
                 "reference_equivalent_tflops": round(rflops / (dms / 1e3) / 1e12, 3)}
     step_tf = useful_flops(N, Ns, m) / world / (ms / 1e3) / 1e12
 
@@ -359,6 +360,7 @@ def main():
             times.append(time.perf_counter() - t0)
             assert r.mean.shape == (ns_loc,) and r.var.shape == (ns_loc,)
         t = statistics.mean(times)
+        log("e2e step ms:", " ".join(f"{1e3 * x:.2f}" for x in times))
         if world > 1:
             tt = torch.tensor([t], dtype=torch.float64, device=X.device)
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
@@ -377,7 +379,7 @@ def main():
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator)",
                "config": config_dict(args, world), "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
-               "clocks": clk.summary(), "gpu_launches": launches_per_step(m, p >= 2) * args.steps,
+               "clocks": clk.summary(), "gpu_launches": launches_per_step(m, 2 <= p <= 8, p) * args.steps,
                "phases_ms": {"tables": round(statistics.mean(tab_ms), 3), "gram": round(g_ms, 3),
                              "allreduce+factor": round(statistics.mean(factor_ms), 3), "predict": round(p_ms, 3)},
                "step_reference_equivalent_tflops": round(step_tf, 3),

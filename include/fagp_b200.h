@@ -52,8 +52,9 @@ typedef enum fagp_status {
  *   [p,  2p)          neg_delta2[d] = -delta2_d               (mercer.py:281, 94-99)
  *   [2p, 3p)          sqrt_beta[d]  = sqrt(beta_d)            (mercer.py:281)
  *   [3p, 3p + p*M)    lam1d[d*M+i]  = eigenvalues_1d(...)[i]  (mercer.py:146-161)
- * All entries are computed on the host with the reference's own scalar formulas so
- * they are bit-identical to it (shape_params, mercer.py:102-119).  m must equal M^p.
+ *   [3p + p*M, +P*L)  modal[pi*L+k] = fagp_modal_coeffs(M)    (P = M(M+1)/2, L = 2M-1)
+ * The shape constants are computed on the host with the reference's own scalar formulas
+ * so they are bit-identical to it (shape_params, mercer.py:102-119).  m must equal M^p.
  */
 typedef struct fagp_basis {
   int32_t p;           /* input dimension, 1..FAGP_MAX_P                         */
@@ -66,6 +67,14 @@ typedef struct fagp_basis {
 int fagp_abi_version(void);
 const char* fagp_strerror(int status);
 int64_t fagp_basis_table_len(int32_t p, int32_t M);
+
+/* HOST: the modal linearisation coefficients (P x L doubles, pairs a <= b a-major):
+ * h_a(z) h_b(z) = sum_k V[pi][k] h_k(sqrt(2) z), h = the reference's normalised Hermite
+ * polynomials (mercer.py:122-143).  Products of two eigenfunctions of one dimension then
+ * lie in the span of L = 2M-1 functions g_k = beta e^{-2 delta2 x^2} h_k(sqrt2 rho beta x),
+ * which is what lets the Gram and variance kernels contract over L^p instead of P^p
+ * columns.  Exact identity (long-double recurrence, |V| <= 1). */
+int fagp_modal_coeffs(int32_t M, double* out_host);
 
 /* Multi-index enumeration, HOST output (m x p int64, 1-based, first dimension slowest).
  * Replaces mercer.multi_indices (mercer.py:195-216); bit-exact with it. */
@@ -119,10 +128,12 @@ int fagp_find_nonfinite(const double* T, int64_t N, const fagp_basis* basis, int
  * `backend.gemm(phi, y - c, transpose_a=True)` (posterior.py:229,233), with Phi never
  * written to HBM.  The output `gram` (fagp_gram_len(basis) doubles) is a compressed form
  * of G = Phi^T Phi and t = Phi^T (y - c), read by fagp_factor / fagp_gram_unpack:
- *  - p >= 2 ("pair form"): [H | t].  G[(a),(a')] = sum_r prod_d phi_d,a_d phi_d,a'_d depends
- *    only on the unordered pair {a_d, a'_d} of every dimension, so G has (M(M+1)/2)^p distinct
- *    entries H[pi_0, ..., pi_{p-1}] (pi = pair index, first dimension slowest), computed as
- *    one rectangular DMMA GEMM over the rows; t follows (m entries, CUDA cores).
+ *  - 2 <= p <= 8 ("modal form"): [K | t].  Every product phi_d,a phi_d,b of one dimension is
+ *    an exact combination of L = 2M-1 functions g_d,k (fagp_modal_coeffs), so
+ *    G[(a),(a')] = sum_kappa K[kappa] prod_d V[{a_d,a'_d}][kappa_d] with
+ *    K[kappa] = sum_r prod_d g_d,kappa_d(x_rd): L^p entries (first dimension slowest), one
+ *    rectangular DMMA GEMM over the rows; t = Phi^T r (m entries, canonical feature order)
+ *    comes out of the same launch.
  *  - p == 1: the packed upper triangle of [Phi | r]^T [Phi | r] ((m+1)(m+2)/2, row-major;
  *    column m holds t), from a fused SYRK.
  * This buffer is also the only data multi-GPU callers all-reduce (sum over row shards).
@@ -134,8 +145,11 @@ size_t fagp_gram_workspace_size(int64_t N, const fagp_basis* basis);
 int fagp_gram(const double* T, int64_t N, const fagp_basis* basis, double* gram, void* workspace,
               size_t workspace_bytes, uint32_t* flags, void* stream);
 
-/* Expand a `gram` buffer into the full symmetric G (m x m, nullable) and t (m, nullable). */
-int fagp_gram_unpack(const double* gram, const fagp_basis* basis, double* G, double* t, void* stream);
+/* Expand a `gram` buffer into the full symmetric G (m x m, nullable) and t (m, nullable).
+ * The modal form needs fagp_gram_unpack_workspace_size(basis) bytes of workspace for G. */
+size_t fagp_gram_unpack_workspace_size(const fagp_basis* basis);
+int fagp_gram_unpack(const double* gram, const fagp_basis* basis, double* G, double* t, void* workspace,
+                     size_t workspace_bytes, void* stream);
 
 /* ---- (3) Cholesky factorisation and solves ----------------------------------------- */
 /* Scaled system A = (s_i G_ij) s_j + sigma2 I (posterior.py:171-174) from the `gram` buffer,
@@ -231,11 +245,12 @@ int fagp_literal_inner(const double* mid, const double* lam_f, int64_t m, double
 
 /* A fagp_predict operand (fagp_predict_operand_len doubles) for an explicit inner matrix:
  * fagp_predict(..., sigma2 = 1.0, ...) then returns var_i = phi*_i^T inner phi*_i and
- * mean_i = mean_const + phi*_i . w.  Pair form (2 <= p <= 8) only: FAGP_EUNSUPPORTED
+ * mean_i = mean_const + phi*_i . w.  Modal form (2 <= p <= 8) only: FAGP_EUNSUPPORTED
  * otherwise (use fagp_features + fagp_dgemm + fagp_rowdot), returned before the pointer
  * checks so a call with NULL pointers probes the form. */
+size_t fagp_inner_operand_workspace_size(const fagp_basis* basis);
 int fagp_inner_operand(const double* inner, const double* w, const fagp_basis* basis,
-                       double* predict_op, void* stream);
+                       double* predict_op, void* workspace, size_t workspace_bytes, void* stream);
 
 /* out[i] = sum_j A[i, j] B[i, j] (A, B: n x k) -- diag(Phi* inner Phi*^T) from
  * B = Phi* inner (posterior.py:262, cli.py:222). */

@@ -55,6 +55,7 @@ SIGNATURES = {
     "fagp_abi_version": (ctypes.c_int, []),
     "fagp_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "fagp_basis_table_len": (_I64, [_I32, _I32]),
+    "fagp_modal_coeffs": (ctypes.c_int, [_I32, _P]),
     "fagp_multi_indices": (ctypes.c_int, [_I32, _I32, _P]),
     "fagp_read_flags": (ctypes.c_int, [_P, _P, _P]),
     "fagp_eigenvalues": (ctypes.c_int, [_BASIS, _D, _P, _P, _P, _P]),
@@ -65,7 +66,8 @@ SIGNATURES = {
     "fagp_features": (ctypes.c_int, [_P, _I64, _BASIS, _P, _P, _P]),
     "fagp_find_nonfinite": (ctypes.c_int, [_P, _I64, _BASIS, _P, _P]),
     "fagp_gram_len": (_I64, [_BASIS]),
-    "fagp_gram_unpack": (ctypes.c_int, [_P, _BASIS, _P, _P, _P]),
+    "fagp_gram_unpack_workspace_size": (ctypes.c_size_t, [_BASIS]),
+    "fagp_gram_unpack": (ctypes.c_int, [_P, _BASIS, _P, _P, _P, ctypes.c_size_t, _P]),
     "fagp_gram_workspace_size": (_SZ, [_I64, _BASIS]),
     "fagp_gram": (ctypes.c_int, [_P, _I64, _BASIS, _P, _P, _SZ, _P, _P]),
     "fagp_factor_workspace_size": (_SZ, [_I64]),
@@ -85,7 +87,8 @@ SIGNATURES = {
     "fagp_vec_op": (ctypes.c_int, [ctypes.c_int32, _I64, _P, _P, _D, _P, _P]),
     "fagp_lambda_bar": (ctypes.c_int, [_P, _P, _I64, _D, _P, _P]),
     "fagp_literal_inner": (ctypes.c_int, [_P, _P, _I64, _P, _P]),
-    "fagp_inner_operand": (ctypes.c_int, [_P, _P, _BASIS, _P, _P]),
+    "fagp_inner_operand_workspace_size": (ctypes.c_size_t, [_BASIS]),
+    "fagp_inner_operand": (ctypes.c_int, [_P, _P, _BASIS, _P, _P, ctypes.c_size_t, _P]),
     "fagp_rowdot": (ctypes.c_int, [_P, _P, _I64, _I64, _P, _P]),
 }
 

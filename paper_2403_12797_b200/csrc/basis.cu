@@ -11,7 +11,9 @@
 // __dsub_rn) so nvcc cannot contract it into an FMA: the result then matches numpy's
 // evaluation order bit for bit except for exp(), whose CUDA and numpy-SIMD versions differ
 // by at most a couple of ulps on a small fraction of arguments.
+#include <cmath>
 #include <cstring>
+#include <vector>
 
 #include "common.cuh"
 
@@ -58,15 +60,19 @@ __global__ void hermite_kernel(const double* __restrict__ z, int64_t n, int coun
 // residual r = y - c (0 without y), 1.0 and 0.0 (see table_width in common.cuh).
 // One thread per (row, dim); rows are staged through shared memory so the table rows
 // are written to HBM with coalesced 8-byte stores.
+// Modal path (2 <= p <= 8): the g-section g_{d,k} = beta_d exp(-2 delta2_d x^2) h_k(sqrt2 z),
+// k < L = 2M - 1, then 1.0 and 0.0 (modal.cu).
 __global__ void basis_eval_kernel(const double* __restrict__ X, int64_t N, BasisView b,
                                   const double* __restrict__ y, double mean_const,
                                   double* __restrict__ T, uint32_t* flags, int rows_per_cta) {
   extern __shared__ double sm[];
   const int M = b.M, p = b.p, pM = p * M, W = table_width(p, M);
-  double* c1 = sm;             // [M]
-  double* c2 = sm + M;         // [M]
-  double* stage = sm + 2 * M;  // [rows_per_cta * W]
-  for (int k = threadIdx.x; k < M; k += blockDim.x) {
+  const bool modal = modal_on(p, M);
+  const int L = modal_L(M), G0 = table_gbase(p, M), KC = modal ? L : M;
+  double* c1 = sm;              // [KC]
+  double* c2 = sm + KC;         // [KC]
+  double* stage = sm + 2 * KC;  // [rows_per_cta * W]
+  for (int k = threadIdx.x; k < KC; k += blockDim.x) {
     c1[k] = herm_c1(k);
     c2[k] = herm_c2(k);
   }
@@ -95,13 +101,38 @@ __global__ void basis_eval_kernel(const double* __restrict__ X, int64_t N, Basis
         h = hn;
       }
     }
+    if (modal) {
+      // beta * exp(-2 delta2 x^2) * h_k(sqrt2 z), k < L
+      const double sb = b.sqrt_beta()[d];
+      const double amp = __dmul_rn(__dmul_rn(sb, sb),
+                                   exp(__dmul_rn(__dmul_rn(__dmul_rn(2.0, b.neg_delta2()[d]), x), x)));
+      const double yz = __dmul_rn(zr, sqrt2);
+      double* g = stage + rl * W + G0 + d * L;
+      double gm1 = 1.0;
+      g[0] = amp;
+      if (L > 1) {
+        double h = __dmul_rn(yz, sqrt2);
+        g[1] = __dmul_rn(amp, h);
+        for (int k = 1; k < L - 1; ++k) {
+          double hn = __dsub_rn(__dmul_rn(__dmul_rn(yz, c1[k]), h), __dmul_rn(c2[k], gm1));
+          g[k + 1] = __dmul_rn(amp, hn);
+          gm1 = h;
+          h = hn;
+        }
+      }
+    }
   }
   for (int rl = threadIdx.x; rl < nrows; rl += blockDim.x) {
     double* o = stage + rl * W;
     o[table_col_r(pM)] = y ? __dsub_rn(y[row0 + rl], mean_const) : 0.0;  // r = y - c (posterior.py:229)
     o[table_col_one(pM)] = 1.0;
     o[table_col_zero(pM)] = 0.0;
-    for (int c = pM + 3; c < W; ++c) o[c] = 0.0;
+    for (int c = pM + 3; c < G0; ++c) o[c] = 0.0;
+    if (modal) {
+      o[G0 + p * L] = 1.0;
+      o[G0 + p * L + 1] = 0.0;
+      for (int c = G0 + p * L + 2; c < W; ++c) o[c] = 0.0;
+    }
   }
   __syncthreads();
   double* dst = T + row0 * W;
@@ -241,7 +272,46 @@ const char* fagp_strerror(int status) {
 
 int64_t fagp_basis_table_len(int32_t p, int32_t M) {
   if (p < 1 || M < 1) return -1;
-  return int64_t(3) * p + int64_t(p) * M;
+  return int64_t(3) * p + int64_t(p) * M + int64_t(M) * (M + 1) / 2 * (2 * int64_t(M) - 1);
+}
+
+// V[pi][k] with h_a(z) h_b(z) = sum_k V[pi][k] h_k(sqrt2 z) for every pair pi = (a <= b)
+// (a-major), h = the reference's normalised Hermite polynomials (mercer.py:122-143).
+// Built from the three-term recurrence lifted to coefficient space, in long double:
+//   z h_k(sqrt2 z) = (sqrt(k+1) h_{k+1}(sqrt2 z) + sqrt(k) h_{k-1}(sqrt2 z)) / 2
+//   h_{a+1}(z) h_b(z) = sqrt(2/(a+1)) z h_a(z) h_b(z) - sqrt(a/(a+1)) h_{a-1}(z) h_b(z)
+// |V| <= 1 (an orthonormal expansion of a product of orthonormal Hermite functions).
+int fagp_modal_coeffs(int32_t M, double* out) {
+  if (M < 1 || out == nullptr) return FAGP_EINVAL;
+  const int L = 2 * M - 1;
+  std::vector<long double> V(size_t(M) * M * L, 0.0L), z(L);
+  auto at = [&](int a, int b) { return V.data() + (size_t(a) * M + b) * L; };
+  auto times_z = [&](const long double* v, long double* o) {
+    for (int k = 0; k < L; ++k) o[k] = 0.0L;
+    for (int k = 0; k < L; ++k) {
+      if (v[k] == 0.0L) continue;
+      if (k + 1 < L) o[k + 1] += v[k] * sqrtl((long double)(k + 1)) / 2.0L;
+      if (k > 0) o[k - 1] += v[k] * sqrtl((long double)k) / 2.0L;
+    }
+  };
+  at(0, 0)[0] = 1.0L;
+  for (int b = 0; b + 1 < M; ++b) {
+    times_z(at(0, b), z.data());
+    const long double c1 = sqrtl(2.0L / (b + 1)), c2 = sqrtl((long double)b / (b + 1));
+    for (int k = 0; k < L; ++k) at(0, b + 1)[k] = c1 * z[k] - (b > 0 ? c2 * at(0, b - 1)[k] : 0.0L);
+  }
+  for (int a = 0; a + 1 < M; ++a) {
+    const long double c1 = sqrtl(2.0L / (a + 1)), c2 = sqrtl((long double)a / (a + 1));
+    for (int b = 0; b < M; ++b) {
+      times_z(at(a, b), z.data());
+      for (int k = 0; k < L; ++k) at(a + 1, b)[k] = c1 * z[k] - (a > 0 ? c2 * at(a - 1, b)[k] : 0.0L);
+    }
+  }
+  int64_t pi = 0;
+  for (int a = 0; a < M; ++a)
+    for (int b = a; b < M; ++b, ++pi)
+      for (int k = 0; k < L; ++k) out[pi * L + k] = double(at(a, b)[k]);
+  return FAGP_OK;
 }
 
 int fagp_multi_indices(int32_t M, int32_t p, int64_t* out) {
@@ -335,7 +405,8 @@ int fagp_basis_eval(const double* X, int64_t N, const fagp_basis* basis, const d
   if (N == 0) return FAGP_OK;
   const int64_t W = table_width(basis->p, basis->M);
   const int rows = int(tmax<int64_t>(1, tmin<int64_t>(64, (96 * 1024) / (W * 8))));
-  size_t smem = (size_t(2) * basis->M + size_t(rows) * W) * sizeof(double);
+  const int KC = modal_on(basis->p, basis->M) ? modal_L(basis->M) : basis->M;
+  size_t smem = (size_t(2) * KC + size_t(rows) * W) * sizeof(double);
   if (smem > 200 * 1024) return FAGP_EUNSUPPORTED;
   FAGP_CUDA_TRY(cudaFuncSetAttribute(basis_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   int64_t grid = ceil_div(N, rows);

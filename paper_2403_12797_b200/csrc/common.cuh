@@ -76,6 +76,9 @@ struct BasisView {
   __host__ __device__ const double* neg_delta2() const { return table + p; }
   __host__ __device__ const double* sqrt_beta() const { return table + 2 * p; }
   __host__ __device__ const double* lam1d() const { return table + 3 * p; }
+  // modal linearisation coefficients V[pi][k] (P x L, pair pi = (a <= b) a-major):
+  // h_a(z) h_b(z) = sum_k V[pi][k] h_k(sqrt2 z)  (see modal.cu)
+  __host__ __device__ const double* modal() const { return table + 3 * p + p * M; }
 };
 
 inline int check_basis(const fagp_basis* b) {
@@ -101,9 +104,27 @@ __host__ __device__ __forceinline__ T tmax(T a, T b) { return a < b ? b : a; }
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
-// Table row layout (fagp_basis_eval): [phi_{d,i} for d < p, i < M | r | 1.0 | 0.0 | pad],
-// width W = round_up(p*M + 3, 2) so every row starts 16-byte aligned (cp.async).
-__host__ __device__ __forceinline__ int table_width(int p, int M) { return (p * M + 3 + 1) & ~1; }
+// The modal (Hermite-linearised) path runs for 2 <= p <= 8 while the pair-indexed
+// intermediates (P^p entries, P = M(M+1)/2) fit 31-bit indices; p = 1 uses the direct SYRK.
+__host__ __device__ inline bool modal_on(int p, int M) {
+  if (p < 2 || p > 8 || M < 1) return false;
+  const int64_t P = int64_t(M) * (M + 1) / 2;
+  int64_t h = 1;
+  for (int d = 0; d < p; ++d) h *= P;
+  return h < (int64_t(1) << 31);
+}
+__host__ __device__ __forceinline__ int modal_L(int M) { return 2 * M - 1; }
+
+// Table row layout (fagp_basis_eval), every section 16-byte aligned for cp.async:
+//   [phi_{d,i} (d < p, i < M) | r | 1.0 | 0.0 | pad]                 width table_gbase = round_up(pM + 3, 2)
+//   [g_{d,k} (d < p, k < L = 2M-1) | 1.0 | 0.0 | pad]                 modal path only, width round_up(pL + 2, 2)
+// g_{d,k}(x) = beta_d exp(-2 delta2_d x^2) h_k(sqrt2 rho_d beta_d x) spans every product
+// phi_{d,a} phi_{d,b} (modal.cu).
+__host__ __device__ __forceinline__ int table_gbase(int p, int M) { return (p * M + 3 + 1) & ~1; }
+__host__ __device__ __forceinline__ int table_gsec(int p, int M) { return (p * modal_L(M) + 2 + 1) & ~1; }
+__host__ __device__ __forceinline__ int table_width(int p, int M) {
+  return table_gbase(p, M) + (modal_on(p, M) ? table_gsec(p, M) : 0);
+}
 __host__ __device__ __forceinline__ int table_col_r(int pM) { return pM; }
 __host__ __device__ __forceinline__ int table_col_one(int pM) { return pM + 1; }
 __host__ __device__ __forceinline__ int table_col_zero(int pM) { return pM + 2; }

@@ -17,7 +17,7 @@
 #include <cstring>
 
 #include "common.cuh"
-#include "pair.cuh"
+#include "modal.cuh"
 
 namespace fagp {
 namespace la {
@@ -594,16 +594,31 @@ size_t fagp_factor_workspace_size(int64_t m) {
 
 int64_t fagp_predict_operand_len(const fagp_basis* basis) {
   if (check_basis(basis) != FAGP_OK) return -1;
-  if (pairk::enabled(basis->p, basis->M)) return pairk::predict_op_len(basis);
+  if (modal::enabled(basis->p, basis->M)) return modal::predict_op_len(basis);
   return op_rows(basis->m) * op_cols(basis->m);
 }
 
-int fagp_gram_unpack(const double* gram, const fagp_basis* basis, double* G, double* t, void* stream) {
+size_t fagp_gram_unpack_workspace_size(const fagp_basis* basis) {
+  if (check_basis(basis) != FAGP_OK || !modal::enabled(basis->p, basis->M)) return 0;
+  return size_t(modal::scratch_len(basis)) * sizeof(double);
+}
+
+int fagp_gram_unpack(const double* gram, const fagp_basis* basis, double* G, double* t, void* workspace,
+                     size_t workspace_bytes, void* stream) {
   int st = check_basis(basis);
   if (st) return st;
   if (gram == nullptr) return FAGP_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (pairk::enabled(basis->p, basis->M)) return pairk::system(gram, nullptr, 0.0, 0.0, basis, nullptr, G, t, s);
+  if (modal::enabled(basis->p, basis->M)) {
+    if (G) {
+      if (workspace == nullptr || workspace_bytes < fagp_gram_unpack_workspace_size(basis)) return FAGP_EWORKSPACE;
+      double* H = static_cast<double*>(workspace);
+      st = modal::expand(gram, basis, H, H + modal::scratch_len(basis) / 2, s);
+      if (st) return st;
+      return modal::system(H, gram, nullptr, 0.0, 0.0, basis, nullptr, G, t, s);
+    }
+    return modal::system(nullptr, gram, nullptr, 0.0, 0.0, basis, nullptr, nullptr, t, s);
+  }
   const int64_t m = basis->m;
   const int grid = int(tmin<int64_t>(ceil_div(m * m, 256), 8 * num_sms()));
   system_build_kernel<<<grid, 256, 0, s>>>(gram, nullptr, 0.0, 0.0, m, nullptr, G, t);
@@ -669,8 +684,8 @@ int fagp_set_mean_weights(double* predict_op, const double* w, const fagp_basis*
   int st = check_basis(basis);
   if (st) return st;
   if (predict_op == nullptr || w == nullptr) return FAGP_EINVAL;
-  if (pairk::enabled(basis->p, basis->M))
-    return pairk::set_weights(predict_op, w, basis, static_cast<cudaStream_t>(stream));
+  if (modal::enabled(basis->p, basis->M))
+    return modal::set_weights(predict_op, w, basis, static_cast<cudaStream_t>(stream));
   const int64_t m = basis->m;
   set_mean_weights_kernel<<<unsigned(ceil_div(m, 256)), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       predict_op, w, m, op_cols(m));
@@ -686,7 +701,7 @@ int fagp_factor(const double* packed, const fagp_basis* basis, const double* sqr
     if (st) return st;
   }
   const int64_t m = basis->m;
-  const bool pm = pairk::enabled(basis->p, basis->M);
+  const bool pm = modal::enabled(basis->p, basis->M);
   if (packed == nullptr || sqrt_lam == nullptr || L == nullptr || t == nullptr || w == nullptr ||
       jitter_attempts < 0)
     return FAGP_EINVAL;
@@ -698,9 +713,15 @@ int fagp_factor(const double* packed, const fagp_basis* basis, const double* sqr
   if (pivot_out) *pivot_out = 0;
   if (jitter_out) *jitter_out = 0.0;
 
+  // modal form: the pair-indexed H (P^p <= m^2 <= mp^2 doubles) lives in ws.Lp until the
+  // factorisation succeeds (ws.X is the expansion's temporary)
+  if (pm) {
+    int rc = modal::expand(packed, basis, ws.Lp, ws.X, s);
+    if (rc) return rc;
+  }
   // G and t once (A is rebuilt per attempt below)
   auto build = [&](double jit, double* A_, double* G_, double* t_) -> int {
-    if (pm) return pairk::system(packed, sqrt_lam, sigma2, jit, basis, A_, G_, t_, s);
+    if (pm) return modal::system(ws.Lp, packed, sqrt_lam, sigma2, jit, basis, A_, G_, t_, s);
     system_build_kernel<<<grid, 256, 0, s>>>(packed, sqrt_lam, sigma2, jit, m, A_, G_, t_);
     FAGP_LAUNCH_CHECK();
     return FAGP_OK;
@@ -766,7 +787,7 @@ int fagp_factor(const double* packed, const fagp_basis* basis, const double* sqr
       GemmArgs g{int(m), int(m), int(m), 1.0, 0.0, ws.X, mp, 0, ws.X, mp, 0, ws.D, m, 0, 0, nullptr};
       int rc = gemm(false, g, 1, s, true);
       if (rc) return rc;
-      rc = pairk::build_predict_op(ws.D, sqrt_lam, w, basis, predict_op, s);
+      rc = modal::build_predict_op(ws.D, sqrt_lam, w, basis, predict_op, ws.Lp, ws.X, s);
       if (rc) return rc;
     } else {
       const int64_t pr = op_rows(m), pc = op_cols(m);

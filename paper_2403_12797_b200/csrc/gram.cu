@@ -25,7 +25,7 @@
 #include <cstring>
 
 #include "common.cuh"
-#include "pair.cuh"
+#include "modal.cuh"
 
 namespace fagp {
 namespace gram {
@@ -370,13 +370,13 @@ extern "C" {
 
 int64_t fagp_gram_len(const fagp_basis* basis) {
   if (check_basis(basis) != FAGP_OK) return -1;
-  if (pairk::enabled(basis->p, basis->M)) return pairk::gram_len(basis);
+  if (modal::enabled(basis->p, basis->M)) return modal::gram_len(basis);
   return (basis->m + 1) * (basis->m + 2) / 2;
 }
 
 size_t fagp_gram_workspace_size(int64_t N, const fagp_basis* basis) {
   if (check_basis(basis) != FAGP_OK || N < 0) return 0;
-  if (pairk::enabled(basis->p, basis->M)) return pairk::gram_workspace(N, basis);
+  if (modal::enabled(basis->p, basis->M)) return modal::gram_workspace(N, basis);
   const gram::Plan pl = gram::choose(N, basis).plan;
   return size_t(pl.S) * pl.npairs * pl.BT * pl.BT * sizeof(double);
 }
@@ -386,8 +386,8 @@ int fagp_gram(const double* T, int64_t N, const fagp_basis* basis, double* gram_
   int st = check_basis(basis);
   if (st) return st;
   if (N < 0 || gram_ext_packed == nullptr || (N > 0 && T == nullptr)) return FAGP_EINVAL;
-  if (pairk::enabled(basis->p, basis->M))
-    return pairk::gram(T, N, basis, gram_ext_packed, workspace, workspace_bytes, flags, static_cast<cudaStream_t>(stream));
+  if (modal::enabled(basis->p, basis->M))
+    return modal::gram(T, N, basis, gram_ext_packed, workspace, workspace_bytes, flags, static_cast<cudaStream_t>(stream));
   const gram::Choice ch = gram::choose(N, basis);
   const gram::Plan pl = ch.plan;
   const size_t need = size_t(pl.S) * pl.npairs * pl.BT * pl.BT * sizeof(double);
@@ -414,7 +414,7 @@ int fagp_gram(const double* T, int64_t N, const fagp_basis* basis, double* gram_
 
 size_t fagp_phi_tmatvec_workspace_size(int64_t N, const fagp_basis* basis) {
   if (check_basis(basis) != FAGP_OK || N < 0) return 0;
-  if (pairk::enabled(basis->p, basis->M)) return pairk::tmatvec_workspace(N, basis);
+  if (modal::enabled(basis->p, basis->M)) return modal::tmatvec_workspace(N, basis);
   // direct form: the packed [G | t] Gram and its workspace (p = 1: the SYRK is the cheap part)
   return fagp_gram_workspace_size(N, basis) + size_t(round_up(fagp_gram_len(basis), 2)) * sizeof(double);
 }
@@ -432,12 +432,12 @@ int fagp_phi_tmatvec(double* T, int64_t N, const fagp_basis* basis, const double
   }
   st = fagp_set_residual(T, N, basis, v, 0.0, stream);
   if (st) return st;
-  if (pairk::enabled(basis->p, basis->M)) return pairk::tmatvec(T, N, basis, out, workspace, workspace_bytes, s);
+  if (modal::enabled(basis->p, basis->M)) return modal::tmatvec(T, N, basis, out, workspace, workspace_bytes, s);
   const size_t gws = fagp_gram_workspace_size(N, basis);
   double* packed = reinterpret_cast<double*>(static_cast<char*>(workspace) + gws);
   st = fagp_gram(T, N, basis, packed, workspace, gws, nullptr, stream);
   if (st) return st;
-  return fagp_gram_unpack(packed, basis, nullptr, out, stream);
+  return fagp_gram_unpack(packed, basis, nullptr, out, nullptr, 0, stream);
 }
 
 }  // extern "C"

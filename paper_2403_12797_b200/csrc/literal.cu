@@ -9,7 +9,7 @@
 //   fagp_inner_operand     pair-folded predict operand from an explicit inner matrix
 //   fagp_rowdot            var_i = sum_j A[i, j] B[i, j] (direct-form variance of Phi* inner Phi*^T)
 #include "common.cuh"
-#include "pair.cuh"
+#include "modal.cuh"
 
 namespace fagp {
 namespace lit {
@@ -103,13 +103,21 @@ int fagp_literal_inner(const double* mid, const double* lam_f, int64_t m, double
   return FAGP_OK;
 }
 
+size_t fagp_inner_operand_workspace_size(const fagp_basis* basis) {
+  if (check_basis(basis) != FAGP_OK || !modal::enabled(basis->p, basis->M)) return 0;
+  return size_t(modal::scratch_len(basis)) * sizeof(double);
+}
+
 int fagp_inner_operand(const double* inner, const double* w, const fagp_basis* basis, double* predict_op,
-                       void* stream) {
+                       void* workspace, size_t workspace_bytes, void* stream) {
   int st = check_basis(basis);
   if (st) return st;
-  if (!pairk::enabled(basis->p, basis->M)) return FAGP_EUNSUPPORTED;  // checked first: callers probe the form
+  if (!modal::enabled(basis->p, basis->M)) return FAGP_EUNSUPPORTED;  // checked first: callers probe the form
   if (inner == nullptr || w == nullptr || predict_op == nullptr) return FAGP_EINVAL;
-  return pairk::build_predict_op(inner, nullptr, w, basis, predict_op, static_cast<cudaStream_t>(stream));
+  if (workspace == nullptr || workspace_bytes < fagp_inner_operand_workspace_size(basis)) return FAGP_EWORKSPACE;
+  double* S0 = static_cast<double*>(workspace);
+  double* S1 = S0 + modal::scratch_len(basis) / 2;
+  return modal::build_predict_op(inner, nullptr, w, basis, predict_op, S0, S1, static_cast<cudaStream_t>(stream));
 }
 
 int fagp_rowdot(const double* A, const double* B, int64_t n, int64_t k, double* out, void* stream) {

@@ -19,7 +19,7 @@
 #include <cstring>
 
 #include "common.cuh"
-#include "pair.cuh"
+#include "modal.cuh"
 
 namespace fagp {
 namespace pred {
@@ -360,7 +360,7 @@ int fagp_phi_matvec(const double* T, int64_t N, const fagp_basis* basis, const d
   if (st) return st;
   if (N < 0 || (N > 0 && (T == nullptr || x == nullptr || out == nullptr))) return FAGP_EINVAL;
   if (basis->p > 8) return FAGP_EUNSUPPORTED;
-  return pairk::matvec(T, N, basis, x, mean_const, out, flags, static_cast<cudaStream_t>(stream));
+  return modal::matvec(T, N, basis, x, mean_const, out, flags, static_cast<cudaStream_t>(stream));
 }
 
 int fagp_predict(const double* Ts, int64_t Ns, const fagp_basis* basis, const double* predict_op, double sigma2,
@@ -369,8 +369,8 @@ int fagp_predict(const double* Ts, int64_t Ns, const fagp_basis* basis, const do
   if (st) return st;
   if (Ns < 0 || predict_op == nullptr || (Ns > 0 && (Ts == nullptr || mean == nullptr))) return FAGP_EINVAL;
   if (Ns == 0) return FAGP_OK;
-  if (pairk::enabled(basis->p, basis->M))
-    return pairk::predict(Ts, Ns, basis, predict_op, sigma2, mean_const, mean, var, flags,
+  if (modal::enabled(basis->p, basis->M))
+    return modal::predict(Ts, Ns, basis, predict_op, sigma2, mean_const, mean, var, flags,
                           static_cast<cudaStream_t>(stream));
   const int64_t pc = round_up(basis->m + 1, pred::OP_COL_ALIGN);
   const int W = table_width(basis->p, basis->M);

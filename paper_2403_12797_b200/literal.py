@@ -142,7 +142,10 @@ def literal_posterior(basis, T, Ts, yd, noise_var, mean_const, want_var=True, wa
     pair = _pair_form(basis)
     if pair:
         op = dev.empty((int(L.fagp_predict_operand_len(basis.ref)),), device=device)
-        _lib.check(L.fagp_inner_operand(_lib.ptr(inner), _lib.ptr(w), basis.ref, _lib.ptr(op), s), "inner_operand")
+        wsz = int(L.fagp_inner_operand_workspace_size(basis.ref))
+        ws = dev.empty((max(1, wsz // 8),), device=device)
+        _lib.check(L.fagp_inner_operand(_lib.ptr(inner), _lib.ptr(w), basis.ref, _lib.ptr(op), _lib.ptr(ws), wsz, s),
+                   "inner_operand")
         mean = dev.empty((Ns,), device=device)
         var = dev.empty((Ns,), device=device) if want_var else None
         if Ns > 0:
@@ -162,8 +165,8 @@ def literal_posterior(basis, T, Ts, yd, noise_var, mean_const, want_var=True, wa
 
 
 def _pair_form(basis):
-    """True when the library runs the pair-structured kernels for this basis (2 <= p <= 8)."""
-    st = _lib.lib().fagp_inner_operand(None, None, basis.ref, None, None)
+    """True when the library runs the modal kernels for this basis (2 <= p <= 8)."""
+    st = _lib.lib().fagp_inner_operand(None, None, basis.ref, None, None, 0, None)
     if st == _lib.FAGP_EUNSUPPORTED:
         return False
     if st == _lib.FAGP_EINVAL:

@@ -15,6 +15,7 @@ never reads it: the Gram and predict kernels generate feature tiles on chip.
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass, field
 
@@ -136,9 +137,18 @@ def basis_table(params, n, delta2_variant=DELTA2_RHO_SQUARED):
         nd.append(-sp.delta2)  # mercer.py:281
         sb.append(math.sqrt(sp.beta))  # mercer.py:281
         lam.append(eigenvalues_1d(k, n, delta2_variant))
-    table = np.concatenate([np.array(rb), np.array(nd), np.array(sb), np.concatenate(lam)])
-    assert table.shape == (3 * p + p * n,)
+    modal = modal_coeffs(n)
+    table = np.concatenate([np.array(rb), np.array(nd), np.array(sb), np.concatenate(lam), modal.reshape(-1)])
+    assert table.shape == (int(_lib.load().fagp_basis_table_len(p, n)),)
     return table
+
+
+def modal_coeffs(n):
+    """V (P x L): h_a(z) h_b(z) = sum_k V[pair(a,b), k] h_k(sqrt2 z) (fagp_modal_coeffs, host)."""
+    P, L = n * (n + 1) // 2, 2 * n - 1
+    out = np.empty((P, L))
+    _lib.check(_lib.load().fagp_modal_coeffs(int(n), out.ctypes.data_as(ctypes.c_void_p)), "modal_coeffs")
+    return out
 
 
 class Basis:

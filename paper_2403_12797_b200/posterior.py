@@ -192,10 +192,13 @@ def factor_packed(basis, packed, noise_var, mean_const, N, keep_gram=False, stre
 
 def gram_unpack(basis, packed):
     """Full symmetric G (m x m) and t (m) from a `gram` buffer (device tensors)."""
+    L = _lib.lib()
     G = dev.empty((basis.m, basis.m), device=packed.device)
     t = dev.empty((basis.m,), device=packed.device)
-    _lib.check(_lib.lib().fagp_gram_unpack(_lib.ptr(packed), basis.ref, _lib.ptr(G), _lib.ptr(t),
-                                           _lib.stream_handle()), "gram_unpack")
+    wsz = int(L.fagp_gram_unpack_workspace_size(basis.ref))
+    ws = dev.empty((max(1, wsz // 8),), device=packed.device)
+    _lib.check(L.fagp_gram_unpack(_lib.ptr(packed), basis.ref, _lib.ptr(G), _lib.ptr(t), _lib.ptr(ws), wsz,
+                                  _lib.stream_handle()), "gram_unpack")
     return G, t
 
 

@@ -36,15 +36,16 @@ def test_host_only_entry_points():
     lib = _lib.load()
     assert lib.fagp_abi_version() == _lib.ABI_VERSION
     assert lib.fagp_strerror(_lib.FAGP_ENOTPD) == b"matrix is not positive definite"
-    assert lib.fagp_basis_table_len(3, 10) == 3 * 3 + 30
+    assert lib.fagp_basis_table_len(3, 10) == 3 * 3 + 30 + 55 * 19  # + modal coefficients
     b3 = _lib.FagpBasis(3, 10, 1000, 8)  # table pointer is not dereferenced by host-only calls
-    assert lib.fagp_gram_len(ctypes.byref(b3)) == 55**3 + 1000  # pair form [H | t]
+    assert lib.fagp_gram_len(ctypes.byref(b3)) == 19**3 + 1000  # modal form [K | t]
     b1 = _lib.FagpBasis(1, 10, 10, 8)
     assert lib.fagp_gram_len(ctypes.byref(b1)) == 11 * 12 // 2  # p == 1: packed [Phi | r] SYRK
     assert lib.fagp_predict_operand_len(ctypes.byref(b1)) == 32 * 128
-    assert lib.fagp_predict_operand_len(ctypes.byref(b3)) >= 55**3 + 1000
+    assert lib.fagp_predict_operand_len(ctypes.byref(b3)) == 368 * 24 + 1000  # C'' (KP x NP) | w
     assert lib.fagp_factor_workspace_size(1000) > 0
-    assert lib.fagp_table_width(3, 10) == 34
+    assert lib.fagp_table_width(3, 10) == 34 + 60  # phi-section | g-section
+    assert lib.fagp_table_width(1, 10) == 14
     b = _lib.FagpBasis(3, 10, 1000, None)
     assert lib.fagp_gram_workspace_size(1000000, ctypes.byref(b)) == 0  # null table is rejected
     assert lib.fagp_gram_workspace_size(1000000, ctypes.byref(b3)) > 0

@@ -25,3 +25,14 @@ for rep in range(3):
     t5 = tick(); r = F.fagp_posterior(T, Xsp, model, memory_cap=None)
     t6 = tick()
     print(f"h2d {1e3*(t1-t0):.2f} engine {1e3*(t2-t1):.2f} run {1e3*(t3-t2):.2f} check {1e3*(t4-t3):.2f} d2h {1e3*(t5-t4):.2f} | api total {1e3*(t6-t5):.2f} ms")
+
+import cProfile, pstats, io
+pr = cProfile.Profile()
+torch.cuda.synchronize()
+pr.enable()
+r = F.fagp_posterior(T, Xsp, model, memory_cap=None)
+torch.cuda.synchronize()
+pr.disable()
+sio = io.StringIO()
+pstats.Stats(pr, stream=sio).sort_stats("cumulative").print_stats(30)
+print(sio.getvalue())
