@@ -14,9 +14,11 @@
 // The host-side driver keeps the reference's jitter schedule: [0, b, 10b, 100b] with
 // b = 1e-12 * trace(A) / m, trace in numpy's summation order.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
+#include "chol.cuh"
 #include "modal.cuh"
 
 namespace fagp {
@@ -216,6 +218,8 @@ __global__ void __launch_bounds__(32) chol_panel_kernel(double* __restrict__ A, 
   }
 }
 
+__global__ void zero_upper_kernel(double* A, int64_t m);
+
 int potrf_blocked(double* A, int64_t m, int64_t lda, int* info, cudaStream_t s) {
   for (int64_t k0 = 0; k0 < m; k0 += 32) {
     const int nb = int(tmin<int64_t>(32, m - k0));
@@ -229,6 +233,21 @@ int potrf_blocked(double* A, int64_t m, int64_t lda, int* info, cudaStream_t s) 
     int st = gemm(true, upd, 1, s);
     if (st) return st;
   }
+  return FAGP_OK;
+}
+
+// One cooperative launch (chol.cu) unless FAGP_POTRF=blocked or the device cannot co-schedule
+// the grid; scratch: chol_scratch_len(m) doubles.  Upper triangle is zeroed.
+int potrf(double* A, int64_t m, int64_t lda, int* info, double* scratch, cudaStream_t s) {
+  const char* e = getenv("FAGP_POTRF");
+  if (!(e && strcmp(e, "blocked") == 0)) {
+    const int rc = potrf_persistent(A, m, lda, info, scratch, s);
+    if (rc != FAGP_EUNSUPPORTED) return rc;
+  }
+  const int rc = potrf_blocked(A, m, lda, info, s);
+  if (rc) return rc;
+  zero_upper_kernel<<<int(tmin<int64_t>(ceil_div(m * m, 256), 8 * num_sms())), 256, 0, s>>>(A, m);
+  FAGP_LAUNCH_CHECK();
   return FAGP_OK;
 }
 
@@ -549,7 +568,8 @@ struct FactorWs {
   double* Lp;      // mp2^2
   double* X;       // mp2^2
   double* Tmp;     // mp2^2 / 4
-  double* D;       // m x m: X^T X for the pair-form predict operand
+  double* D;       // m x m: X^T X for the modal predict operand
+  double* chol;    // chol_scratch_len(m)
   size_t bytes;
 };
 
@@ -573,11 +593,14 @@ inline FactorWs carve(void* base, int64_t m) {
   w.X = reinterpret_cast<double*>(take(size_t(mp) * mp * sizeof(double)));
   w.Tmp = reinterpret_cast<double*>(take(size_t(mp) * mp / 4 * sizeof(double) + sizeof(double)));
   w.D = reinterpret_cast<double*>(take(size_t(m) * m * sizeof(double)));
+  w.chol = reinterpret_cast<double*>(take(size_t(chol_scratch_len(m)) * sizeof(double)));
   w.bytes = off;
   return w;
 }
 
-inline size_t potrf_ws_bytes() { return align256(sizeof(int)) + align256(32 * 32 * sizeof(double)); }
+inline size_t potrf_ws_bytes(int64_t m) {
+  return align256(sizeof(int)) + align256(32 * 32 * sizeof(double)) + align256(size_t(chol_scratch_len(m)) * sizeof(double));
+}
 
 }  // namespace la
 }  // namespace fagp
@@ -626,14 +649,16 @@ int fagp_gram_unpack(const double* gram, const fagp_basis* basis, double* G, dou
   return FAGP_OK;
 }
 
-size_t fagp_potrf_workspace_size(int64_t m) { return m < 1 ? 0 : potrf_ws_bytes(); }
+size_t fagp_potrf_workspace_size(int64_t m) { return m < 1 ? 0 : potrf_ws_bytes(m); }
 
 int fagp_potrf(double* A, int64_t m, int32_t* info_dev, void* workspace, size_t workspace_bytes, void* stream) {
   if (A == nullptr || m < 1 || info_dev == nullptr) return FAGP_EINVAL;
-  if (workspace == nullptr || workspace_bytes < potrf_ws_bytes()) return FAGP_EWORKSPACE;
+  if (workspace == nullptr || workspace_bytes < potrf_ws_bytes(m)) return FAGP_EWORKSPACE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   FAGP_CUDA_TRY(cudaMemsetAsync(info_dev, 0, sizeof(int32_t), s));
-  return potrf_blocked(A, m, m, reinterpret_cast<int*>(info_dev), s);
+  double* diag = reinterpret_cast<double*>(static_cast<char*>(workspace) + align256(sizeof(int)) +
+                                           align256(32 * 32 * sizeof(double)));
+  return potrf(A, m, m, reinterpret_cast<int*>(info_dev), diag, s);
 }
 
 int fagp_potrs(const double* L, int64_t m, double* B, int64_t nrhs, void* stream) {
@@ -758,7 +783,7 @@ int fagp_factor(const double* packed, const fagp_basis* basis, const double* sqr
       if (rc1) return rc1;
     }
     FAGP_CUDA_TRY(cudaMemsetAsync(ws.info, 0, sizeof(int), s));
-    int rc = potrf_blocked(L, m, m, ws.info, s);
+    int rc = potrf(L, m, m, ws.info, ws.chol, s);
     if (rc) return rc;
     FAGP_CUDA_TRY(cudaMemcpyAsync(&info_h, ws.info, sizeof(int), cudaMemcpyDeviceToHost, s));
     FAGP_CUDA_TRY(cudaStreamSynchronize(s));

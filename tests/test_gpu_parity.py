@@ -222,3 +222,35 @@ def test_c3_full_size_properties():
     ref = O.posterior(ds.X, ds.y, Xs[idx], [1.0] * p, [1.0] * p, M, 0.0025, block=65536)
     assert rel_err(a.mean[idx], ref["mean"]) <= MEAN_VAR_RTOL
     assert rel_err(a.var[idx], ref["var"]) <= MEAN_VAR_RTOL
+
+
+@pytest.mark.parametrize("impl", ["persistent", "blocked"])
+@pytest.mark.parametrize("m", [1, 5, 31, 32, 33, 64, 100, 257, 1000])
+def test_potrf_matches_lapack(m, impl, monkeypatch):
+    """fagp_potrf (persistent cooperative kernel, and the blocked fallback) against LAPACK
+    dpotrf on SPD matrices, and LAPACK's 1-based info on an indefinite one."""
+    import scipy.linalg as sla
+
+    from paper_2403_12797_b200.linalg import potrf
+
+    if impl == "blocked":
+        monkeypatch.setenv("FAGP_POTRF", "blocked")
+    rng = np.random.default_rng(m)
+    B = rng.standard_normal((m, m))
+    A = B @ B.T + m * np.eye(m)
+    L, info = potrf(A)
+    assert info == 0
+    Lh = dev.to_host(L)
+    ref = np.linalg.cholesky(A)
+    assert np.array_equal(np.triu(Lh, 1), np.zeros((m, m)))
+    assert np.max(np.abs(Lh - ref)) / np.max(np.abs(ref)) < 1e-13
+    if m >= 5:
+        # indefinite: eigenvalue -1 placed so the breakdown lands mid-matrix
+        q, _ = np.linalg.qr(rng.standard_normal((m, m)))
+        ev = np.linspace(1.0, 2.0, m)
+        ev[m // 2] = -1.0
+        Ai = (q * ev) @ q.T
+        Ai = 0.5 * (Ai + Ai.T)
+        _, info_ref = sla.lapack.dpotrf(Ai, lower=1)
+        _, info = potrf(Ai)
+        assert info == info_ref > 0
