@@ -48,7 +48,7 @@ CONFIGS = {
 METRIC = "posterior mean+var samples/s (N=1e6, p=3, M=10); % FP64 tensor peak"
 NOISE_VAR = 0.0025
 FP64_PEAK_FILE = ROOT / "profiles" / "fp64_peak_r01.json"
-NCU_SUMMARY_FILE = ROOT / "profiles" / "ncu_summary_r01.json"
+NCU_SUMMARY_FILE = ROOT / "profiles" / "ncu_summary_r01m.json"
 
 
 def log(*a):
@@ -141,11 +141,16 @@ def fp64_peak():
 
 
 def ncu_traffic(kernel):
+    """DRAM bytes per launch (read + write) of the kernel whose name starts with `kernel`,
+    from the committed ncu --set full summary (None when it was not captured)."""
     try:
         d = json.loads(NCU_SUMMARY_FILE.read_text())
-        return d["kernels"][kernel]["dram_bytes_per_launch"]
+        for name, ent in d["kernels"].items():
+            if name.split("<")[0].split("::")[-1] == kernel:
+                return ent.get("dram_bytes_per_launch")
     except (OSError, KeyError, ValueError):
-        return None
+        pass
+    return None
 
 
 def make_inputs(cfg, rank, world):
@@ -325,11 +330,11 @@ def main():
     if g_ms >= p_ms:
         dom, dflops, rflops, dms = "fagp_gram (modal DMMA GEMM + reduce + t)" if pair else \
             "fagp_gram (fused SYRK + reduce)", gram_flops, ref_gram, g_ms
-        traffic = ncu_traffic("gram_kernel")
+        traffic = ncu_traffic("modal_gram_kernel" if pair else "gram_kernel_fast")
     else:
         dom, dflops, rflops, dms = "fagp_predict (modal variance GEMM + mean)" if pair else \
             "fagp_predict (fused triangular GEMM)", pred_flops, ref_pred, p_ms
-        traffic = ncu_traffic("predict_kernel")
+        traffic = ncu_traffic("modal_var_kernel" if pair else "predict_kernel_fast")
     achieved = dflops / (dms / 1e3) / 1e12
     roofline = {"bound": "tensor", "kernel": dom, "achieved": round(achieved, 3), "peak": peak, "unit": "TFLOP/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
