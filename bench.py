@@ -61,7 +61,7 @@ def useful_flops(N, Ns, m):
     return N * m * (m + 1) + 2 * N * m + 2 * m**3 / 3 + 2 * Ns * m + Ns * m * (m + 1) + 2 * Ns * m
 
 
-def launches_per_step(m, pair, p=1):
+def launches_per_step(m, pair, p=1, fused=False):
     """Kernels of ours launched by one PosteriorEngine.run() (no jitter retry)."""
     nblk = -(-m // 32)
     potrf = nblk + (nblk - 1)  # fused diag+panel kernel per step, trailing GEMM between steps
@@ -79,6 +79,8 @@ def launches_per_step(m, pair, p=1):
         # launch), zero upper, trtri, w GEMVs x2, D = X^T X, Ct, Ct -> C'' (p mode products),
         # scatter, w copy
         factor = p + 1 + 1 + 1 + 1 + trtri + 2 + 1 + 1 + p + 1 + 1
+        if fused:
+            return 2 + factor + 1  # fused Gram + partial sum, factor, fused mean + variance
         return 2 + 2 + factor + 2  # basis_eval x2, modal GEMM + reduce, factor, var + mean
     factor = 1 + 1 + potrf + 1 + trtri + 2 + 1  # build G/t, build A, potrf, zero upper, trtri, GEMVs, operand
     return 2 + 2 + factor + 1  # basis_eval x2, gram + reduce, factor, predict
@@ -274,7 +276,7 @@ def main():
 
     for _ in range(args.warmup):
         eng.run(X, y, Xs)
-    eng.check(X, Xs)
+    eng.check(X, Xs, y)
     torch.cuda.synchronize()
 
     stream = torch.cuda.current_stream()
@@ -287,16 +289,15 @@ def main():
             e = ev[k]
             e[0].record(stream)
             eng.flags.zero_()
-            eng.stage_tables(X, y, Xs)
             e[1].record(stream)
-            eng.stage_gram()
+            eng.stage_gram(X, y)
             e[2].record(stream)
             eng.stage_reduce()
             st = eng.stage_factor()
             if st != 0:
-                eng.raise_errors(X, Xs, factor_failed=True)
+                eng.raise_errors(X, Xs, y, factor_failed=True)
             e[3].record(stream)
-            eng.stage_predict()
+            eng.stage_predict(Xs)
             e[4].record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -305,7 +306,7 @@ def main():
     factor_ms = [e[2].elapsed_time(e[3]) for e in ev]
     pred_ms = [e[3].elapsed_time(e[4]) for e in ev]
     tab_ms = [e[0].elapsed_time(e[1]) for e in ev]
-    eng.check(X, Xs)
+    eng.check(X, Xs, y)
     ms = statistics.mean(step_ms)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=X.device)
@@ -386,8 +387,8 @@ def main():
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator)",
                "config": config_dict(args, world), "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
-               "clocks": clk.summary(), "gpu_launches": launches_per_step(m, 2 <= p <= 8, p) * args.steps,
-               "phases_ms": {"tables": round(statistics.mean(tab_ms), 3), "gram": round(g_ms, 3),
+               "clocks": clk.summary(), "gpu_launches": launches_per_step(m, 2 <= p <= 8, p, fused=eng.pred_ws_bytes == 0) * args.steps,
+               "phases_ms": {"gram": round(g_ms, 3),
                              "allreduce+factor": round(statistics.mean(factor_ms), 3), "predict": round(p_ms, 3)},
                "step_reference_equivalent_tflops": round(step_tf, 3),
                "jitter": eng.jitter.value, "lib": str(_lib.LIB_PATH.name)}

@@ -145,6 +145,16 @@ size_t fagp_gram_workspace_size(int64_t N, const fagp_basis* basis);
 int fagp_gram(const double* T, int64_t N, const fagp_basis* basis, double* gram, void* workspace,
               size_t workspace_bytes, uint32_t* flags, void* stream);
 
+/* The same `gram` buffer straight from the points: X (N x p) and y (N, nullable: t = 0),
+ * r = y - mean_const (posterior.py:229).  For the modal shapes whose output fits one CTA's
+ * registers (p <= 4, e.g. BASELINE C2/C3) the 1-D eigenfunctions are evaluated on chip by
+ * producer warps and no basis table ever reaches HBM (fused.cu); other shapes evaluate a
+ * table into the workspace and run fagp_gram.  Same output, determinism and flags as
+ * fagp_gram (FAGP_FLAG_X_NONFINITE for a non-finite coordinate, mercer.py:334-335). */
+size_t fagp_gram_x_workspace_size(int64_t N, const fagp_basis* basis);
+int fagp_gram_x(const double* X, int64_t N, const fagp_basis* basis, const double* y, double mean_const,
+                double* gram, void* workspace, size_t workspace_bytes, uint32_t* flags, void* stream);
+
 /* Expand a `gram` buffer into the full symmetric G (m x m, nullable) and t (m, nullable).
  * The modal form needs fagp_gram_unpack_workspace_size(basis) bytes of workspace for G. */
 size_t fagp_gram_unpack_workspace_size(const fagp_basis* basis);
@@ -206,6 +216,18 @@ int fagp_trtri(const double* L, const double* s, int64_t m, double* V, void* wor
 int fagp_predict(const double* Ts, int64_t Ns, const fagp_basis* basis, const double* predict_op,
                  double sigma2, double mean_const, double* mean, double* var, uint32_t* flags,
                  void* stream);
+
+/* fagp_predict straight from the test points Xs (Ns x p): mean and variance
+ * (posterior.py:247, 249-263 diagonal) in one fused pass -- producer warps evaluate the
+ * eigenfunctions on chip, the variance operand and mean weights sit in shared memory, and
+ * both contractions run on the DMMA pipe (fused.cu) -- for the modal shapes whose operand
+ * fits shared memory (p <= 4, M <= 24, e.g. BASELINE C2/C3); other shapes evaluate a table
+ * into the workspace (fagp_predict_x_workspace_size bytes, 0 on the fused path) and run
+ * fagp_predict.  var may be NULL. */
+size_t fagp_predict_x_workspace_size(int64_t Ns, const fagp_basis* basis);
+int fagp_predict_x(const double* Xs, int64_t Ns, const fagp_basis* basis, const double* predict_op,
+                   double sigma2, double mean_const, double* mean, double* var, uint32_t* flags,
+                   void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- (6) method="literal": the reference's cross-check route ---------------------------
  * posterior.py:236-244 (mean through t1..t5) and 256-260 (inner covariance).  Built from

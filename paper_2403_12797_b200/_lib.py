@@ -70,6 +70,10 @@ SIGNATURES = {
     "fagp_gram_unpack": (ctypes.c_int, [_P, _BASIS, _P, _P, _P, ctypes.c_size_t, _P]),
     "fagp_gram_workspace_size": (_SZ, [_I64, _BASIS]),
     "fagp_gram": (ctypes.c_int, [_P, _I64, _BASIS, _P, _P, _SZ, _P, _P]),
+    "fagp_gram_x_workspace_size": (_SZ, [_I64, _BASIS]),
+    "fagp_gram_x": (ctypes.c_int, [_P, _I64, _BASIS, _P, _D, _P, _P, _SZ, _P, _P]),
+    "fagp_predict_x_workspace_size": (_SZ, [_I64, _BASIS]),
+    "fagp_predict_x": (ctypes.c_int, [_P, _I64, _BASIS, _P, _D, _D, _P, _P, _P, _P, _SZ, _P]),
     "fagp_factor_workspace_size": (_SZ, [_I64]),
     "fagp_predict_operand_len": (_I64, [_BASIS]),
     "fagp_factor": (ctypes.c_int, [_P, _BASIS, _P, _D, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),

@@ -155,16 +155,15 @@ def run_sweep(cfg, row_sink=None, progress=None, want_var=False):
                 t1 = now()
                 eng = PosteriorEngine(kernel, n, cfg.n_samples, cfg.n_test, cfg.noise_var, 0.0, device=X.device,
                                       want_var=want_var)
-                eng.stage_tables(X, y, Xd)
-                t2 = now()
-                eng.stage_gram()
+                t2 = now()  # "eigen": the eigenfunctions are evaluated on chip inside the two kernels below
+                eng.stage_gram(X, y)
                 if eng.stage_factor() != 0:
-                    eng.raise_errors(X, Xd, factor_failed=True)
-                eng.stage_predict()
+                    eng.raise_errors(X, Xd, y, factor_failed=True)
+                eng.stage_predict(Xd)
                 t3 = now()
                 dev.to_host(eng.mean)
                 t4 = now()
-                eng.check(X, Xd)
+                eng.check(X, Xd, y)
                 for phase, sec in zip(PHASES, (t1 - t0, t2 - t1, t3 - t2, t4 - t3)):
                     emit((BACKEND_NAME, p, n, rep, phase, sec))
                 if progress:

@@ -16,16 +16,9 @@
 #include <vector>
 
 #include "common.cuh"
+#include "eigfun.cuh"
 
 namespace fagp {
-
-// Recurrence coefficients exactly as the reference computes them with Python floats:
-// c1[k] = sqrt(2/(k+1)), c2[k] = sqrt(k/(k+1))  (mercer.py:137-142).  IEEE division and
-// square root are correctly rounded on both sides, so these are bit-identical.
-__device__ __forceinline__ double herm_c1(int k) { return __dsqrt_rn(__ddiv_rn(2.0, double(k + 1))); }
-__device__ __forceinline__ double herm_c2(int k) {
-  return __dsqrt_rn(__ddiv_rn(double(k), double(k + 1)));
-}
 
 __global__ void hermite_kernel(const double* __restrict__ z, int64_t n, int count,
                                double* __restrict__ out) {
@@ -35,7 +28,7 @@ __global__ void hermite_kernel(const double* __restrict__ z, int64_t n, int coun
     coef[count + k] = herm_c2(k);
   }
   __syncthreads();
-  const double sqrt2 = 1.4142135623730951;  // math.sqrt(2.0)
+  const double sqrt2 = kSqrt2;
   for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n;
        r += int64_t(gridDim.x) * blockDim.x) {
     const double zr = z[r];
@@ -80,47 +73,12 @@ __global__ void basis_eval_kernel(const double* __restrict__ X, int64_t N, Basis
   const int nrows = int(tmin<int64_t>(rows_per_cta, N - row0));
   __syncthreads();
   bool bad_x = false;
-  const double sqrt2 = 1.4142135623730951;
   for (int task = threadIdx.x; task < nrows * p; task += blockDim.x) {
     const int rl = task / p, d = task - rl * p;
     const double x = X[(row0 + rl) * p + d];
     bad_x |= not_finite(x);
-    const double zr = __dmul_rn(b.rho_beta()[d], x);
-    // sqrt(beta) * exp((-delta2 * x) * x)
-    const double env = __dmul_rn(b.sqrt_beta()[d], exp(__dmul_rn(__dmul_rn(b.neg_delta2()[d], x), x)));
-    double* o = stage + rl * W + d * M;
-    double hm1 = 1.0;
-    o[0] = __dmul_rn(env, 1.0);
-    if (M > 1) {
-      double h = __dmul_rn(zr, sqrt2);
-      o[1] = __dmul_rn(env, h);
-      for (int k = 1; k < M - 1; ++k) {
-        double hn = __dsub_rn(__dmul_rn(__dmul_rn(zr, c1[k]), h), __dmul_rn(c2[k], hm1));
-        o[k + 1] = __dmul_rn(env, hn);
-        hm1 = h;
-        h = hn;
-      }
-    }
-    if (modal) {
-      // beta * exp(-2 delta2 x^2) * h_k(sqrt2 z), k < L
-      const double sb = b.sqrt_beta()[d];
-      const double amp = __dmul_rn(__dmul_rn(sb, sb),
-                                   exp(__dmul_rn(__dmul_rn(__dmul_rn(2.0, b.neg_delta2()[d]), x), x)));
-      const double yz = __dmul_rn(zr, sqrt2);
-      double* g = stage + rl * W + G0 + d * L;
-      double gm1 = 1.0;
-      g[0] = amp;
-      if (L > 1) {
-        double h = __dmul_rn(yz, sqrt2);
-        g[1] = __dmul_rn(amp, h);
-        for (int k = 1; k < L - 1; ++k) {
-          double hn = __dsub_rn(__dmul_rn(__dmul_rn(yz, c1[k]), h), __dmul_rn(c2[k], gm1));
-          g[k + 1] = __dmul_rn(amp, hn);
-          gm1 = h;
-          h = hn;
-        }
-      }
-    }
+    eval_phi_dim(x, b, d, c1, c2, stage + rl * W + d * M);
+    if (modal) eval_g_dim(x, b, d, c1, c2, stage + rl * W + G0 + d * L);
   }
   for (int rl = threadIdx.x; rl < nrows; rl += blockDim.x) {
     double* o = stage + rl * W;

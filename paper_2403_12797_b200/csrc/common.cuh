@@ -7,22 +7,32 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <stdio.h>
+#include <stdlib.h>
 #include <stdint.h>
 
 #include "../../include/fagp_b200.h"
 
-#define FAGP_CUDA_TRY(expr)                         \
-  do {                                              \
-    cudaError_t _e = (expr);                        \
-    if (_e != cudaSuccess) return FAGP_ECUDA;       \
+// FAGP_DEBUG=1 in the environment prints the CUDA error behind an FAGP_ECUDA status.
+#define FAGP_CUDA_TRY(expr)                                    \
+  do {                                                         \
+    cudaError_t _e = (expr);                                   \
+    if (_e != cudaSuccess) return ::fagp::cuda_fail(_e, __FILE__, __LINE__); \
   } while (0)
 
-#define FAGP_LAUNCH_CHECK()                          \
-  do {                                               \
-    if (cudaGetLastError() != cudaSuccess) return FAGP_ECUDA; \
+#define FAGP_LAUNCH_CHECK()                                    \
+  do {                                                         \
+    cudaError_t _e = cudaGetLastError();                       \
+    if (_e != cudaSuccess) return ::fagp::cuda_fail(_e, __FILE__, __LINE__); \
   } while (0)
 
 namespace fagp {
+
+__host__ inline int cuda_fail(cudaError_t e, const char* file, int line) {
+  const char* dbg = getenv("FAGP_DEBUG");
+  if (dbg && dbg[0] == '1') fprintf(stderr, "[fagp] %s:%d: %s\n", file, line, cudaGetErrorString(e));
+  return FAGP_ECUDA;
+}
 
 constexpr int kNumSMs = 148;  // B200; only used as a grid-sizing hint (queried at run time)
 

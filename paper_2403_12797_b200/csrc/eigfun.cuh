@@ -1,0 +1,66 @@
+// Per-point 1-D eigenfunction evaluation shared by the table kernel (basis.cu) and the
+// fused kernels that never write a table (fused.cu).  One call = one (point, dimension).
+//
+//   phi_{d,i}(x) = (sqrt_beta_d * exp((-delta2_d * x) * x)) * h_i((rho_d beta_d) * x)   mercer.py:276-281
+//   h_0 = 1, h_1 = z sqrt2, h_{k+1} = (z * c1[k]) * h_k - c2[k] * h_{k-1}            mercer.py:122-143
+//   g_{d,k}(x)   = (beta_d * exp(((2 * -delta2_d) * x) * x)) * h_k(sqrt2 * rho_d beta_d x)   (modal.cu)
+//
+// Every multiply/subtract is an explicit round-to-nearest op so nvcc cannot contract it into
+// an FMA: phi matches numpy's evaluation order bit for bit except for exp().
+#pragma once
+
+#include "common.cuh"
+
+namespace fagp {
+
+// c1[k] = sqrt(2/(k+1)), c2[k] = sqrt(k/(k+1)) exactly as the reference computes them with
+// Python floats (mercer.py:137-142); IEEE division and sqrt are correctly rounded.
+__device__ __forceinline__ double herm_c1(int k) { return __dsqrt_rn(__ddiv_rn(2.0, double(k + 1))); }
+__device__ __forceinline__ double herm_c2(int k) { return __dsqrt_rn(__ddiv_rn(double(k), double(k + 1))); }
+
+constexpr double kSqrt2 = 1.4142135623730951;  // math.sqrt(2.0)
+
+// out[i * stride] = phi_{d,i}(x), i < M
+__device__ __forceinline__ void eval_phi_dim(double x, const BasisView& b, int d, const double* c1, const double* c2,
+                                             double* out, int stride = 1) {
+  const int M = b.M;
+  const double zr = __dmul_rn(b.rho_beta()[d], x);
+  const double env = __dmul_rn(b.sqrt_beta()[d], exp(__dmul_rn(__dmul_rn(b.neg_delta2()[d], x), x)));
+  double hm1 = 1.0;
+  out[0] = __dmul_rn(env, 1.0);
+  if (M > 1) {
+    double h = __dmul_rn(zr, kSqrt2);
+    out[stride] = __dmul_rn(env, h);
+    for (int k = 1; k < M - 1; ++k) {
+      const double hn = __dsub_rn(__dmul_rn(__dmul_rn(zr, c1[k]), h), __dmul_rn(c2[k], hm1));
+      out[(k + 1) * stride] = __dmul_rn(env, hn);
+      hm1 = h;
+      h = hn;
+    }
+  }
+}
+
+// out[k * stride] = g_{d,k}(x), k < L = 2M - 1 (the modal functions spanning phi_a phi_b)
+__device__ __forceinline__ void eval_g_dim(double x, const BasisView& b, int d, const double* c1, const double* c2,
+                                           double* out, int stride = 1) {
+  const int L = modal_L(b.M);
+  const double zr = __dmul_rn(b.rho_beta()[d], x);
+  const double sb = b.sqrt_beta()[d];
+  const double amp =
+      __dmul_rn(__dmul_rn(sb, sb), exp(__dmul_rn(__dmul_rn(__dmul_rn(2.0, b.neg_delta2()[d]), x), x)));
+  const double yz = __dmul_rn(zr, kSqrt2);
+  double gm1 = 1.0;
+  out[0] = amp;
+  if (L > 1) {
+    double h = __dmul_rn(yz, kSqrt2);
+    out[stride] = __dmul_rn(amp, h);
+    for (int k = 1; k < L - 1; ++k) {
+      const double hn = __dsub_rn(__dmul_rn(__dmul_rn(yz, c1[k]), h), __dmul_rn(c2[k], gm1));
+      out[(k + 1) * stride] = __dmul_rn(amp, hn);
+      gm1 = h;
+      h = hn;
+    }
+  }
+}
+
+}  // namespace fagp

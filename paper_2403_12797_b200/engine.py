@@ -2,11 +2,12 @@
 
 One engine per (basis, N, N*) shape.  ``run`` issues, on the current CUDA stream:
 
-    fagp_basis_eval(X), fagp_basis_eval(X*)           K0   1-D eigenfunction tables
-    fagp_gram                                          K1   fused Phi-gen + DMMA Gram (+ t)
+    fagp_gram_x(X, y)                                  K1   eigenfunctions on chip + DMMA Gram (+ t)
     [all_reduce(SUM) of the packed Gram over `group`]  C1   NCCL over NVLink when sharded
-    fagp_factor                                        K2-K4  A, Cholesky+jitter, w, V^T
-    fagp_predict                                       K5   fused Phi*-gen + DMMA + row sums
+    fagp_factor                                        K2-K4  A, Cholesky+jitter, w, predict operand
+    fagp_predict_x(X*)                                 K5   eigenfunctions on chip + DMMA mean + variance
+
+(no basis table reaches HBM on the fused shapes; the others evaluate one into the workspace)
 
 and performs exactly one host synchronisation (inside fagp_factor, which must read the
 Cholesky status to run the reference's jitter schedule).  No allocation happens inside
@@ -39,11 +40,11 @@ class PosteriorEngine:
         self.want_var = want_var
         m, W = b.m, b.width
         e = lambda *shape: dev.empty(shape, device=self.device)  # noqa: E731
-        self.T = e(self.N, W)
-        self.Ts = e(self.Ns, W)
         self.packed = e(int(L.fagp_gram_len(b.ref)))
-        self.gram_ws_bytes = int(L.fagp_gram_workspace_size(self.N, b.ref))
-        self.gram_ws = e(max(1, self.gram_ws_bytes // 8))
+        self.gram_ws_bytes = int(L.fagp_gram_x_workspace_size(self.N, b.ref))
+        self.gram_ws = e(max(1, -(-self.gram_ws_bytes // 8)))
+        self.pred_ws_bytes = int(L.fagp_predict_x_workspace_size(self.Ns, b.ref))
+        self.pred_ws = e(max(1, -(-self.pred_ws_bytes // 8)))
         self.lam, self.lam_floored, self.sqrt_lam = e(m), e(m), e(m)
         self.L = e(m, m)
         self.G = e(m, m) if keep_gram else None
@@ -64,27 +65,21 @@ class PosteriorEngine:
         return ctypes.c_void_p(self.flags.data_ptr() + 4 * k)
 
     # -- stages (each usable alone, e.g. for per-kernel timing) --------------------------
-    def stage_tables(self, X, y, Xs, stream=None):
-        """K0 for train (with the residual column r = y - c) and test rows."""
-        self.stage_train_table(X, y, stream)
-        self.stage_test_table(Xs, stream)
+    def table(self, X, y=None, flag=None):
+        """The 1-D eigenfunction table of X (fagp_basis_eval): only for the error path (naming
+        a non-finite feature) and the optional full covariance -- never on the hot path."""
+        L, b = _lib.lib(), self.basis
+        T = dev.empty((int(X.shape[0]), b.width), device=self.device)
+        if X.shape[0]:
+            _lib.check(L.fagp_basis_eval(_lib.ptr(X), int(X.shape[0]), b.ref, _lib.ptr(y), self.mean_const,
+                                         _lib.ptr(T), flag, _lib.stream_handle()), "basis_eval")
+        return T
 
-    def stage_train_table(self, X, y, stream=None):
+    def stage_gram(self, X, y, stream=None):
+        """K1: eigenfunctions of the train rows + Gram [K | t] (fagp_gram_x)."""
         L, s, b = _lib.lib(), _lib.stream_handle(stream), self.basis
-        if self.N:
-            _lib.check(L.fagp_basis_eval(_lib.ptr(X), self.N, b.ref, _lib.ptr(y), self.mean_const, _lib.ptr(self.T),
-                                         self._flag(0), s), "basis_eval")
-
-    def stage_test_table(self, Xs, stream=None):
-        L, s, b = _lib.lib(), _lib.stream_handle(stream), self.basis
-        if self.Ns:
-            _lib.check(L.fagp_basis_eval(_lib.ptr(Xs), self.Ns, b.ref, None, 0.0, _lib.ptr(self.Ts), self._flag(1), s),
-                       "basis_eval")
-
-    def stage_gram(self, stream=None):
-        L, s, b = _lib.lib(), _lib.stream_handle(stream), self.basis
-        _lib.check(L.fagp_gram(_lib.ptr(self.T), self.N, b.ref, _lib.ptr(self.packed), _lib.ptr(self.gram_ws),
-                               self.gram_ws_bytes, self._flag(0), s), "gram")
+        _lib.check(L.fagp_gram_x(_lib.ptr(X), self.N, b.ref, _lib.ptr(y), self.mean_const, _lib.ptr(self.packed),
+                                 _lib.ptr(self.gram_ws), self.gram_ws_bytes, self._flag(0), s), "gram")
 
     def stage_reduce(self):
         if self.group is not None:
@@ -106,38 +101,37 @@ class PosteriorEngine:
         _lib.check(_lib.lib().fagp_set_mean_weights(_lib.ptr(self.predict_op), _lib.ptr(self.w), self.basis.ref,
                                                     _lib.stream_handle(stream)), "set_mean_weights")
 
-    def stage_predict(self, stream=None):
+    def stage_predict(self, Xs, stream=None):
+        """K5: eigenfunctions of the test rows + mean and variance (fagp_predict_x)."""
         L, s, b = _lib.lib(), _lib.stream_handle(stream), self.basis
         if self.Ns:
-            _lib.check(L.fagp_predict(_lib.ptr(self.Ts), self.Ns, b.ref, _lib.ptr(self.predict_op), self.noise_var,
-                                      self.mean_const, _lib.ptr(self.mean), _lib.ptr(self.var), self._flag(1), s),
-                       "predict")
+            _lib.check(L.fagp_predict_x(_lib.ptr(Xs), self.Ns, b.ref, _lib.ptr(self.predict_op), self.noise_var,
+                                        self.mean_const, _lib.ptr(self.mean), _lib.ptr(self.var), self._flag(1),
+                                        _lib.ptr(self.pred_ws), self.pred_ws_bytes, s), "predict")
 
     # -- the whole step -------------------------------------------------------------------
     def run(self, X, y, Xs, fault_flip=False, xs_ready=None):
         """One posterior evaluation from device-resident inputs; returns device (mean, var).
 
-        The test table is evaluated after the factorisation, so an X* upload still in
-        flight on another stream (``xs_ready``: its event) overlaps the Gram contraction."""
+        X* is first touched by the predict kernel, so an X* upload still in flight on another
+        stream (``xs_ready``: its event) overlaps the Gram contraction and the factorisation."""
         import torch
 
         self.flags.zero_()
-        self.stage_train_table(X, y)
-        self.stage_gram()
+        self.stage_gram(X, y)
         self.stage_reduce()
         st = self.stage_factor()
         if xs_ready is not None:
             torch.cuda.current_stream().wait_event(xs_ready)
-        self.stage_test_table(Xs)
         if st != _lib.FAGP_OK:
-            self.raise_errors(X, Xs, factor_failed=True)
+            self.raise_errors(X, Xs, y, factor_failed=True)
         if fault_flip:
             self.w.neg_()
             self.set_mean_weights()
-        self.stage_predict()
+        self.stage_predict(Xs)
         return self.mean, self.var
 
-    def raise_errors(self, X=None, Xs=None, factor_failed=False, after_predict=False):
+    def raise_errors(self, X=None, Xs=None, y=None, factor_failed=False, after_predict=False):
         """Raise the reference's exception for whatever went wrong (validation order of
         fagp_posterior: train X, train Phi, test X, test Phi, then the factorisation)."""
         fl = [int(v) for v in dev.to_host(self.flags)]
@@ -145,18 +139,23 @@ class PosteriorEngine:
         if fl[0] & _lib.FLAG_X_NONFINITE:
             raise ValueError("X must be finite")
         if fl[0] & _lib.FLAG_PHI_NONFINITE:
-            raise_nonfinite(self.T, X, b)
+            raise_nonfinite(self.table(X, y), X, b)
         if fl[1] & _lib.FLAG_X_NONFINITE:
             raise ValueError("X must be finite")
-        if (fl[1] & _lib.FLAG_PHI_NONFINITE) or factor_failed:
-            if self.Ns:
-                raise_nonfinite(self.Ts, Xs, b)
+        if factor_failed and self.Ns and not fl[1]:
+            # the test rows were not evaluated yet: do it now (sets the X* flag when needed)
+            Ts = self.table(Xs, flag=self._flag(1))
+            if int(dev.to_host(self.flags)[1]) & _lib.FLAG_X_NONFINITE:
+                raise ValueError("X must be finite")
+            raise_nonfinite(Ts, Xs, b)
+        elif fl[1] & _lib.FLAG_PHI_NONFINITE and self.Ns:
+            raise_nonfinite(self.table(Xs), Xs, b)
         if factor_failed:
             piv = int(self.pivot.value)
             raise NumericalError(
                 f"matrix of order {b.m} is not positive definite: leading minor {piv} failed even with "
                 f"diagonal jitter up to the third escalation", pivot_index=piv)
 
-    def check(self, X, Xs):
+    def check(self, X, Xs, y=None):
         """Post-run validation (one small D2H read of the flag words)."""
-        self.raise_errors(X, Xs)
+        self.raise_errors(X, Xs, y)

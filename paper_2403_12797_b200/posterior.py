@@ -3,12 +3,13 @@
 Pipeline of :func:`fagp_posterior` (posterior.py:267-318 in the reference), every stage a
 call into libfagp_b200.so on the current CUDA stream:
 
-    fagp_basis_eval(X), fagp_basis_eval(X*)    1-D eigenfunction tables      (mercer.py:276-281)
     fagp_eigenvalues                           lam, lam_floored, s           (mercer.py:350-353)
-    fagp_gram                                  [Phi|r]^T[Phi|r], fused        (posterior.py:168,233)
+    fagp_gram_x(X, y)                          eigenfunctions on chip         (mercer.py:276-281)
+                                               + Gram [K | t] on DMMA         (posterior.py:168,233)
     [torch.distributed all_reduce of the packed Gram when sharded]
-    fagp_factor                                A, Cholesky+jitter, w, V        (posterior.py:171-175,234-235)
-    fagp_predict                               mean, var, fused               (posterior.py:247,249-263)
+    fagp_factor                                A, Cholesky+jitter, w, op      (posterior.py:171-175,234-235)
+    fagp_predict_x(X*)                         eigenfunctions on chip         (posterior.py:247,249-263)
+                                               + mean and variance on DMMA
 
 ``method="literal"`` (the reference's cross-check route, posterior.py:236-244, 256-260) runs
 on the device too: see :mod:`literal`.
@@ -162,6 +163,19 @@ def gram_packed(basis, T, yd=None, mean_const=0.0, flag_ptr=None, stream=None):
     return packed
 
 
+def gram_x_packed(basis, Xd, yd=None, mean_const=0.0, flag_ptr=None, stream=None):
+    """fagp_gram_x: the same `gram` buffer straight from the points (eigenfunctions on chip)."""
+    L = _lib.lib()
+    s = _lib.stream_handle(stream)
+    N = int(Xd.shape[0])
+    packed = dev.empty((int(L.fagp_gram_len(basis.ref)),), device=Xd.device)
+    wsz = int(L.fagp_gram_x_workspace_size(N, basis.ref))
+    ws = dev.empty((max(1, -(-wsz // 8)),), device=Xd.device)
+    _lib.check(L.fagp_gram_x(_lib.ptr(Xd), N, basis.ref, _lib.ptr(yd), float(mean_const), _lib.ptr(packed),
+                             _lib.ptr(ws), wsz, flag_ptr, s), "gram_x")
+    return packed
+
+
 def factor_packed(basis, packed, noise_var, mean_const, N, keep_gram=False, stream=None):
     """fagp_factor: Cholesky with jitter, weights, predict operand.  Returns (Fit, status, pivot)."""
     L = _lib.lib()
@@ -230,6 +244,21 @@ def predict_device(f, Ts, want_var=True, flag_ptr=None, stream=None):
     return mean, var
 
 
+def predict_x_device(f, Xs, want_var=True, flag_ptr=None, stream=None):
+    """fagp_predict_x straight from the test points; returns device (mean, var|None)."""
+    L = _lib.lib()
+    s = _lib.stream_handle(stream)
+    Ns = int(Xs.shape[0])
+    mean = dev.empty((Ns,), device=Xs.device)
+    var = dev.empty((Ns,), device=Xs.device) if want_var else None
+    if Ns > 0:
+        wsz = int(L.fagp_predict_x_workspace_size(Ns, f.basis.ref))
+        ws = dev.empty((max(1, -(-wsz // 8)),), device=Xs.device)
+        _lib.check(L.fagp_predict_x(_lib.ptr(Xs), Ns, f.basis.ref, _lib.ptr(f.predict_op), f.noise_var, f.mean_const,
+                                    _lib.ptr(mean), _lib.ptr(var), flag_ptr, _lib.ptr(ws), wsz, s), "predict_x")
+    return mean, var
+
+
 def _covariance(f, Ts):
     """Full predictive covariance sigma2 * Z Z^T, Z = Phi* V^T (posterior.py:249-263)."""
     from .linalg import dgemm
@@ -281,8 +310,7 @@ def fit(train, model, backend=None, memory_cap=DEFAULT_MEMORY_CAP, delta2_varian
     basis = Basis(kernel, model.n_eigen, delta2_variant, device=X.device)
     flags = _Flags(X.device)
     s = _lib.stream_handle()
-    T = _stage_tables(basis, X, flags.ptr(0), s)
-    packed = gram_packed(basis, T, yd, model.mean_const, flags.ptr(0))
+    packed = gram_x_packed(basis, X, yd, model.mean_const, flags.ptr(0))
     if group is not None:
         from .distributed import all_reduce_sum
 
@@ -292,7 +320,7 @@ def fit(train, model, backend=None, memory_cap=DEFAULT_MEMORY_CAP, delta2_varian
     if fl[0] & _lib.FLAG_X_NONFINITE:
         raise ValueError("X must be finite")
     if fl[0] & _lib.FLAG_PHI_NONFINITE:
-        raise_nonfinite(T, X, basis)
+        raise_nonfinite(_stage_tables(basis, X, None, s), X, basis)
     if st != _lib.FAGP_OK:
         _raise_factor(st, piv, basis.m)
     _apply_fault(f)
@@ -303,14 +331,13 @@ def predict(f, Xstar, want_var=True, want_cov=False, return_device=False):
     """Posterior mean (and variance / covariance) at X* for a fit handle."""
     Xs = dev.points(Xstar, f.basis.p, "Xstar")
     flags = _Flags(Xs.device)
-    Ts = _stage_tables(f.basis, Xs, flags.ptr(1), _lib.stream_handle())
-    mean, var = predict_device(f, Ts, want_var=want_var, flag_ptr=flags.ptr(1))
-    cov = _covariance(f, Ts) if want_cov else None
+    mean, var = predict_x_device(f, Xs, want_var=want_var, flag_ptr=flags.ptr(1))
+    cov = _covariance(f, _stage_tables(f.basis, Xs, None, _lib.stream_handle())) if want_cov else None
     fl = flags.read()
     if fl[1] & _lib.FLAG_X_NONFINITE:
         raise ValueError("Xstar must be finite")
     if fl[1] & _lib.FLAG_PHI_NONFINITE:
-        raise_nonfinite(Ts, Xs, f.basis)
+        raise_nonfinite(_stage_tables(f.basis, Xs, None, _lib.stream_handle()), Xs, f.basis)
     if return_device:
         return PosteriorResult(mean=mean, cov=cov, var=var)
     return PosteriorResult(mean=dev.to_host(mean), cov=None if cov is None else dev.to_host(cov),
@@ -362,13 +389,13 @@ def fagp_posterior(train, Xstar, model, backend=None, want_cov=False, method="sc
     eng = PosteriorEngine(kernel, model.n_eigen, N, Ns, model.noise_var, model.mean_const, delta2_variant,
                           device=X.device, group=group, want_var=want_var)
     mean, var = eng.run(X, yd, Xs, fault_flip=_FAULT_FLIP_MEAN_SIGN, xs_ready=xs_ready)
-    eng.check(X, Xs)
+    eng.check(X, Xs, yd)
     cov = None
     if want_cov:
         f = Fit(basis=eng.basis, noise_var=eng.noise_var, mean_const=eng.mean_const, N=N, lam=eng.lam,
                 lam_floored=eng.lam_floored, sqrt_lam=eng.sqrt_lam, packed=eng.packed, L=eng.L, t=eng.t, w=eng.w,
                 predict_op=eng.predict_op, jitter=float(eng.jitter.value))
-        cov = _covariance(f, eng.Ts)
+        cov = _covariance(f, eng.table(Xs))
     return _result(mean, var, cov, return_device)
 
 
@@ -394,12 +421,12 @@ def fagp_posterior_from_eigensystems(es, es_star, y, model, backend=None, want_c
         mean, var, cov = literal_posterior(es.basis, es.table, es_star.table, yd, model.noise_var, model.mean_const,
                                            want_var=want_var, want_cov=want_cov, fault_flip=_FAULT_FLIP_MEAN_SIGN)
         return _result(mean, var, cov, return_device)
-    packed = gram_packed(es.basis, es.table, yd, model.mean_const)
+    packed = gram_x_packed(es.basis, es.X, yd, model.mean_const)
     f, st, piv = factor_packed(es.basis, packed, model.noise_var, model.mean_const, es.N)
     if st != _lib.FAGP_OK:
         _raise_factor(st, piv, es.basis.m)
     _apply_fault(f)
-    mean, var = predict_device(f, es_star.table, want_var=want_var)
+    mean, var = predict_x_device(f, es_star.X, want_var=want_var)
     cov = _covariance(f, es_star.table) if want_cov else None
     return _result(mean, var, cov, return_device)
 
@@ -419,7 +446,7 @@ class LambdaBarSolve:
         self.form = form
         self.noise_var = float(noise_var)
         self._es = es
-        packed = gram_packed(es.basis, es.table, None, 0.0)
+        packed = gram_x_packed(es.basis, es.X, None, 0.0)
         f, st, piv = factor_packed(es.basis, packed, noise_var, 0.0, es.N, keep_gram=True)
         self._fit = f
         self._gram = f.G

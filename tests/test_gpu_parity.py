@@ -254,3 +254,66 @@ def test_potrf_matches_lapack(m, impl, monkeypatch):
         _, info_ref = sla.lapack.dpotrf(Ai, lower=1)
         _, info = potrf(Ai)
         assert info == info_ref > 0
+
+
+# ---- the point-input (fused) entry points against the table path ----------------------
+@pytest.mark.parametrize("p,M,N", [(2, 10, 1), (2, 10, 63), (2, 10, 5000), (3, 10, 1), (3, 10, 64), (3, 10, 4097),
+                                   (3, 6, 777), (4, 4, 3001), (3, 10, 200_003)])
+def test_gram_x_matches_table_gram(p, M, N):
+    from paper_2403_12797_b200.posterior import gram_x_packed
+
+    rng = np.random.default_rng(1000 * p + M)
+    X = rng.uniform(-1, 1, (N, p))
+    y = np.cos(X).sum(1) + 0.05 * rng.standard_normal(N)
+    kernel = F.ArdKernelParams.isotropic(p, 1.0, 1.0)
+    basis = F.Basis(kernel, M)
+    Xd, yd = dev.to_device(X), dev.to_device(y)
+    ref = dev.to_host(gram_packed(basis, _stage_tables(basis, Xd, None, None), yd, 0.3))
+    got = dev.to_host(gram_x_packed(basis, Xd, yd, 0.3))
+    assert got.shape == ref.shape
+    assert scaled_err(got, ref) <= 1e-13, scaled_err(got, ref)
+    again = dev.to_host(gram_x_packed(basis, Xd, yd, 0.3))
+    assert np.array_equal(got, again)  # deterministic
+
+
+@pytest.mark.parametrize("p,M,Ns", [(2, 10, 1), (2, 10, 65), (3, 10, 1), (3, 10, 127), (3, 10, 100_001),
+                                    (3, 6, 999), (4, 4, 3001)])
+def test_predict_x_matches_table_predict(p, M, Ns):
+    from paper_2403_12797_b200.posterior import predict_x_device
+
+    rng = np.random.default_rng(7 * p + M)
+    N = 4000
+    X = rng.uniform(-1, 1, (N, p))
+    y = np.cos(X).sum(1) + 0.05 * rng.standard_normal(N)
+    Xs = rng.uniform(-1.2, 1.2, (Ns, p))
+    kernel = F.ArdKernelParams.isotropic(p, 1.0, 1.0)
+    basis = F.Basis(kernel, M)
+    Xd, yd, Xsd = dev.to_device(X), dev.to_device(y), dev.to_device(Xs)
+    packed = gram_packed(basis, _stage_tables(basis, Xd, None, None), yd, 0.1)
+    f, st, _ = factor_packed(basis, packed, 0.0025, 0.1, N)
+    assert st == 0
+    m_ref, v_ref = (dev.to_host(a) for a in predict_device_table(f, basis, Xsd))
+    m_got, v_got = (dev.to_host(a) for a in predict_x_device(f, Xsd))
+    assert rel_err(m_got, m_ref) <= 1e-11, rel_err(m_got, m_ref)
+    assert rel_err(v_got, v_ref) <= 1e-9, rel_err(v_got, v_ref)
+    m_only, none = predict_x_device(f, Xsd, want_var=False)
+    assert none is None and np.array_equal(dev.to_host(m_only), m_got)
+
+
+def predict_device_table(f, basis, Xsd):
+    from paper_2403_12797_b200.posterior import predict_device
+
+    return predict_device(f, _stage_tables(basis, Xsd, None, None))
+
+
+def test_fused_path_flags_nonfinite_points():
+    from paper_2403_12797_b200.posterior import gram_x_packed
+
+    X = np.random.default_rng(0).uniform(-1, 1, (500, 3))
+    X[123, 1] = np.nan
+    basis = F.Basis(F.ArdKernelParams.isotropic(3, 1.0, 1.0), 10)
+    flags = dev.zeros((1,), dtype="int32")
+    from paper_2403_12797_b200 import _lib
+
+    gram_x_packed(basis, dev.to_device(X), None, 0.0, flag_ptr=_lib.ptr(flags))
+    assert int(dev.to_host(flags)[0]) & _lib.FLAG_X_NONFINITE

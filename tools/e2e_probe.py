@@ -20,7 +20,7 @@ for rep in range(3):
     t0 = tick(); X = dev.to_device(Xp); y = dev.to_device(yp); Xd = dev.to_device(Xsp)
     t1 = tick(); eng = PosteriorEngine(kernel, M, N, N, 0.0025, 0.0, device=X.device)
     t2 = tick(); mean, var = eng.run(X, y, Xd)
-    t3 = tick(); eng.check(X, Xd)
+    t3 = tick(); eng.check(X, Xd, y)
     t4 = tick(); mh, vh = dev.to_host(mean), dev.to_host(var)
     t5 = tick(); r = F.fagp_posterior(T, Xsp, model, memory_cap=None)
     t6 = tick()
