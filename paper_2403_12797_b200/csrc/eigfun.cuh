@@ -64,3 +64,70 @@ __device__ __forceinline__ void eval_g_dim(double x, const BasisView& b, int d, 
 }
 
 }  // namespace fagp
+
+namespace fagp {
+
+// T independent (point, dimension) evaluations advanced in lockstep: the same operations in
+// the same order as eval_phi_dim / eval_g_dim for each point (bit-identical results), but T
+// independent recurrence chains per thread, so the FP64 latency of one chain hides behind
+// the others.  out_phi[t] / out_g[t] may be null (skip that section for point t).
+template <int T>
+__device__ __forceinline__ void eval_multi(const double (&x)[T], const int (&d)[T], const BasisView& b,
+                                           const double* c1, const double* c2, double* const (&out_phi)[T],
+                                           double* const (&out_g)[T], bool want_phi, bool want_g) {
+  const int M = b.M, L = modal_L(M);
+  double zr[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) zr[t] = __dmul_rn(b.rho_beta()[d[t]], x[t]);
+  if (want_phi) {
+    double env[T], h[T], hm1[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      env[t] = __dmul_rn(b.sqrt_beta()[d[t]], exp(__dmul_rn(__dmul_rn(b.neg_delta2()[d[t]], x[t]), x[t])));
+      hm1[t] = 1.0;
+      h[t] = __dmul_rn(zr[t], kSqrt2);
+      if (out_phi[t]) {
+        out_phi[t][0] = __dmul_rn(env[t], 1.0);
+        if (M > 1) out_phi[t][1] = __dmul_rn(env[t], h[t]);
+      }
+    }
+    for (int k = 1; k < M - 1; ++k) {
+      const double a1 = c1[k], a2 = c2[k];
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const double hn = __dsub_rn(__dmul_rn(__dmul_rn(zr[t], a1), h[t]), __dmul_rn(a2, hm1[t]));
+        if (out_phi[t]) out_phi[t][k + 1] = __dmul_rn(env[t], hn);
+        hm1[t] = h[t];
+        h[t] = hn;
+      }
+    }
+  }
+  if (want_g) {
+    double amp[T], yz[T], h[T], gm1[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const double sb = b.sqrt_beta()[d[t]];
+      amp[t] = __dmul_rn(__dmul_rn(sb, sb),
+                         exp(__dmul_rn(__dmul_rn(__dmul_rn(2.0, b.neg_delta2()[d[t]]), x[t]), x[t])));
+      yz[t] = __dmul_rn(zr[t], kSqrt2);
+      gm1[t] = 1.0;
+      h[t] = __dmul_rn(yz[t], kSqrt2);
+      if (out_g[t]) {
+        out_g[t][0] = amp[t];
+        if (L > 1) out_g[t][1] = __dmul_rn(amp[t], h[t]);
+      }
+    }
+    for (int k = 1; k < L - 1; ++k) {
+      const double a1 = c1[k], a2 = c2[k];
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const double hn = __dsub_rn(__dmul_rn(__dmul_rn(yz[t], a1), h[t]), __dmul_rn(a2, gm1[t]));
+        if (out_g[t]) out_g[t][k + 1] = __dmul_rn(amp[t], hn);
+        gm1[t] = h[t];
+        h[t] = hn;
+      }
+    }
+  }
+}
+
+}  // namespace fagp

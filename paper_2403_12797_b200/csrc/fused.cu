@@ -39,17 +39,18 @@ namespace fagp {
 namespace fused {
 
 // ---------------------------------------------------------------------------------------
-// Shared-memory row slab: [g_{d,k} (p L) | phi_{d,a} (p M) | r | 1.0 | 0.0 | pad], stride BW
-// with BW % 16 == 4 so 4 rows x 4 consecutive doubles hit 16 distinct bank pairs.
+// Shared-memory row slab: [g_{d,k} (p L) | phi_{d,a} (p M) | r phi_{p-1,a} (M) | r | 1.0 | 0.0 | pad],
+// stride BW with BW % 16 == 4 so 4 rows x 4 consecutive doubles hit 16 distinct bank pairs.
 struct RowLayout {
-  int goff, poff, roff, one, zero, bw;
+  int goff, poff, rpoff, roff, one, zero, bw;
 };
 __host__ __device__ inline RowLayout row_layout(int p, int M) {
   const int L = modal_L(M);
   RowLayout r;
   r.goff = 0;
   r.poff = p * L;
-  r.roff = p * L + p * M;
+  r.rpoff = p * L + p * M;
+  r.roff = r.rpoff + M;
   r.one = r.roff + 1;
   r.zero = r.roff + 2;
   int w = r.zero + 1;
@@ -60,48 +61,48 @@ __host__ __device__ inline RowLayout row_layout(int p, int M) {
 
 constexpr int kRows = 64;      // rows per block (16 DMMA k-steps of 4 rows)
 constexpr int kProdWarps = 2;  // producer warps per CTA
-constexpr int kMaxTasks = 4;   // (row, dim) tasks per producer thread: kRows * p / 64 <= 4
 constexpr int kMaxF = 4;       // factors per generated column (p <= 4 on the fused path)
 
-// Producer: rows [0, kRows) of `slab` <- basis of points row0 + i (i < nvalid; the rest zero).
-__device__ __forceinline__ void produce_rows(const double* __restrict__ X, const double* __restrict__ y, double c,
-                                             int64_t row0, int nvalid, const BasisView& b, const RowLayout& rl,
-                                             const double* c1, const double* c2, double* slab, int ptid,
-                                             bool want_phi, bool want_g, bool& bad_x) {
-  const int p = b.p, M = b.M, L = modal_L(M);
+// Producer (predict): rows [0, kRows) of `slab` <- basis of points row0 + i (i < nvalid; the
+// rest zero).  Each of the 64 producer threads owns P (row, dim) tasks and advances their
+// recurrences in lockstep (eval_multi): P independent FP64 chains per thread.
+template <int P>
+__device__ __forceinline__ void produce_rows(const double* __restrict__ X, int64_t row0, int nvalid,
+                                             const BasisView& b, const RowLayout& rl, const double* c1,
+                                             const double* c2, double* slab, int ptid, bool want_g, bool& bad_x) {
+  const int M = b.M, L = modal_L(M);
   constexpr int NTH = kProdWarps * 32;
-  const int tasks = kRows * p;
-  double xs[kMaxTasks];
+  constexpr int tasks = kRows * P;
+  double xs[P];
+  int ds[P];
+  double* op[P];
+  double* og[P];
 #pragma unroll
-  for (int i = 0; i < kMaxTasks; ++i) {  // all loads first: one HBM round trip per block
+  for (int i = 0; i < P; ++i) {  // all loads first: one HBM round trip per block
     const int t = ptid + i * NTH;
-    xs[i] = 0.0;
-    if (t < tasks) {
-      const int r = t / p;
-      if (r < nvalid) xs[i] = X[row0 * p + t];
-    }
+    const int r = t / P, d = t - r * P;
+    const bool in = t < tasks, valid = in && r < nvalid;
+    xs[i] = valid ? X[row0 * P + t] : 0.0;
+    ds[i] = in ? d : 0;
+    double* row = slab + (in ? r : 0) * rl.bw;
+    op[i] = valid ? row + rl.poff + d * M : nullptr;
+    og[i] = (valid && want_g) ? row + rl.goff + d * L : nullptr;
   }
 #pragma unroll
-  for (int i = 0; i < kMaxTasks; ++i) {
+  for (int i = 0; i < P; ++i) {
     const int t = ptid + i * NTH;
-    if (t < tasks) {
-      const int r = t / p, d = t - r * p;
+    const int r = t / P, d = t - r * P;
+    if (t < tasks && r < nvalid) {
+      bad_x |= not_finite(xs[i]);
+    } else if (t < tasks) {
       double* row = slab + r * rl.bw;
-      if (r < nvalid) {
-        bad_x |= not_finite(xs[i]);
-        if (want_phi) eval_phi_dim(xs[i], b, d, c1, c2, row + rl.poff + d * M);
-        if (want_g) eval_g_dim(xs[i], b, d, c1, c2, row + rl.goff + d * L);
-      } else {
-        if (want_phi)
-          for (int k = 0; k < M; ++k) row[rl.poff + d * M + k] = 0.0;
-        if (want_g)
-          for (int k = 0; k < L; ++k) row[rl.goff + d * L + k] = 0.0;
-      }
+      for (int k = 0; k < M; ++k) row[rl.poff + d * M + k] = 0.0;
+      for (int k = 0; k < L; ++k) row[rl.goff + d * L + k] = 0.0;
     }
   }
+  eval_multi<P>(xs, ds, b, c1, c2, op, og, true, want_g);
   for (int r = ptid; r < kRows; r += NTH) {
     double* row = slab + r * rl.bw;
-    row[rl.roff] = (y != nullptr && r < nvalid) ? __dsub_rn(y[row0 + r], c) : 0.0;  // r = y - c (posterior.py:229)
     row[rl.one] = 1.0;
     row[rl.zero] = 0.0;
   }
@@ -139,27 +140,30 @@ __device__ __forceinline__ double gather_prod(const double* row, const int (&off
 }
 
 // ---------------------------------------------------------------------------------------
-// Fused Gram
-// 16 warps = 4 per SM sub-partition: the most that still leaves each thread 128 registers
-// (every sub-partition owns a quarter of the register file)
-constexpr int kGramCW = 14;                                // consumer warps
-constexpr int kGramNT = (kGramCW + kProdWarps) * 32;       // 512 threads
-constexpr int kGramJobs = 5;                               // job slots per consumer warp
-constexpr int kNF = 3;                                     // n-fragments per job (<= 24 columns)
+// Fused Gram.  16 warps = 4 per SM sub-partition (each sub-partition owns a quarter of the
+// register file, so this is the most warps that keep 128 registers per thread) and no
+// dedicated producer: warp w evaluates the eigenfunctions of rows [4w, 4w + 4) of the NEXT
+// 64-row block at a point of its k-loop staggered against the other three warps of its
+// sub-partition, which keep the DMMA pipe busy meanwhile.
+// Output columns (first dimension slowest, A side = dims [0, p-1), B side = dim p-1):
+//   K: A = g-products (L^(p-1)) x B = g (L)          t: A = phi-products (M^(p-1)) x B = phi * r (M)
+// Warp wi of a row group owns K m-fragments wi + WG j (j < JK) and t m-fragments wi + WG j
+// (j < JT), each against every B fragment: all counts compile-time, no predication.
+constexpr int kGramW = 16;
+constexpr int kGramNT = kGramW * 32;
 
 struct GPlan {
   int p, M, L, LC;
-  int pA, pT;          // K: A = dims [0,pA) x B = dims [pA,p) (g, radix L); t: A = [0,pT) x B = [pT,p) * r (phi)
-  int KA, KB, TA, TB;  // section extents
-  int kmf, knf, tmf, tnf;
-  int G;               // row groups per CTA (each covers every job on k-steps kk = g mod G)
+  int KA, KB, TA, TB;  // KA = L^(p-1), KB = L, TA = M^(p-1), TB = M
+  int kmf, tmf;        // A-side m-fragments of K and t
+  int G, WG;           // row groups per CTA (k-steps kk = g mod G) and warps per group
+  int JK, JT;          // m-fragments per warp
   int64_t Klen, len;   // partial / output layout [K (KA*KB) | t (TA*TB = m)]
   int64_t rows_per_cta;
   int grid, nparts;
-  signed char job[kGramCW][kGramJobs];  // per warp-in-group: -1, K m-frag id, or kmf + t m-frag id
 };
 
-template <int FA, int FB>
+template <int FA, int NFK, int NFT, int JK, int JT>
 __global__ void __launch_bounds__(kGramNT, 1)
 fused_gram_kernel(const double* __restrict__ X, const double* __restrict__ y, double c, int64_t N, BasisView b,
                   const GPlan pl, double* __restrict__ ws, uint32_t* flags) {
@@ -169,6 +173,7 @@ fused_gram_kernel(const double* __restrict__ X, const double* __restrict__ y, do
   double* c2 = sm + pl.LC;
   double* slabs = sm + 2 * pl.LC;  // [2][kRows * bw]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int p = pl.p, M = pl.M, L = pl.L;
   for (int k = tid; k < pl.LC; k += kGramNT) {
     c1[k] = herm_c1(k);
     c2[k] = herm_c2(k);
@@ -176,94 +181,137 @@ fused_gram_kernel(const double* __restrict__ X, const double* __restrict__ y, do
   const int64_t r0 = int64_t(blockIdx.x) * pl.rows_per_cta;
   const int64_t r1 = tmin<int64_t>(N, r0 + pl.rows_per_cta);
   const int nblk = r1 > r0 ? int(ceil_div(r1 - r0, kRows)) : 0;
-  const bool producer = warp >= kGramCW;
-  const int ptid = tid - kGramCW * 32;
   bool bad_x = false;
-  __syncthreads();
-  if (producer && nblk > 0)
-    produce_rows(X, y, c, r0, int(tmin<int64_t>(kRows, r1 - r0)), b, rl, c1, c2, slabs, ptid, true, true, bad_x);
 
-  // consumer job setup (all warp-uniform except the lane's column)
-  const int WG = kGramCW / pl.G;
-  const int grp = warp / WG, wi = warp - grp * WG;
-  int jid[kGramJobs];
-  bool jK[kGramJobs];
-  int offA[kGramJobs][FA];
-  bool hasK = false, hasT = false;
-#pragma unroll
-  for (int j = 0; j < kGramJobs; ++j) {
-    jid[j] = producer ? -1 : int(pl.job[wi][j]);
-    jK[j] = jid[j] >= 0 && jid[j] < pl.kmf;
-    hasK |= jK[j];
-    hasT |= jid[j] >= pl.kmf;
-    if (jK[j])
-      col_offsets<FA>(jid[j] * 8 + (lane >> 2), pl.KA, rl.goff, 0, pl.pA, pl.L, -1, rl, offA[j]);
-    else
-      col_offsets<FA>((jid[j] - pl.kmf) * 8 + (lane >> 2), pl.TA, rl.poff, 0, pl.pT, pl.M, -1, rl, offA[j]);
-  }
-  int offBK[kNF][FB], offBT[kNF][FB];
-#pragma unroll
-  for (int nf = 0; nf < kNF; ++nf) {
-    col_offsets<FB>(nf * 8 + (lane >> 2), pl.KB, rl.goff, pl.pA, pl.p - pl.pA, pl.L, -1, rl, offBK[nf]);
-    col_offsets<FB>(nf * 8 + (lane >> 2), pl.TB, rl.poff, pl.pT, pl.p - pl.pT, pl.M, rl.roff, rl, offBT[nf]);
-  }
-  double acc[kGramJobs][kNF][2];
-#pragma unroll
-  for (int j = 0; j < kGramJobs; ++j)
-#pragma unroll
-    for (int nf = 0; nf < kNF; ++nf) acc[j][nf][0] = acc[j][nf][1] = 0.0;
-  __syncthreads();
-
-  for (int n = 0; n < nblk; ++n) {
-    const double* cur = slabs + (n & 1) * (kRows * rl.bw);
-    if (producer) {
-      if (n + 1 < nblk) {
-        const int64_t rn = r0 + int64_t(n + 1) * kRows;
-        produce_rows(X, y, c, rn, int(tmin<int64_t>(kRows, r1 - rn)), b, rl, c1, c2,
-                     slabs + ((n + 1) & 1) * (kRows * rl.bw), ptid, true, true, bad_x);
+  // production role (lanes < 8p): row 4 warp + lane / 2p, dimension (lane % 2p) / 2, section
+  // phi (even lanes) or g (odd lanes); the phi lane of the last dimension also writes r phi.
+  const bool plane = lane < 8 * p;
+  const int prow = 4 * warp + lane / (2 * p), pdim = (lane % (2 * p)) >> 1;
+  const bool psec_g = lane & 1;
+  auto load_x = [&](int64_t rb) -> double {
+    const int64_t r = rb + prow;
+    return (plane && r < r1) ? X[r * p + pdim] : 0.0;
+  };
+  auto produce = [&](double x, int64_t rb, double* slab) {
+    if (plane) {
+      double* row = slab + prow * rl.bw;
+      const bool valid = rb + prow < r1;
+      const double rr = (valid && y != nullptr) ? __dsub_rn(y[rb + prow], c) : 0.0;  // r = y - c (posterior.py:229)
+      if (valid) {
+        bad_x |= not_finite(x);
+        if (psec_g) {
+          eval_g_dim(x, b, pdim, c1, c2, row + rl.goff + pdim * L);
+        } else {
+          eval_phi_dim(x, b, pdim, c1, c2, row + rl.poff + pdim * M);
+          if (pdim == p - 1)
+            for (int k = 0; k < M; ++k) row[rl.rpoff + k] = __dmul_rn(rr, row[rl.poff + pdim * M + k]);
+        }
+      } else if (psec_g) {
+        for (int k = 0; k < L; ++k) row[rl.goff + pdim * L + k] = 0.0;
+      } else {
+        for (int k = 0; k < M; ++k) row[rl.poff + pdim * M + k] = 0.0;
+        if (pdim == p - 1)
+          for (int k = 0; k < M; ++k) row[rl.rpoff + k] = 0.0;
       }
-    } else {
-      for (int kk = grp; kk < kRows / 4; kk += pl.G) {
-        const double* row = cur + (kk * 4 + (lane & 3)) * rl.bw;
-        double bK[kNF], bT[kNF];
-#pragma unroll
-        for (int nf = 0; nf < kNF; ++nf) {
-          bK[nf] = (hasK && nf < pl.knf) ? gather_prod<FB>(row, offBK[nf]) : 0.0;
-          bT[nf] = (hasT && nf < pl.tnf) ? gather_prod<FB>(row, offBT[nf]) : 0.0;
-        }
-#pragma unroll
-        for (int j = 0; j < kGramJobs; ++j) {
-          if (jid[j] >= 0) {
-            const double a = gather_prod<FA>(row, offA[j]);
-            const int nfs = jK[j] ? pl.knf : pl.tnf;
-#pragma unroll
-            for (int nf = 0; nf < kNF; ++nf)
-              if (nf < nfs) dmma_8x8x4(acc[j][nf][0], acc[j][nf][1], a, jK[j] ? bK[nf] : bT[nf]);
-          }
-        }
+      if (pdim == 0 && !psec_g) {
+        row[rl.roff] = rr;
+        row[rl.one] = 1.0;
+        row[rl.zero] = 0.0;
       }
     }
+  };
+  __syncthreads();
+  if (nblk > 0) produce(load_x(r0), r0, slabs);
+  double xn = nblk > 1 ? load_x(r0 + kRows) : 0.0;
+
+  const int grp = warp / pl.WG, wi = warp - grp * pl.WG;
+  int offAK[JK][FA], offAT[JT][FA], offBK[NFK], offBT[NFT];
+#pragma unroll
+  for (int j = 0; j < JK; ++j)
+    col_offsets<FA>((wi + pl.WG * j) * 8 + (lane >> 2), pl.KA, rl.goff, 0, p - 1, L, -1, rl, offAK[j]);
+#pragma unroll
+  for (int j = 0; j < JT; ++j)
+    col_offsets<FA>((wi + pl.WG * j) * 8 + (lane >> 2), pl.TA, rl.poff, 0, p - 1, M, -1, rl, offAT[j]);
+#pragma unroll
+  for (int nf = 0; nf < NFK; ++nf) {
+    int o[1];
+    col_offsets<1>(nf * 8 + (lane >> 2), pl.KB, rl.goff, p - 1, 1, L, -1, rl, o);
+    offBK[nf] = o[0];
+  }
+#pragma unroll
+  for (int nf = 0; nf < NFT; ++nf) {
+    int o[1];
+    col_offsets<1>(nf * 8 + (lane >> 2), pl.TB, rl.rpoff, 0, 1, M, -1, rl, o);
+    offBT[nf] = o[0];
+  }
+  double accK[JK][NFK][2], accT[JT][NFT][2];
+#pragma unroll
+  for (int j = 0; j < JK; ++j)
+#pragma unroll
+    for (int nf = 0; nf < NFK; ++nf) accK[j][nf][0] = accK[j][nf][1] = 0.0;
+#pragma unroll
+  for (int j = 0; j < JT; ++j)
+#pragma unroll
+    for (int nf = 0; nf < NFT; ++nf) accT[j][nf][0] = accT[j][nf][1] = 0.0;
+  const int nloc = (kRows / 4 - grp + pl.G - 1) / pl.G;  // k-steps of this warp per block
+  const int sp = ((warp >> 2) & 3) * nloc / 4;           // staggered production point
+  __syncthreads();
+
+  auto kstep = [&](const double* cur, int i) {
+    const double* row = cur + ((grp + i * pl.G) * 4 + (lane & 3)) * rl.bw;
+    double bK[NFK], bT[NFT];
+#pragma unroll
+    for (int nf = 0; nf < NFK; ++nf) bK[nf] = row[offBK[nf]];
+#pragma unroll
+    for (int nf = 0; nf < NFT; ++nf) bT[nf] = row[offBT[nf]];
+#pragma unroll
+    for (int j = 0; j < JK; ++j) {
+      const double a = gather_prod<FA>(row, offAK[j]);
+#pragma unroll
+      for (int nf = 0; nf < NFK; ++nf) dmma_8x8x4(accK[j][nf][0], accK[j][nf][1], a, bK[nf]);
+    }
+#pragma unroll
+    for (int j = 0; j < JT; ++j) {
+      const double a = gather_prod<FA>(row, offAT[j]);
+#pragma unroll
+      for (int nf = 0; nf < NFT; ++nf) dmma_8x8x4(accT[j][nf][0], accT[j][nf][1], a, bT[nf]);
+    }
+  };
+  for (int n = 0; n < nblk; ++n) {
+    const double* cur = slabs + (n & 1) * (kRows * rl.bw);
+#pragma unroll 2
+    for (int i = 0; i < sp; ++i) kstep(cur, i);
+    if (n + 1 < nblk) {
+      produce(xn, r0 + int64_t(n + 1) * kRows, slabs + ((n + 1) & 1) * (kRows * rl.bw));
+      xn = n + 2 < nblk ? load_x(r0 + int64_t(n + 2) * kRows) : 0.0;
+    }
+#pragma unroll 2
+    for (int i = sp; i < nloc; ++i) kstep(cur, i);
     __syncthreads();
   }
 
-  if (!producer) {
-    double* out = ws + (int64_t(blockIdx.x) * pl.G + grp) * pl.len;
+  double* out = ws + (int64_t(blockIdx.x) * pl.G + grp) * pl.len;
 #pragma unroll
-    for (int j = 0; j < kGramJobs; ++j) {
-      if (jid[j] < 0) continue;
-      const int mrow = (jK[j] ? jid[j] : jid[j] - pl.kmf) * 8 + (lane >> 2);
+  for (int j = 0; j < JK; ++j) {
+    const int mrow = (wi + pl.WG * j) * 8 + (lane >> 2);
 #pragma unroll
-      for (int nf = 0; nf < kNF; ++nf)
+    for (int nf = 0; nf < NFK; ++nf)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int ncol = nf * 8 + 2 * (lane & 3) + e;
-          if (jK[j]) {
-            if (mrow < pl.KA && ncol < pl.KB && nf < pl.knf) out[int64_t(mrow) * pl.KB + ncol] = acc[j][nf][e];
-          } else {
-            if (mrow < pl.TA && ncol < pl.TB && nf < pl.tnf) out[pl.Klen + int64_t(mrow) * pl.TB + ncol] = acc[j][nf][e];
-          }
-        }
-    }
+      for (int e = 0; e < 2; ++e) {
+        const int ncol = nf * 8 + 2 * (lane & 3) + e;
+        if (mrow < pl.KA && ncol < pl.KB) out[int64_t(mrow) * pl.KB + ncol] = accK[j][nf][e];
+      }
+  }
+#pragma unroll
+  for (int j = 0; j < JT; ++j) {
+    const int mrow = (wi + pl.WG * j) * 8 + (lane >> 2);
+#pragma unroll
+    for (int nf = 0; nf < NFT; ++nf)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int ncol = nf * 8 + 2 * (lane & 3) + e;
+        if (mrow < pl.TA && ncol < pl.TB) out[pl.Klen + int64_t(mrow) * pl.TB + ncol] = accT[j][nf][e];
+      }
   }
   if (bad_x) raise_flag(flags, FAGP_FLAG_X_NONFINITE);
 }
@@ -287,85 +335,42 @@ static int64_t ipow(int64_t b, int e) {
   return r;
 }
 
-// Plan for N rows; ok = false when the shape needs the tiled table path.
+// (JK, JT) warp shapes compiled for the fused Gram
+constexpr int kGramShapes[][2] = {{1, 1}, {3, 1}, {4, 2}};
+
+// Plan for N rows; false when the shape needs the tiled table path.
 static bool make_gplan(int64_t N, int p, int M, GPlan& pl) {
   std::memset(&pl, 0, sizeof(pl));
-  if (!modal_on(p, M) || p > kMaxF) return false;
+  if (!modal_on(p, M) || p > kMaxF || M > 12) return false;
   pl.p = p;
   pl.M = M;
   pl.L = modal_L(M);
   pl.LC = (pl.L + 1) & ~1;
-  int64_t best = -1;
-  for (int pA = 1; pA < p; ++pA) {
-    const int64_t KA = ipow(pl.L, pA), KB = ipow(pl.L, p - pA);
-    if (ceil_div(KB, 8) > kNF || pA > kMaxF || p - pA > kMaxF) continue;
-    const int64_t cost = ceil_div(KA, 8) * ceil_div(KB, 8);
-    if (best < 0 || cost < best) {
-      best = cost;
-      pl.pA = pA;
-    }
-  }
-  if (best < 0) return false;
-  best = -1;
-  for (int pT = 1; pT < p; ++pT) {
-    const int64_t TA = ipow(M, pT), TB = ipow(M, p - pT);
-    if (ceil_div(TB, 8) > kNF || pT > kMaxF || p - pT + 1 > kMaxF) continue;
-    const int64_t cost = ceil_div(TA, 8) * ceil_div(TB, 8);
-    if (best < 0 || cost < best) {
-      best = cost;
-      pl.pT = pT;
-    }
-  }
-  if (best < 0) return false;
-  pl.KA = int(ipow(pl.L, pl.pA));
-  pl.KB = int(ipow(pl.L, p - pl.pA));
-  pl.TA = int(ipow(M, pl.pT));
-  pl.TB = int(ipow(M, p - pl.pT));
+  pl.KA = int(ipow(pl.L, p - 1));
+  pl.KB = pl.L;
+  pl.TA = int(ipow(M, p - 1));
+  pl.TB = M;
   pl.kmf = int(ceil_div(pl.KA, 8));
-  pl.knf = int(ceil_div(pl.KB, 8));
   pl.tmf = int(ceil_div(pl.TA, 8));
-  pl.tnf = int(ceil_div(pl.TB, 8));
-  // Row groups G (each group of kGramCW/G warps covers every job on k-steps kk = g mod G) and
-  // the job -> warp assignment (longest processing time first, cost = n-frags): choose the G
-  // with the smallest per-block critical path (ceil(16/G) k-steps x the busiest warp's DMMAs).
-  int bestG = -1;
-  double bestc = 0.0;
-  signed char bestjob[kGramCW][kGramJobs];
-  for (int G = 1; G <= kGramCW; ++G) {
-    if (kGramCW % G) continue;
-    const int WG = kGramCW / G;
-    signed char job[kGramCW][kGramJobs];
-    std::memset(job, -1, sizeof(job));
-    int load[kGramCW] = {0}, cnt[kGramCW] = {0};
-    bool fits = true;
-    for (int pass = 0; pass < 2 && fits; ++pass) {
-      const bool kpass = (pl.knf >= pl.tnf) ? pass == 0 : pass == 1;
-      const int nj = kpass ? pl.kmf : pl.tmf, cost = kpass ? pl.knf : pl.tnf;
-      for (int j = 0; j < nj && fits; ++j) {
-        int w = -1;
-        for (int q = 0; q < WG; ++q)
-          if (cnt[q] < kGramJobs && (w < 0 || load[q] < load[w])) w = q;
-        if (w < 0) {
-          fits = false;
-          break;
-        }
-        job[w][cnt[w]++] = static_cast<signed char>(kpass ? j : pl.kmf + j);
-        load[w] += cost;
+  const int NFK = int(ceil_div(pl.KB, 8)), NFT = int(ceil_div(pl.TB, 8));
+  // row groups and warp shape with the smallest per-block critical path:
+  // ceil(16 / G) k-steps x (JK NFK + JT NFT) DMMAs per warp
+  int best = -1;
+  for (int G = 1; G <= kGramW; G *= 2) {
+    const int WG = kGramW / G;
+    for (const auto& sh : kGramShapes) {
+      if (WG * sh[0] < pl.kmf || WG * sh[1] < pl.tmf) continue;
+      const int cost = ((kRows / 4 + G - 1) / G) * (sh[0] * NFK + sh[1] * NFT);
+      if (best < 0 || cost < best) {
+        best = cost;
+        pl.G = G;
+        pl.WG = WG;
+        pl.JK = sh[0];
+        pl.JT = sh[1];
       }
     }
-    if (!fits) continue;
-    int mx = 0;
-    for (int q = 0; q < WG; ++q) mx = tmax(mx, load[q]);
-    const double crit = double(mx) * double((kRows / 4 + G - 1) / G);
-    if (bestG < 0 || crit < bestc - 1e-9) {
-      bestG = G;
-      bestc = crit;
-      std::memcpy(bestjob, job, sizeof(job));
-    }
   }
-  if (bestG < 0) return false;
-  pl.G = bestG;
-  std::memcpy(pl.job, bestjob, sizeof(bestjob));
+  if (best < 0) return false;
   pl.Klen = int64_t(pl.KA) * pl.KB;
   pl.len = pl.Klen + int64_t(pl.TA) * pl.TB;
   const RowLayout rl = row_layout(p, M);
@@ -383,29 +388,28 @@ static size_t gram_smem(const GPlan& pl) {
   return (size_t(2) * pl.LC + size_t(2) * kRows * row_layout(pl.p, pl.M).bw) * sizeof(double);
 }
 
-template <int FA>
-static int launch_gram_fb(int FB, const double* X, const double* y, double c, int64_t N, const fagp_basis* b,
-                          const GPlan& pl, double* ws, uint32_t* flags, cudaStream_t s) {
+template <int FA, int NFK, int NFT>
+static int launch_gram_shape(const double* X, const double* y, double c, int64_t N, const fagp_basis* b,
+                             const GPlan& pl, double* ws, uint32_t* flags, cudaStream_t s) {
   const size_t smem = gram_smem(pl);
   auto go = [&](auto kern) -> int {
     FAGP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    const char* dbg = getenv("FAGP_DEBUG");
-    if (dbg && dbg[0] == '1') {
-      cudaFuncAttributes fa;
-      cudaFuncGetAttributes(&fa, kern);
-      fprintf(stderr, "[fagp] fused_gram: regs %d maxthreads %d static smem %zu dyn %zu local %zu grid %d block %d\n",
-              fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes, smem, fa.localSizeBytes, pl.grid, kGramNT);
-    }
     kern<<<pl.grid, kGramNT, smem, s>>>(X, y, c, N, view(b), pl, ws, flags);
     return FAGP_OK;
   };
-  switch (FB) {
-    case 1: return go(fused_gram_kernel<FA, 1>);
-    case 2: return go(fused_gram_kernel<FA, 2>);
-    case 3: return go(fused_gram_kernel<FA, 3>);
-    case 4: return go(fused_gram_kernel<FA, 4>);
-    default: return FAGP_EUNSUPPORTED;
-  }
+  if (pl.JK == 1 && pl.JT == 1) return go(fused_gram_kernel<FA, NFK, NFT, 1, 1>);
+  if (pl.JK == 3 && pl.JT == 1) return go(fused_gram_kernel<FA, NFK, NFT, 3, 1>);
+  if (pl.JK == 4 && pl.JT == 2) return go(fused_gram_kernel<FA, NFK, NFT, 4, 2>);
+  return FAGP_EUNSUPPORTED;
+}
+
+template <int FA>
+static int launch_gram_fa(const double* X, const double* y, double c, int64_t N, const fagp_basis* b,
+                          const GPlan& pl, double* ws, uint32_t* flags, cudaStream_t s) {
+  // (n-frags of K, n-frags of t) from M: L = 2M - 1 <= 8 NFK, M <= 8 NFT
+  if (pl.M <= 4) return launch_gram_shape<FA, 1, 1>(X, y, c, N, b, pl, ws, flags, s);
+  if (pl.M <= 8) return launch_gram_shape<FA, 2, 1>(X, y, c, N, b, pl, ws, flags, s);
+  return launch_gram_shape<FA, 3, 2>(X, y, c, N, b, pl, ws, flags, s);
 }
 
 bool gram_eligible(int64_t N, int p, int M) {
@@ -425,13 +429,11 @@ int gram(const double* X, const double* y, double c, int64_t N, const fagp_basis
   if (!make_gplan(N, b->p, b->M, pl)) return FAGP_EUNSUPPORTED;
   if (ws == nullptr || ws_bytes < size_t(pl.nparts) * size_t(pl.len) * sizeof(double)) return FAGP_EWORKSPACE;
   double* w = static_cast<double*>(ws);
-  const int FA = tmax(pl.pA, pl.pT), FB = tmax(b->p - pl.pA, b->p - pl.pT + 1);
   int rc;
-  switch (FA) {
-    case 1: rc = launch_gram_fb<1>(FB, X, y, c, N, b, pl, w, flags, s); break;
-    case 2: rc = launch_gram_fb<2>(FB, X, y, c, N, b, pl, w, flags, s); break;
-    case 3: rc = launch_gram_fb<3>(FB, X, y, c, N, b, pl, w, flags, s); break;
-    case 4: rc = launch_gram_fb<4>(FB, X, y, c, N, b, pl, w, flags, s); break;
+  switch (b->p - 1) {
+    case 1: rc = launch_gram_fa<1>(X, y, c, N, b, pl, w, flags, s); break;
+    case 2: rc = launch_gram_fa<2>(X, y, c, N, b, pl, w, flags, s); break;
+    case 3: rc = launch_gram_fa<3>(X, y, c, N, b, pl, w, flags, s); break;
     default: rc = FAGP_EUNSUPPORTED;
   }
   if (rc) return rc;
@@ -443,29 +445,33 @@ int gram(const double* X, const double* y, double c, int64_t N, const fagp_basis
 }
 
 // ---------------------------------------------------------------------------------------
-// Fused predict (variance + mean)
-constexpr int kPredCW = 8;                              // 4 row groups x 2 K-halves
-constexpr int kPredNT = (kPredCW + kProdWarps) * 32;    // 320 threads
+// Fused predict (variance + mean).  8 consumer warps = 2 row groups (32 rows = 4 m-fragments)
+// x 4 K-quarters, plus 2 producer warps.  The variance and mean epilogues are linear in the
+// GEMM outputs, so every warp applies them to its own K-quarter partial (g / phi products
+// gathered from the row slab, 4-lane shuffle reduction) and only one scalar per row and
+// quarter meets in shared memory; the quarters are summed in fixed order.
+constexpr int kPredCW = 8;
+constexpr int kPredNT = (kPredCW + kProdWarps) * 32;  // 320 threads
 
 struct VPlan {
   int p, M, L, LC;
-  int pN;                  // variance: N side dims [0,pN) (epilogue), K side [pN,p), radix L
-  int NR, KR, vnf, vks;    // N extent (<= 24), K extent, n-frags, k-steps of 4
-  int NM, KM, mnf, mks;    // mean: N side dim 0 (M), K side dims [1,p) (M^(p-1))
-  int64_t KP, NP;          // predict_op layout (modal::Plan): C'' [KP][NP], then w (m)
+  int pN;                // variance: N side dims [0,pN) (epilogue), K side [pN,p), radix L
+  int NR, KR, vks;       // N extent (<= 8 NFV), K extent, k-steps of 4
+  int NM, KM, mks;       // mean: N side dim 0 (M), K side dims [1,p) (M^(p-1))
+  int64_t KP, NP;        // predict_op layout (modal::Plan): C'' [KP][NP], then w (m)
   int64_t nblocks;
   int grid;
   size_t smem;
 };
 
-// byte-packed factor offsets of K column kappa (FK factors, 8 bits each; offsets < 256)
+// byte-packed factor offsets of K column kappa (F factors, 8 bits each; offsets < 256)
 template <int F>
 __device__ __forceinline__ void unpack_off(uint32_t v, int (&off)[F]) {
 #pragma unroll
   for (int f = 0; f < F; ++f) off[f] = int((v >> (8 * f)) & 0xffu);
 }
 
-template <int FK, int FE, int FKM>
+template <int FK, int FE, int FKM, int NFV, int NFM>
 __global__ void __launch_bounds__(kPredNT, 1)
 fused_predict_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView b, const VPlan pl,
                      const double* __restrict__ op, double sigma2, double c, double* __restrict__ mean,
@@ -475,10 +481,10 @@ fused_predict_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView b, con
   const bool want_var = var != nullptr;
   double* c1 = sm;
   double* c2 = sm + pl.LC;
-  double* Bv = c2 + pl.LC;                          // [vks][vnf][32]
-  double* Bm = Bv + pl.vks * pl.vnf * 32;           // [mks][mnf][32]
-  double* red = Bm + pl.mks * pl.mnf * 32;          // [4 mg][2 mf][kNF][2][2 (var, mean)][32]
-  double* slabs = red + 4 * 2 * kNF * 2 * 2 * 32;   // [2][kRows * bw]
+  double* Bv = c2 + pl.LC;                   // [vks][NFV][32]
+  double* Bm = Bv + pl.vks * NFV * 32;       // [mks][NFM][32]
+  double* red = Bm + pl.mks * NFM * 32;      // [4 quarters][kRows][2 (var, mean)]
+  double* slabs = red + 4 * kRows * 2;       // [2][kRows * bw]
   uint32_t* offV = reinterpret_cast<uint32_t*>(slabs + 2 * kRows * rl.bw);  // [vks * 4]
   uint32_t* offM = offV + pl.vks * 4;                                       // [mks * 4]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -489,13 +495,13 @@ fused_predict_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView b, con
   }
   // operands, fragment-major: B[ks][nf][lane] = Op[4 ks + (lane & 3)][8 nf + (lane >> 2)]
   if (want_var)
-    for (int i = tid; i < pl.vks * pl.vnf * 32; i += kPredNT) {
-      const int ln = i & 31, q = i >> 5, nf = q % pl.vnf, ks = q / pl.vnf;
+    for (int i = tid; i < pl.vks * NFV * 32; i += kPredNT) {
+      const int ln = i & 31, q = i >> 5, nf = q % NFV, ks = q / NFV;
       const int kap = 4 * ks + (ln & 3), nu = 8 * nf + (ln >> 2);
       Bv[i] = (kap < pl.KR && nu < pl.NR) ? op[int64_t(kap) * pl.NP + nu] : 0.0;
     }
-  for (int i = tid; i < pl.mks * pl.mnf * 32; i += kPredNT) {
-    const int ln = i & 31, q = i >> 5, nf = q % pl.mnf, ks = q / pl.mnf;
+  for (int i = tid; i < pl.mks * NFM * 32; i += kPredNT) {
+    const int ln = i & 31, q = i >> 5, nf = q % NFM, ks = q / NFM;
     const int kap = 4 * ks + (ln & 3), nu = 8 * nf + (ln >> 2);
     Bm[i] = (kap < pl.KM && nu < pl.NM) ? w[int64_t(nu) * pl.KM + kap] : 0.0;
   }
@@ -520,25 +526,27 @@ fused_predict_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView b, con
   const int ptid = tid - kPredCW * 32;
   bool bad_x = false, bad = false;
   __syncthreads();
-  const int64_t blk0 = blockIdx.x;
-  const int64_t stride = gridDim.x;
+  const int64_t blk0 = blockIdx.x, stride = gridDim.x;
   if (producer && blk0 < pl.nblocks) {
     const int64_t rr = blk0 * kRows;
-    produce_rows(Xs, nullptr, 0.0, rr, int(tmin<int64_t>(kRows, Ns - rr)), b, rl, c1, c2, slabs, ptid, true,
-                 want_var, bad_x);
+    produce_rows<FK + FE>(Xs, rr, int(tmin<int64_t>(kRows, Ns - rr)), b, rl, c1, c2, slabs, ptid, want_var, bad_x);
   }
-  // consumer roles
-  const int mg = warp & 3, kh = (warp >> 2) & 1;
-  const int vk0 = kh ? (pl.vks + 1) / 2 : 0, vk1 = kh ? pl.vks : (pl.vks + 1) / 2;
-  const int mk0 = kh ? (pl.mks + 1) / 2 : 0, mk1 = kh ? pl.mks : (pl.mks + 1) / 2;
+  // consumer roles: rows [32 mg, 32 mg + 32), K-quarter kq
+  const int mg = warp & 1, kq = (warp >> 1) & 3;
+  const int v0 = kq * pl.vks / 4, v1 = (kq + 1) * pl.vks / 4;
+  const int m0 = kq * pl.mks / 4, m1 = (kq + 1) * pl.mks / 4;
   // epilogue factor offsets: variance E[i, nu] = prod_{d < pN} g_d; mean phi_0[i, nu]
-  int offE[kNF][2][FE], offEm[kNF][2];
+  int offE[NFV][2][FE], offEm[NFM][2];
 #pragma unroll
-  for (int nf = 0; nf < kNF; ++nf)
+  for (int nf = 0; nf < NFV; ++nf)
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      col_offsets<FE>(nf * 8 + 2 * (lane & 3) + e, pl.NR, rl.goff, 0, pl.pN, pl.L, -1, rl, offE[nf][e]);
+#pragma unroll
+  for (int nf = 0; nf < NFM; ++nf)
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int nu = nf * 8 + 2 * (lane & 3) + e;
-      col_offsets<FE>(nu, pl.NR, rl.goff, 0, pl.pN, pl.L, -1, rl, offE[nf][e]);
       offEm[nf][e] = nu < pl.NM ? rl.poff + nu : rl.zero;
     }
   __syncthreads();
@@ -550,89 +558,91 @@ fused_predict_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView b, con
       const int64_t nb = blk + stride;
       if (nb < pl.nblocks) {
         const int64_t rr = nb * kRows;
-        produce_rows(Xs, nullptr, 0.0, rr, int(tmin<int64_t>(kRows, Ns - rr)), b, rl, c1, c2,
-                     slabs + ((it + 1) & 1) * (kRows * rl.bw), ptid, true, want_var, bad_x);
+        produce_rows<FK + FE>(Xs, rr, int(tmin<int64_t>(kRows, Ns - rr)), b, rl, c1, c2,
+                              slabs + ((it + 1) & 1) * (kRows * rl.bw), ptid, want_var, bad_x);
       }
     } else {
-      const double* rowA = cur + (mg * 16 + (lane >> 2)) * rl.bw;  // m-frag 0 row; m-frag 1 = +8 rows
-      const double* rowB = rowA + 8 * rl.bw;
-      double accV[2][kNF][2], accM[2][kNF][2];
+      const double* row0 = cur + (mg * 32 + (lane >> 2)) * rl.bw;  // m-fragment f: + 8 f rows
+      double accV[4][NFV][2], accM[4][NFM][2];
 #pragma unroll
-      for (int f = 0; f < 2; ++f)
+      for (int f = 0; f < 4; ++f) {
 #pragma unroll
-        for (int nf = 0; nf < kNF; ++nf) accV[f][nf][0] = accV[f][nf][1] = accM[f][nf][0] = accM[f][nf][1] = 0.0;
+        for (int nf = 0; nf < NFV; ++nf) accV[f][nf][0] = accV[f][nf][1] = 0.0;
+#pragma unroll
+        for (int nf = 0; nf < NFM; ++nf) accM[f][nf][0] = accM[f][nf][1] = 0.0;
+      }
       if (want_var) {
-        for (int ks = vk0; ks < vk1; ++ks) {
+#pragma unroll 2
+        for (int ks = v0; ks < v1; ++ks) {
           int off[FK];
           unpack_off<FK>(offV[4 * ks + (lane & 3)], off);
-          const double a0 = gather_prod<FK>(rowA, off), a1 = gather_prod<FK>(rowB, off);
-          const double* bp = Bv + (ks * pl.vnf) * 32 + lane;
+          double a[4], bb[NFV];
 #pragma unroll
-          for (int nf = 0; nf < kNF; ++nf)
-            if (nf < pl.vnf) {
-              const double bb = bp[nf * 32];
-              dmma_8x8x4(accV[0][nf][0], accV[0][nf][1], a0, bb);
-              dmma_8x8x4(accV[1][nf][0], accV[1][nf][1], a1, bb);
-            }
+          for (int f = 0; f < 4; ++f) a[f] = gather_prod<FK>(row0 + 8 * f * rl.bw, off);
+#pragma unroll
+          for (int nf = 0; nf < NFV; ++nf) bb[nf] = Bv[(ks * NFV + nf) * 32 + lane];
+#pragma unroll
+          for (int f = 0; f < 4; ++f)
+#pragma unroll
+            for (int nf = 0; nf < NFV; ++nf) dmma_8x8x4(accV[f][nf][0], accV[f][nf][1], a[f], bb[nf]);
         }
       }
-      for (int ks = mk0; ks < mk1; ++ks) {
+#pragma unroll 2
+      for (int ks = m0; ks < m1; ++ks) {
         int off[FKM];
         unpack_off<FKM>(offM[4 * ks + (lane & 3)], off);
-        const double a0 = gather_prod<FKM>(rowA, off), a1 = gather_prod<FKM>(rowB, off);
-        const double* bp = Bm + (ks * pl.mnf) * 32 + lane;
+        double a[4], bb[NFM];
 #pragma unroll
-        for (int nf = 0; nf < kNF; ++nf)
-          if (nf < pl.mnf) {
-            const double bb = bp[nf * 32];
-            dmma_8x8x4(accM[0][nf][0], accM[0][nf][1], a0, bb);
-            dmma_8x8x4(accM[1][nf][0], accM[1][nf][1], a1, bb);
-          }
+        for (int f = 0; f < 4; ++f) a[f] = gather_prod<FKM>(row0 + 8 * f * rl.bw, off);
+#pragma unroll
+        for (int nf = 0; nf < NFM; ++nf) bb[nf] = Bm[(ks * NFM + nf) * 32 + lane];
+#pragma unroll
+        for (int f = 0; f < 4; ++f)
+#pragma unroll
+          for (int nf = 0; nf < NFM; ++nf) dmma_8x8x4(accM[f][nf][0], accM[f][nf][1], a[f], bb[nf]);
       }
-      // split-K: the upper K-half hands its partial sums to the lower one (fixed order)
-      double* rp = red + mg * (2 * kNF * 2 * 2 * 32);
-      if (kh) {
+      // this quarter's epilogue contribution per row: sum_nu Y[i, nu] E[i, nu] (var),
+      // sum_nu Z[i, nu] phi_0[i, nu] (mean); the 4 lanes of a row hold disjoint columns
 #pragma unroll
-        for (int f = 0; f < 2; ++f)
+      for (int f = 0; f < 4; ++f) {
+        const double* row = row0 + 8 * f * rl.bw;
+        double vs = 0.0, ms = 0.0;
 #pragma unroll
-          for (int nf = 0; nf < kNF; ++nf)
+        for (int nf = 0; nf < NFV; ++nf)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              rp[(((f * kNF + nf) * 2 + e) * 2 + 0) * 32 + lane] = accV[f][nf][e];
-              rp[(((f * kNF + nf) * 2 + e) * 2 + 1) * 32 + lane] = accM[f][nf][e];
-            }
+          for (int e = 0; e < 2; ++e)
+            if (want_var) vs = fma(accV[f][nf][e], gather_prod<FE>(row, offE[nf][e]), vs);
+#pragma unroll
+        for (int nf = 0; nf < NFM; ++nf)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) ms = fma(accM[f][nf][e], row[offEm[nf][e]], ms);
+        vs += __shfl_xor_sync(0xffffffffu, vs, 1);
+        vs += __shfl_xor_sync(0xffffffffu, vs, 2);
+        ms += __shfl_xor_sync(0xffffffffu, ms, 1);
+        ms += __shfl_xor_sync(0xffffffffu, ms, 2);
+        if ((lane & 3) == 0) {
+          const int r = mg * 32 + 8 * f + (lane >> 2);
+          red[(kq * kRows + r) * 2 + 0] = vs;
+          red[(kq * kRows + r) * 2 + 1] = ms;
+        }
       }
       asm volatile("bar.sync 1, %0;\n" ::"n"(kPredCW * 32));
-      if (!kh) {
-        const int64_t rbase = blk * kRows + mg * 16 + (lane >> 2);
+      if (tid < kRows) {
+        const int64_t row_i = blk * kRows + tid;
+        if (row_i < Ns) {
+          double vs = red[tid * 2], ms = red[tid * 2 + 1];
 #pragma unroll
-        for (int f = 0; f < 2; ++f) {
-          const double* row = f ? rowB : rowA;
-          double vs = 0.0, ms = 0.0;
-#pragma unroll
-          for (int nf = 0; nf < kNF; ++nf)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const double yv = accV[f][nf][e] + rp[(((f * kNF + nf) * 2 + e) * 2 + 0) * 32 + lane];
-              const double zv = accM[f][nf][e] + rp[(((f * kNF + nf) * 2 + e) * 2 + 1) * 32 + lane];
-              if (nf < pl.vnf && want_var) vs = fma(yv, gather_prod<FE>(row, offE[nf][e]), vs);
-              if (nf < pl.mnf) ms = fma(zv, row[offEm[nf][e]], ms);
-            }
-          // the 4 lanes of a row hold disjoint columns: fixed-order xor reduction
-          vs += __shfl_xor_sync(0xffffffffu, vs, 1);
-          vs += __shfl_xor_sync(0xffffffffu, vs, 2);
-          ms += __shfl_xor_sync(0xffffffffu, ms, 1);
-          ms += __shfl_xor_sync(0xffffffffu, ms, 2);
-          const int64_t row_i = rbase + 8 * f;
-          if ((lane & 3) == 0 && row_i < Ns) {
-            const double mm = c + ms;  // posterior.py:247
-            mean[row_i] = mm;
-            bad |= not_finite(mm);
-            if (want_var) {
-              const double vv = sigma2 * vs;
-              var[row_i] = vv;
-              bad |= not_finite(vv);
-            }
+          for (int q = 1; q < 4; ++q) {
+            vs += red[(q * kRows + tid) * 2];
+            ms += red[(q * kRows + tid) * 2 + 1];
+          }
+          const double mm = c + ms;  // posterior.py:247
+          mean[row_i] = mm;
+          bad |= not_finite(mm);
+          if (want_var) {
+            const double vv = sigma2 * vs;
+            var[row_i] = vv;
+            bad |= not_finite(vv);
           }
         }
       }
@@ -645,7 +655,7 @@ fused_predict_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView b, con
 
 static bool make_vplan(int64_t Ns, int p, int M, VPlan& pl) {
   std::memset(&pl, 0, sizeof(pl));
-  if (!modal_on(p, M) || p > kMaxF || M > 24) return false;
+  if (!modal_on(p, M) || p > kMaxF || M > 12) return false;
   const modal::Plan mp = modal::make_plan(0, p, M);
   pl.p = p;
   pl.M = M;
@@ -656,17 +666,17 @@ static bool make_vplan(int64_t Ns, int p, int M, VPlan& pl) {
   pl.KR = int(mp.KR);
   pl.KP = mp.KP;
   pl.NP = mp.NP;
-  if (pl.NR > 8 * kNF || p - pl.pN > kMaxF || pl.pN > 2) return false;
-  pl.vnf = int(ceil_div(pl.NR, 8));
+  const int NFV = M <= 4 ? 1 : M <= 8 ? 2 : 3;
+  if (pl.NR > 8 * NFV || p - pl.pN > kMaxF - 1 || pl.pN > 2 || (pl.pN == 2 && M > 4)) return false;
   pl.vks = int(ceil_div(pl.KR, 4));
   pl.NM = M;
   pl.KM = int(ipow(M, p - 1));
-  pl.mnf = int(ceil_div(pl.NM, 8));
   pl.mks = int(ceil_div(pl.KM, 4));
+  const int NFM = M <= 8 ? 1 : 2;
   const RowLayout rl = row_layout(p, M);
   if (rl.bw > 256) return false;  // byte-packed offsets
-  pl.smem = (size_t(2) * pl.LC + size_t(pl.vks) * pl.vnf * 32 + size_t(pl.mks) * pl.mnf * 32 +
-             size_t(4) * 2 * kNF * 2 * 2 * 32 + size_t(2) * kRows * rl.bw) * sizeof(double) +
+  pl.smem = (size_t(2) * pl.LC + size_t(pl.vks) * NFV * 32 + size_t(pl.mks) * NFM * 32 + size_t(4) * kRows * 2 +
+             size_t(2) * kRows * rl.bw) * sizeof(double) +
             size_t(pl.vks + pl.mks) * 4 * sizeof(uint32_t);
   if (pl.smem > 225 * 1024) return false;
   pl.nblocks = ceil_div(tmax<int64_t>(Ns, 0), kRows);
@@ -674,24 +684,25 @@ static bool make_vplan(int64_t Ns, int p, int M, VPlan& pl) {
   return true;
 }
 
+template <int FK, int FE, int NFV, int NFM>
+static int launch_pred(const double* Xs, int64_t Ns, const fagp_basis* b, const VPlan& pl, const double* op,
+                       double sigma2, double c, double* mean, double* var, uint32_t* flags, cudaStream_t s) {
+  auto kern = fused_predict_kernel<FK, FE, FK + FE - 1, NFV, NFM>;
+  FAGP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem)));
+  kern<<<pl.grid, kPredNT, pl.smem, s>>>(Xs, Ns, view(b), pl, op, sigma2, c, mean, var, flags);
+  return FAGP_OK;
+}
+
 template <int FK>
-static int launch_pred_fe(int FE, const double* Xs, int64_t Ns, const fagp_basis* b, const VPlan& pl, const double* op,
+static int launch_pred_fk(const double* Xs, int64_t Ns, const fagp_basis* b, const VPlan& pl, const double* op,
                           double sigma2, double c, double* mean, double* var, uint32_t* flags, cudaStream_t s) {
-  auto go = [&](auto kern) -> int {
-    FAGP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem)));
-    kern<<<pl.grid, kPredNT, pl.smem, s>>>(Xs, Ns, view(b), pl, op, sigma2, c, mean, var, flags);
-    return FAGP_OK;
-  };
-  // FKM = p - 1 = FK + FE - 1
-  switch (FE) {
-    case 1:
-      return go(fused_predict_kernel<FK, 1, FK>);
-    case 2:
-      if constexpr (FK + 1 <= kMaxF) return go(fused_predict_kernel<FK, 2, FK + 1>);
-      return FAGP_EUNSUPPORTED;
-    default:
-      return FAGP_EUNSUPPORTED;
+  if (pl.pN == 2) {
+    if constexpr (FK + 1 <= kMaxF - 1) return launch_pred<FK, 2, 1, 1>(Xs, Ns, b, pl, op, sigma2, c, mean, var, flags, s);
+    return FAGP_EUNSUPPORTED;
   }
+  if (pl.M <= 4) return launch_pred<FK, 1, 1, 1>(Xs, Ns, b, pl, op, sigma2, c, mean, var, flags, s);
+  if (pl.M <= 8) return launch_pred<FK, 1, 2, 1>(Xs, Ns, b, pl, op, sigma2, c, mean, var, flags, s);
+  return launch_pred<FK, 1, 3, 2>(Xs, Ns, b, pl, op, sigma2, c, mean, var, flags, s);
 }
 
 bool predict_eligible(int p, int M) {
@@ -704,12 +715,11 @@ int predict(const double* Xs, int64_t Ns, const fagp_basis* b, const double* op,
   VPlan pl;
   if (!make_vplan(Ns, b->p, b->M, pl)) return FAGP_EUNSUPPORTED;
   if (Ns == 0) return FAGP_OK;
-  const int FK = b->p - pl.pN, FE = pl.pN;
   int rc;
-  switch (FK) {
-    case 1: rc = launch_pred_fe<1>(FE, Xs, Ns, b, pl, op, sigma2, c, mean, var, flags, s); break;
-    case 2: rc = launch_pred_fe<2>(FE, Xs, Ns, b, pl, op, sigma2, c, mean, var, flags, s); break;
-    case 3: rc = launch_pred_fe<3>(FE, Xs, Ns, b, pl, op, sigma2, c, mean, var, flags, s); break;
+  switch (b->p - pl.pN) {
+    case 1: rc = launch_pred_fk<1>(Xs, Ns, b, pl, op, sigma2, c, mean, var, flags, s); break;
+    case 2: rc = launch_pred_fk<2>(Xs, Ns, b, pl, op, sigma2, c, mean, var, flags, s); break;
+    case 3: rc = launch_pred_fk<3>(Xs, Ns, b, pl, op, sigma2, c, mean, var, flags, s); break;
     default: rc = FAGP_EUNSUPPORTED;
   }
   if (rc) return rc;
