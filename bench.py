@@ -27,7 +27,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -87,51 +86,71 @@ def launches_per_step(m, pair, p=1, fused=False):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 100 ms during the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled through NVML every ~2 ms while the
+    timed region runs (the region is only a few ms long, too short for `nvidia-smi -lms`),
+    plus one sample when it starts and one when it ends."""
 
-    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.sw_power_cap", "clocks_event_reasons.hw_slowdown",
-              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown"]
+    REASONS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+               "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80}
 
-    def __init__(self, index):
+    def __init__(self, index, period_s=0.002):
         self.index = index
+        self.period = period_s
         self.rows = []
-        self.proc = None
+        self.handle = None
+        self._stop = threading.Event()
+
+    def _sample(self):
+        import pynvml
+
+        sm = pynvml.nvmlDeviceGetClockInfo(self.handle, pynvml.NVML_CLOCK_SM)
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM)
+        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+        self.rows.append((sm, mx, rs))
+
+    def _loop(self):
+        while not self._stop.wait(self.period):
+            try:
+                self._sample()
+            except Exception:  # noqa: BLE001 - sampling must never break the bench
+                return
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits", "-lms",
-                 "100", "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            cuda_index = self.index
+            visible = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if visible:
+                ids = [v.strip() for v in visible.split(",")]
+                if cuda_index < len(ids) and ids[cuda_index].isdigit():
+                    cuda_index = int(ids[cuda_index])
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(cuda_index)
+            self._sample()
+            self.thread = threading.Thread(target=self._loop, daemon=True)
             self.thread.start()
-        except (OSError, ValueError):
-            self.proc = None
+        except Exception:  # noqa: BLE001
+            self.handle = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == len(self.FIELDS):
-                self.rows.append(parts)
-
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        if self.handle is not None:
+            self._stop.set()
             self.thread.join(timeout=2)
+            try:
+                self._sample()
+            except Exception:  # noqa: BLE001
+                pass
 
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        sm = [r[0] for r in self.rows]
+        mx = [r[1] for r in self.rows]
+        reasons = sorted({name for r in self.rows for name, bit in self.REASONS.items() if r[2] & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": reasons,
+                "samples": len(self.rows), "source": "NVML, every 2 ms during the timed steps"}
 
 
 def fp64_peak():
@@ -358,6 +377,10 @@ def main():
         for _ in range(max(2, args.warmup)):  # warm-up (2+: the pinned result buffers of call k-1 are
             fagp_posterior(Train, Xsp, model, memory_cap=None, group=group)  # still alive in call k)
         times = []
+        import gc
+
+        gc.collect()
+        gc.disable()  # as timeit does: no cyclic-GC pause inside the timed calls
         for k in range(args.steps):
             flush.fill_(float(k))
             barrier()
@@ -367,6 +390,7 @@ def main():
             torch.cuda.synchronize()
             times.append(time.perf_counter() - t0)
             assert r.mean.shape == (ns_loc,) and r.var.shape == (ns_loc,)
+        gc.enable()
         t = statistics.mean(times)
         log("e2e step ms:", " ".join(f"{1e3 * x:.2f}" for x in times))
         if world > 1:

@@ -155,6 +155,20 @@ size_t fagp_gram_x_workspace_size(int64_t N, const fagp_basis* basis);
 int fagp_gram_x(const double* X, int64_t N, const fagp_basis* basis, const double* y, double mean_const,
                 double* gram, void* workspace, size_t workspace_bytes, uint32_t* flags, void* stream);
 
+/* The same call split into fagp_gram_x_chunks(N, basis) launches so a host pipeline can
+ * overlap the upload of the rows with the contraction: every CTA owns a contiguous row range
+ * cut into that many sub-ranges, chunk k contracts sub-range k of every CTA (all SMs busy),
+ * and fagp_gram_x_upload_chunk(k) is the matching H2D copy (HOST X_host / y_host, pinned for
+ * an asynchronous copy; one 2-D cudaMemcpy per array).  Chunks are issued in order on one
+ * stream; the last one writes `gram`.  Bitwise identical to fagp_gram_x (the same per
+ * (CTA, sub-range) partials summed in the same fixed order).  Table-path shapes: 1 chunk. */
+int32_t fagp_gram_x_chunks(int64_t N, const fagp_basis* basis);
+int fagp_gram_x_upload_chunk(const double* X_host, const double* y_host, int64_t N, const fagp_basis* basis,
+                             int32_t k, double* X, double* y, void* stream);
+int fagp_gram_x_chunk(const double* X, int64_t N, const fagp_basis* basis, const double* y, double mean_const,
+                      int32_t k, double* gram, void* workspace, size_t workspace_bytes, uint32_t* flags,
+                      void* stream);
+
 /* Expand a `gram` buffer into the full symmetric G (m x m, nullable) and t (m, nullable).
  * The modal form needs fagp_gram_unpack_workspace_size(basis) bytes of workspace for G. */
 size_t fagp_gram_unpack_workspace_size(const fagp_basis* basis);

@@ -124,3 +124,41 @@ def points(X, p, name):
         raise ValueError(f"{name} has {Xh.shape[1]} columns, expected p={p}")
     # finiteness is checked on the device (FAGP_FLAG_X_NONFINITE from fagp_basis_eval)
     return to_device(Xh)
+
+
+def is_cuda(a):
+    torch = _torch()
+    return isinstance(a, torch.Tensor) and a.is_cuda
+
+
+def host_points(X, p, name):
+    """Validate an (N, p) HOST point set like :func:`points` without uploading it; returns a
+    contiguous float64 numpy array or CPU tensor (pinned tensors stay pinned)."""
+    torch = _torch()
+    if isinstance(X, torch.Tensor):
+        Xt = X.detach()
+        if Xt.dim() == 1:
+            Xt = Xt.reshape(1, -1) if Xt.numel() else Xt.reshape(0, p)
+        if Xt.dim() != 2 or Xt.shape[1] != p:
+            raise ValueError(f"{name} has {Xt.shape[-1]} columns, expected p={p}")
+        if Xt.dtype != torch.float64 or not Xt.is_contiguous():
+            Xt = Xt.to(torch.float64).contiguous()
+        return Xt
+    Xh = np.atleast_2d(np.asarray(X, dtype=float))
+    if Xh.shape[1] != p:
+        raise ValueError(f"{name} has {Xh.shape[1]} columns, expected p={p}")
+    return np.ascontiguousarray(Xh)
+
+
+def host_vector(y, N, name="y"):
+    """Validate a HOST (N,) vector without uploading it."""
+    torch = _torch()
+    if isinstance(y, torch.Tensor):
+        yt = y.detach()
+        if tuple(yt.shape) != (N,):
+            raise ValueError(f"{name} has shape {tuple(yt.shape)}, expected ({N},)")
+        return yt.to(torch.float64).contiguous() if yt.dtype != torch.float64 or not yt.is_contiguous() else yt
+    yh = np.asarray(y, dtype=float)
+    if yh.shape != (N,):
+        raise ValueError(f"{name} has shape {yh.shape}, expected ({N},)")
+    return np.ascontiguousarray(yh)

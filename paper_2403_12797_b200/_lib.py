@@ -72,6 +72,9 @@ SIGNATURES = {
     "fagp_gram": (ctypes.c_int, [_P, _I64, _BASIS, _P, _P, _SZ, _P, _P]),
     "fagp_gram_x_workspace_size": (_SZ, [_I64, _BASIS]),
     "fagp_gram_x": (ctypes.c_int, [_P, _I64, _BASIS, _P, _D, _P, _P, _SZ, _P, _P]),
+    "fagp_gram_x_chunks": (_I32, [_I64, _BASIS]),
+    "fagp_gram_x_upload_chunk": (ctypes.c_int, [_P, _P, _I64, _BASIS, _I32, _P, _P, _P]),
+    "fagp_gram_x_chunk": (ctypes.c_int, [_P, _I64, _BASIS, _P, _D, _I32, _P, _P, _SZ, _P, _P]),
     "fagp_predict_x_workspace_size": (_SZ, [_I64, _BASIS]),
     "fagp_predict_x": (ctypes.c_int, [_P, _I64, _BASIS, _P, _D, _D, _P, _P, _P, _P, _SZ, _P]),
     "fagp_factor_workspace_size": (_SZ, [_I64]),

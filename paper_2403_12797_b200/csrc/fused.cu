@@ -158,15 +158,17 @@ struct GPlan {
   int kmf, tmf;        // A-side m-fragments of K and t
   int G, WG;           // row groups per CTA (k-steps kk = g mod G) and warps per group
   int JK, JT;          // m-fragments per warp
-  int64_t Klen, len;   // partial / output layout [K (KA*KB) | t (TA*TB = m)]
-  int64_t rows_per_cta;
-  int grid, nparts;
+  int64_t Klen, len;   // output layout [K (KA*KB) | t (TA*TB = m)]
+  int64_t plen;        // one partial: (kmf NFK + tmf NFT) fragments of 64 doubles
+  int64_t rows_per_cta;  // multiple of kRows
+  int S;                 // sub-ranges per CTA = chunks a host pipeline may launch separately
+  int grid, nparts;      // nparts = grid * S * G partials
 };
 
 template <int FA, int NFK, int NFT, int JK, int JT>
 __global__ void __launch_bounds__(kGramNT, 1)
 fused_gram_kernel(const double* __restrict__ X, const double* __restrict__ y, double c, int64_t N, BasisView b,
-                  const GPlan pl, double* __restrict__ ws, uint32_t* flags) {
+                  const GPlan pl, int k0, int k1, double* __restrict__ ws, uint32_t* flags) {
   extern __shared__ double sm[];
   const RowLayout rl = row_layout(pl.p, pl.M);
   double* c1 = sm;
@@ -178,9 +180,16 @@ fused_gram_kernel(const double* __restrict__ X, const double* __restrict__ y, do
     c1[k] = herm_c1(k);
     c2[k] = herm_c2(k);
   }
-  const int64_t r0 = int64_t(blockIdx.x) * pl.rows_per_cta;
-  const int64_t r1 = tmin<int64_t>(N, r0 + pl.rows_per_cta);
-  const int nblk = r1 > r0 ? int(ceil_div(r1 - r0, kRows)) : 0;
+  // CTA rows [cta rpc, (cta + 1) rpc) = blocks [0, bpc) of kRows rows, cut into pl.S sub-ranges
+  // (sub-range k = blocks [k bpc / S, (k + 1) bpc / S)); this launch covers sub-ranges [k0, k1)
+  // and writes one partial per (CTA, sub-range, row group)
+  const int cta = int(blockIdx.x);
+  const int bpc = int(pl.rows_per_cta / kRows);
+  auto sb = [&](int k) { return int(int64_t(k) * bpc / pl.S); };
+  const int g0 = sb(k0);
+  const int nblk = sb(k1) - g0;
+  auto blk_base = [&](int j) -> int64_t { return int64_t(cta) * pl.rows_per_cta + int64_t(g0 + j) * kRows; };
+  auto blk_end = [&](int j) -> int64_t { return tmin<int64_t>(N, blk_base(j) + kRows); };
   bool bad_x = false;
 
   // production role (lanes < 8p): row 4 warp + lane / 2p, dimension (lane % 2p) / 2, section
@@ -188,14 +197,15 @@ fused_gram_kernel(const double* __restrict__ X, const double* __restrict__ y, do
   const bool plane = lane < 8 * p;
   const int prow = 4 * warp + lane / (2 * p), pdim = (lane % (2 * p)) >> 1;
   const bool psec_g = lane & 1;
-  auto load_x = [&](int64_t rb) -> double {
-    const int64_t r = rb + prow;
-    return (plane && r < r1) ? X[r * p + pdim] : 0.0;
+  auto load_x = [&](int j) -> double {
+    const int64_t r = blk_base(j) + prow;
+    return (plane && r < blk_end(j)) ? X[r * p + pdim] : 0.0;
   };
-  auto produce = [&](double x, int64_t rb, double* slab) {
+  auto produce = [&](double x, int j, double* slab) {
     if (plane) {
       double* row = slab + prow * rl.bw;
-      const bool valid = rb + prow < r1;
+      const int64_t rb = blk_base(j);
+      const bool valid = rb + prow < blk_end(j);
       const double rr = (valid && y != nullptr) ? __dsub_rn(y[rb + prow], c) : 0.0;  // r = y - c (posterior.py:229)
       if (valid) {
         bad_x |= not_finite(x);
@@ -221,8 +231,8 @@ fused_gram_kernel(const double* __restrict__ X, const double* __restrict__ y, do
     }
   };
   __syncthreads();
-  if (nblk > 0) produce(load_x(r0), r0, slabs);
-  double xn = nblk > 1 ? load_x(r0 + kRows) : 0.0;
+  if (nblk > 0) produce(load_x(0), 0, slabs);
+  double xn = nblk > 1 ? load_x(1) : 0.0;
 
   const int grp = warp / pl.WG, wi = warp - grp * pl.WG;
   int offAK[JK][FA], offAT[JT][FA], offBK[NFK], offBT[NFT];
@@ -257,72 +267,116 @@ fused_gram_kernel(const double* __restrict__ X, const double* __restrict__ y, do
   const int sp = ((warp >> 2) & 3) * nloc / 4;           // staggered production point
   __syncthreads();
 
-  auto kstep = [&](const double* cur, int i) {
+  // one k-step = 4 rows: operands (B: K g-values, t r*phi-values; A: products over the first p-1
+  // dims) then the DMMAs.  kloop software-pipelines: operands of step i + 1 are formed in program
+  // order before the DMMAs of step i.
+  struct Ops {
+    double bK[NFK], bT[NFT], aK[JK], aT[JT];
+  };
+  auto load_ops = [&](const double* cur, int i, Ops& o) {
     const double* row = cur + ((grp + i * pl.G) * 4 + (lane & 3)) * rl.bw;
-    double bK[NFK], bT[NFT];
 #pragma unroll
-    for (int nf = 0; nf < NFK; ++nf) bK[nf] = row[offBK[nf]];
+    for (int nf = 0; nf < NFK; ++nf) o.bK[nf] = row[offBK[nf]];
 #pragma unroll
-    for (int nf = 0; nf < NFT; ++nf) bT[nf] = row[offBT[nf]];
+    for (int nf = 0; nf < NFT; ++nf) o.bT[nf] = row[offBT[nf]];
+#pragma unroll
+    for (int j = 0; j < JK; ++j) o.aK[j] = gather_prod<FA>(row, offAK[j]);
+#pragma unroll
+    for (int j = 0; j < JT; ++j) o.aT[j] = gather_prod<FA>(row, offAT[j]);
+  };
+  auto mma_ops = [&](const Ops& o) {
+#pragma unroll
+    for (int j = 0; j < JK; ++j)
+#pragma unroll
+      for (int nf = 0; nf < NFK; ++nf) dmma_8x8x4(accK[j][nf][0], accK[j][nf][1], o.aK[j], o.bK[nf]);
+#pragma unroll
+    for (int j = 0; j < JT; ++j)
+#pragma unroll
+      for (int nf = 0; nf < NFT; ++nf) dmma_8x8x4(accT[j][nf][0], accT[j][nf][1], o.aT[j], o.bT[nf]);
+  };
+  auto kloop = [&](const double* cur, int i0, int i1) {
+    if (i0 >= i1) return;
+    Ops o;
+    load_ops(cur, i0, o);
+    for (int i = i0; i < i1; ++i) {
+      Ops on;
+      load_ops(cur, i + 1 < i1 ? i + 1 : i, on);
+      mma_ops(o);
+      o = on;
+    }
+  };
+  // partial of sub-range k in fragment-major order (coalesced: one 256 B store per fragment
+  // half), then restart the accumulators; partial_sum_kernel maps it back to [K | t]
+  auto flush = [&](int k) {
+    double* out = ws + ((int64_t(cta) * pl.S + k) * pl.G + grp) * pl.plen;
 #pragma unroll
     for (int j = 0; j < JK; ++j) {
-      const double a = gather_prod<FA>(row, offAK[j]);
+      const int mf = wi + pl.WG * j;
 #pragma unroll
-      for (int nf = 0; nf < NFK; ++nf) dmma_8x8x4(accK[j][nf][0], accK[j][nf][1], a, bK[nf]);
+      for (int nf = 0; nf < NFK; ++nf) {
+        if (mf < pl.kmf)
+          *reinterpret_cast<double2*>(out + (int64_t(mf) * NFK + nf) * 64 + 2 * lane) =
+              make_double2(accK[j][nf][0], accK[j][nf][1]);
+        accK[j][nf][0] = accK[j][nf][1] = 0.0;
+      }
     }
 #pragma unroll
     for (int j = 0; j < JT; ++j) {
-      const double a = gather_prod<FA>(row, offAT[j]);
+      const int mf = wi + pl.WG * j;
 #pragma unroll
-      for (int nf = 0; nf < NFT; ++nf) dmma_8x8x4(accT[j][nf][0], accT[j][nf][1], a, bT[nf]);
+      for (int nf = 0; nf < NFT; ++nf) {
+        if (mf < pl.tmf)
+          *reinterpret_cast<double2*>(out + (int64_t(pl.kmf) * NFK + int64_t(mf) * NFT + nf) * 64 + 2 * lane) =
+              make_double2(accT[j][nf][0], accT[j][nf][1]);
+        accT[j][nf][0] = accT[j][nf][1] = 0.0;
+      }
     }
   };
   for (int n = 0; n < nblk; ++n) {
     const double* cur = slabs + (n & 1) * (kRows * rl.bw);
-#pragma unroll 2
-    for (int i = 0; i < sp; ++i) kstep(cur, i);
+    kloop(cur, 0, sp);
     if (n + 1 < nblk) {
-      produce(xn, r0 + int64_t(n + 1) * kRows, slabs + ((n + 1) & 1) * (kRows * rl.bw));
-      xn = n + 2 < nblk ? load_x(r0 + int64_t(n + 2) * kRows) : 0.0;
+      produce(xn, n + 1, slabs + ((n + 1) & 1) * (kRows * rl.bw));
+      xn = n + 2 < nblk ? load_x(n + 2) : 0.0;
     }
-#pragma unroll 2
-    for (int i = sp; i < nloc; ++i) kstep(cur, i);
+    kloop(cur, sp, nloc);
+    for (int k = k0; k < k1; ++k)
+      if (g0 + n + 1 == sb(k + 1)) flush(k);
     __syncthreads();
-  }
-
-  double* out = ws + (int64_t(blockIdx.x) * pl.G + grp) * pl.len;
-#pragma unroll
-  for (int j = 0; j < JK; ++j) {
-    const int mrow = (wi + pl.WG * j) * 8 + (lane >> 2);
-#pragma unroll
-    for (int nf = 0; nf < NFK; ++nf)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int ncol = nf * 8 + 2 * (lane & 3) + e;
-        if (mrow < pl.KA && ncol < pl.KB) out[int64_t(mrow) * pl.KB + ncol] = accK[j][nf][e];
-      }
-  }
-#pragma unroll
-  for (int j = 0; j < JT; ++j) {
-    const int mrow = (wi + pl.WG * j) * 8 + (lane >> 2);
-#pragma unroll
-    for (int nf = 0; nf < NFT; ++nf)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int ncol = nf * 8 + 2 * (lane & 3) + e;
-        if (mrow < pl.TA && ncol < pl.TB) out[pl.Klen + int64_t(mrow) * pl.TB + ncol] = accT[j][nf][e];
-      }
   }
   if (bad_x) raise_flag(flags, FAGP_FLAG_X_NONFINITE);
 }
 
-// out[e] = sum over partials (fixed order: deterministic); non-finite -> PHI flag
-__global__ void partial_sum_kernel(const double* __restrict__ ws, int nparts, int64_t len, double* __restrict__ out,
+// out[e] = sum over the partials (fixed order: deterministic) of entry e of [K | t], read from
+// the fragment-major partial layout; non-finite -> PHI flag
+__global__ void partial_sum_kernel(const double* __restrict__ ws, const GPlan pl, double* __restrict__ out,
                                    uint32_t* flags) {
+  const int NFK = int(ceil_div(pl.KB, 8)), NFT = int(ceil_div(pl.TB, 8));
   bool bad = false;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < len; e += int64_t(gridDim.x) * blockDim.x) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < pl.len;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    int64_t m, n, frag;
+    if (e < pl.Klen) {
+      m = e / pl.KB;
+      n = e - m * pl.KB;
+      frag = (m >> 3) * NFK + (n >> 3);
+    } else {
+      m = (e - pl.Klen) / pl.TB;
+      n = (e - pl.Klen) - m * pl.TB;
+      frag = int64_t(pl.kmf) * NFK + (m >> 3) * NFT + (n >> 3);
+    }
+    const int64_t idx = frag * 64 + ((m & 7) * 4 + ((n & 7) >> 1)) * 2 + (n & 1);
+    // loads batched 16 at a time (latency-bound otherwise); the sum stays in partial order
     double s = 0.0;
-    for (int q = 0; q < nparts; ++q) s += ws[int64_t(q) * len + e];
+    int q = 0;
+    for (; q + 16 <= pl.nparts; q += 16) {
+      double v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) v[u] = ws[int64_t(q + u) * pl.plen + idx];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) s += v[u];
+    }
+    for (; q < pl.nparts; ++q) s += ws[int64_t(q) * pl.plen + idx];
     out[e] = s;
     bad |= not_finite(s);
   }
@@ -373,14 +427,21 @@ static bool make_gplan(int64_t N, int p, int M, GPlan& pl) {
   if (best < 0) return false;
   pl.Klen = int64_t(pl.KA) * pl.KB;
   pl.len = pl.Klen + int64_t(pl.TA) * pl.TB;
+  pl.plen = (int64_t(pl.kmf) * NFK + int64_t(pl.tmf) * NFT) * 64;
   const RowLayout rl = row_layout(p, M);
   const size_t smem = (size_t(2) * pl.LC + size_t(2) * kRows * rl.bw) * sizeof(double);
   if (smem > 220 * 1024) return false;
+  // rows: one CTA per SM, each a contiguous range of S sub-ranges (S = 4 once every sub-range
+  // holds at least 4 blocks, so a host pipeline can upload sub-range k + 1 of every CTA while
+  // the Gram contracts sub-range k)
   const int64_t blocks = tmax<int64_t>(1, ceil_div(N, kRows));
   pl.grid = int(tmin<int64_t>(num_sms(), blocks));
-  pl.rows_per_cta = ceil_div(blocks, pl.grid) * kRows;
+  const int64_t bpc = ceil_div(blocks, pl.grid);  // blocks per CTA
+  pl.S = bpc >= 8 ? 4 : 1;
+  if (const char* e = getenv("FAGP_GRAM_SUBRANGES")) pl.S = tmax(1, tmin<int>(int(bpc), atoi(e)));  // tuning knob
+  pl.rows_per_cta = bpc * kRows;
   pl.grid = int(tmax<int64_t>(1, ceil_div(tmax<int64_t>(N, 1), pl.rows_per_cta)));
-  pl.nparts = pl.grid * pl.G;
+  pl.nparts = pl.grid * pl.S * pl.G;
   return true;
 }
 
@@ -390,11 +451,11 @@ static size_t gram_smem(const GPlan& pl) {
 
 template <int FA, int NFK, int NFT>
 static int launch_gram_shape(const double* X, const double* y, double c, int64_t N, const fagp_basis* b,
-                             const GPlan& pl, double* ws, uint32_t* flags, cudaStream_t s) {
+                             const GPlan& pl, int k0, int k1, double* ws, uint32_t* flags, cudaStream_t s) {
   const size_t smem = gram_smem(pl);
   auto go = [&](auto kern) -> int {
     FAGP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    kern<<<pl.grid, kGramNT, smem, s>>>(X, y, c, N, view(b), pl, ws, flags);
+    kern<<<pl.grid, kGramNT, smem, s>>>(X, y, c, N, view(b), pl, k0, k1, ws, flags);
     return FAGP_OK;
   };
   if (pl.JK == 1 && pl.JT == 1) return go(fused_gram_kernel<FA, NFK, NFT, 1, 1>);
@@ -405,11 +466,11 @@ static int launch_gram_shape(const double* X, const double* y, double c, int64_t
 
 template <int FA>
 static int launch_gram_fa(const double* X, const double* y, double c, int64_t N, const fagp_basis* b,
-                          const GPlan& pl, double* ws, uint32_t* flags, cudaStream_t s) {
+                          const GPlan& pl, int k0, int k1, double* ws, uint32_t* flags, cudaStream_t s) {
   // (n-frags of K, n-frags of t) from M: L = 2M - 1 <= 8 NFK, M <= 8 NFT
-  if (pl.M <= 4) return launch_gram_shape<FA, 1, 1>(X, y, c, N, b, pl, ws, flags, s);
-  if (pl.M <= 8) return launch_gram_shape<FA, 2, 1>(X, y, c, N, b, pl, ws, flags, s);
-  return launch_gram_shape<FA, 3, 2>(X, y, c, N, b, pl, ws, flags, s);
+  if (pl.M <= 4) return launch_gram_shape<FA, 1, 1>(X, y, c, N, b, pl, k0, k1, ws, flags, s);
+  if (pl.M <= 8) return launch_gram_shape<FA, 2, 1>(X, y, c, N, b, pl, k0, k1, ws, flags, s);
+  return launch_gram_shape<FA, 3, 2>(X, y, c, N, b, pl, k0, k1, ws, flags, s);
 }
 
 bool gram_eligible(int64_t N, int p, int M) {
@@ -420,27 +481,74 @@ bool gram_eligible(int64_t N, int p, int M) {
 size_t gram_workspace(int64_t N, int p, int M) {
   GPlan pl;
   if (!make_gplan(N, p, M, pl)) return 0;
-  return size_t(pl.nparts) * size_t(pl.len) * sizeof(double);
+  return size_t(pl.nparts) * size_t(pl.plen) * sizeof(double);
 }
 
-int gram(const double* X, const double* y, double c, int64_t N, const fagp_basis* b, double* out, void* ws,
-         size_t ws_bytes, uint32_t* flags, cudaStream_t s) {
+int gram_chunks(int64_t N, int p, int M) {
+  GPlan pl;
+  return make_gplan(N, p, M, pl) ? pl.S : 1;
+}
+
+// H2D of the rows chunk k reads: sub-range k of every CTA (one 2-D copy for the CTAs whose
+// sub-range lies inside [0, N), one plain copy for the CTA that holds row N - 1)
+int upload_chunk(const double* Xh, const double* yh, int64_t N, int p, int M, int k, double* Xd, double* yd,
+                 cudaStream_t s) {
+  GPlan pl;
+  if (!make_gplan(N, p, M, pl)) {
+    if (k != 0) return FAGP_EINVAL;
+    if (N > 0) {
+      FAGP_CUDA_TRY(cudaMemcpyAsync(Xd, Xh, size_t(N) * p * sizeof(double), cudaMemcpyHostToDevice, s));
+      if (yh && yd) FAGP_CUDA_TRY(cudaMemcpyAsync(yd, yh, size_t(N) * sizeof(double), cudaMemcpyHostToDevice, s));
+    }
+    return FAGP_OK;
+  }
+  if (k < 0 || k >= pl.S) return FAGP_EINVAL;
+  const int64_t bpc = pl.rows_per_cta / kRows;
+  const int64_t off = (int64_t(k) * bpc / pl.S) * kRows;
+  const int64_t sub_rows = ((int64_t(k + 1) * bpc / pl.S) * kRows) - off;
+  // CTAs c with c rpc + off + sub_rows <= N
+  const int64_t head = N - off - sub_rows;
+  const int64_t full = head < 0 ? 0 : tmin<int64_t>(pl.grid, head / pl.rows_per_cta + 1);
+  if (full > 0) {
+    const size_t pitch = size_t(pl.rows_per_cta) * sizeof(double);
+    FAGP_CUDA_TRY(cudaMemcpy2DAsync(Xd + off * p, pitch * p, Xh + off * p, pitch * p, size_t(sub_rows) * p * 8,
+                                    size_t(full), cudaMemcpyHostToDevice, s));
+    if (yh && yd)
+      FAGP_CUDA_TRY(cudaMemcpy2DAsync(yd + off, pitch, yh + off, pitch, size_t(sub_rows) * 8, size_t(full),
+                                      cudaMemcpyHostToDevice, s));
+  }
+  if (full < pl.grid) {
+    const int64_t a = full * pl.rows_per_cta + off, e = tmin<int64_t>(N, a + sub_rows);
+    if (e > a) {
+      FAGP_CUDA_TRY(cudaMemcpyAsync(Xd + a * p, Xh + a * p, size_t(e - a) * p * 8, cudaMemcpyHostToDevice, s));
+      if (yh && yd) FAGP_CUDA_TRY(cudaMemcpyAsync(yd + a, yh + a, size_t(e - a) * 8, cudaMemcpyHostToDevice, s));
+    }
+  }
+  return FAGP_OK;
+}
+
+// chunks [k0, k1) of the plan; the last chunk also sums the partials into `out`
+int gram(const double* X, const double* y, double c, int64_t N, const fagp_basis* b, int k0, int k1, double* out,
+         void* ws, size_t ws_bytes, uint32_t* flags, cudaStream_t s) {
   GPlan pl;
   if (!make_gplan(N, b->p, b->M, pl)) return FAGP_EUNSUPPORTED;
-  if (ws == nullptr || ws_bytes < size_t(pl.nparts) * size_t(pl.len) * sizeof(double)) return FAGP_EWORKSPACE;
+  if (ws == nullptr || ws_bytes < size_t(pl.nparts) * size_t(pl.plen) * sizeof(double)) return FAGP_EWORKSPACE;
+  if (k0 < 0 || k1 > pl.S || k0 >= k1) return FAGP_EINVAL;
   double* w = static_cast<double*>(ws);
   int rc;
   switch (b->p - 1) {
-    case 1: rc = launch_gram_fa<1>(X, y, c, N, b, pl, w, flags, s); break;
-    case 2: rc = launch_gram_fa<2>(X, y, c, N, b, pl, w, flags, s); break;
-    case 3: rc = launch_gram_fa<3>(X, y, c, N, b, pl, w, flags, s); break;
+    case 1: rc = launch_gram_fa<1>(X, y, c, N, b, pl, k0, k1, w, flags, s); break;
+    case 2: rc = launch_gram_fa<2>(X, y, c, N, b, pl, k0, k1, w, flags, s); break;
+    case 3: rc = launch_gram_fa<3>(X, y, c, N, b, pl, k0, k1, w, flags, s); break;
     default: rc = FAGP_EUNSUPPORTED;
   }
   if (rc) return rc;
   FAGP_LAUNCH_CHECK();
-  const int grid = int(tmax<int64_t>(1, tmin<int64_t>(ceil_div(pl.len, 256), 4 * num_sms())));
-  partial_sum_kernel<<<grid, 256, 0, s>>>(w, pl.nparts, pl.len, out, flags);
-  FAGP_LAUNCH_CHECK();
+  if (k1 == pl.S) {
+    const int grid = int(tmax<int64_t>(1, tmin<int64_t>(ceil_div(pl.len, 256), 4 * num_sms())));
+    partial_sum_kernel<<<grid, 256, 0, s>>>(w, pl, out, flags);
+    FAGP_LAUNCH_CHECK();
+  }
   return FAGP_OK;
 }
 
@@ -469,6 +577,38 @@ template <int F>
 __device__ __forceinline__ void unpack_off(uint32_t v, int (&off)[F]) {
 #pragma unroll
   for (int f = 0; f < F; ++f) off[f] = int((v >> (8 * f)) & 0xffu);
+}
+
+// acc[f][nf] += A[rows 8 f + (lane >> 2)][kappa] B[kappa][nu] over the k-steps [k0, k1) of 4 kappa:
+// A gathered from the row slab by the packed offsets of kappa = 4 ks + (lane & 3), B from the
+// fragment-major operand.  Software-pipelined: the operands of k-step ks + 1 are loaded and
+// multiplied in program order before the DMMAs of k-step ks, so they overlap.
+template <int F, int NF>
+__device__ __forceinline__ void contract4(const double* row0, int bw, const uint32_t* offs, const double* B, int k0,
+                                          int k1, int lane, double (&acc)[4][NF][2]) {
+  if (k0 >= k1) return;
+  auto load = [&](int ks, double (&ao)[4], double (&bo)[NF]) {
+    int off[F];
+    unpack_off<F>(offs[4 * ks + (lane & 3)], off);
+#pragma unroll
+    for (int f = 0; f < 4; ++f) ao[f] = gather_prod<F>(row0 + 8 * f * bw, off);
+#pragma unroll
+    for (int nf = 0; nf < NF; ++nf) bo[nf] = B[(ks * NF + nf) * 32 + lane];
+  };
+  double a[4], bb[NF];
+  load(k0, a, bb);
+  for (int ks = k0; ks < k1; ++ks) {
+    double an[4], bn[NF];
+    load(ks + 1 < k1 ? ks + 1 : ks, an, bn);
+#pragma unroll
+    for (int f = 0; f < 4; ++f)
+#pragma unroll
+      for (int nf = 0; nf < NF; ++nf) dmma_8x8x4(acc[f][nf][0], acc[f][nf][1], a[f], bb[nf]);
+#pragma unroll
+    for (int f = 0; f < 4; ++f) a[f] = an[f];
+#pragma unroll
+    for (int nf = 0; nf < NF; ++nf) bb[nf] = bn[nf];
+  }
 }
 
 template <int FK, int FE, int FKM, int NFV, int NFM>
@@ -571,36 +711,8 @@ fused_predict_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView b, con
 #pragma unroll
         for (int nf = 0; nf < NFM; ++nf) accM[f][nf][0] = accM[f][nf][1] = 0.0;
       }
-      if (want_var) {
-#pragma unroll 2
-        for (int ks = v0; ks < v1; ++ks) {
-          int off[FK];
-          unpack_off<FK>(offV[4 * ks + (lane & 3)], off);
-          double a[4], bb[NFV];
-#pragma unroll
-          for (int f = 0; f < 4; ++f) a[f] = gather_prod<FK>(row0 + 8 * f * rl.bw, off);
-#pragma unroll
-          for (int nf = 0; nf < NFV; ++nf) bb[nf] = Bv[(ks * NFV + nf) * 32 + lane];
-#pragma unroll
-          for (int f = 0; f < 4; ++f)
-#pragma unroll
-            for (int nf = 0; nf < NFV; ++nf) dmma_8x8x4(accV[f][nf][0], accV[f][nf][1], a[f], bb[nf]);
-        }
-      }
-#pragma unroll 2
-      for (int ks = m0; ks < m1; ++ks) {
-        int off[FKM];
-        unpack_off<FKM>(offM[4 * ks + (lane & 3)], off);
-        double a[4], bb[NFM];
-#pragma unroll
-        for (int f = 0; f < 4; ++f) a[f] = gather_prod<FKM>(row0 + 8 * f * rl.bw, off);
-#pragma unroll
-        for (int nf = 0; nf < NFM; ++nf) bb[nf] = Bm[(ks * NFM + nf) * 32 + lane];
-#pragma unroll
-        for (int f = 0; f < 4; ++f)
-#pragma unroll
-          for (int nf = 0; nf < NFM; ++nf) dmma_8x8x4(accM[f][nf][0], accM[f][nf][1], a[f], bb[nf]);
-      }
+      if (want_var) contract4<FK, NFV>(row0, rl.bw, offV, Bv, v0, v1, lane, accV);
+      contract4<FKM, NFM>(row0, rl.bw, offM, Bm, m0, m1, lane, accM);
       // this quarter's epilogue contribution per row: sum_nu Y[i, nu] E[i, nu] (var),
       // sum_nu Z[i, nu] phi_0[i, nu] (mean); the 4 lanes of a row hold disjoint columns
 #pragma unroll
@@ -743,14 +855,29 @@ size_t fagp_gram_x_workspace_size(int64_t N, const fagp_basis* basis) {
   return round_up(table, 256) + fagp_gram_workspace_size(N, basis);
 }
 
-int fagp_gram_x(const double* X, int64_t N, const fagp_basis* basis, const double* y, double mean_const,
-                double* gram, void* workspace, size_t workspace_bytes, uint32_t* flags, void* stream) {
+int32_t fagp_gram_x_chunks(int64_t N, const fagp_basis* basis) {
+  if (check_basis(basis) || N < 0) return 1;
+  return fused::gram_chunks(N, basis->p, basis->M);
+}
+
+int fagp_gram_x_upload_chunk(const double* X_host, const double* y_host, int64_t N, const fagp_basis* basis,
+                              int32_t k, double* X, double* y, void* stream) {
+  int st = check_basis(basis);
+  if (st) return st;
+  if (N < 0 || (N > 0 && (X_host == nullptr || X == nullptr))) return FAGP_EINVAL;
+  return fused::upload_chunk(X_host, y_host, N, basis->p, basis->M, k, X, y, static_cast<cudaStream_t>(stream));
+}
+
+int fagp_gram_x_chunk(const double* X, int64_t N, const fagp_basis* basis, const double* y, double mean_const,
+                      int32_t k, double* gram, void* workspace, size_t workspace_bytes, uint32_t* flags,
+                      void* stream) {
   int st = check_basis(basis);
   if (st) return st;
   if (N < 0 || gram == nullptr || (N > 0 && X == nullptr)) return FAGP_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (fused::gram_eligible(N, basis->p, basis->M))
-    return fused::gram(X, y, mean_const, N, basis, gram, workspace, workspace_bytes, flags, s);
+    return fused::gram(X, y, mean_const, N, basis, k, k + 1, gram, workspace, workspace_bytes, flags, s);
+  if (k != 0) return FAGP_EINVAL;
   const size_t table = round_up(size_t(N) * table_width(basis->p, basis->M) * sizeof(double), 256);
   if (workspace == nullptr || workspace_bytes < table + fagp_gram_workspace_size(N, basis)) return FAGP_EWORKSPACE;
   double* T = static_cast<double*>(workspace);
@@ -759,6 +886,18 @@ int fagp_gram_x(const double* X, int64_t N, const fagp_basis* basis, const doubl
     if (st) return st;
   }
   return fagp_gram(T, N, basis, gram, static_cast<char*>(workspace) + table, workspace_bytes - table, flags, stream);
+}
+
+int fagp_gram_x(const double* X, int64_t N, const fagp_basis* basis, const double* y, double mean_const,
+                double* gram, void* workspace, size_t workspace_bytes, uint32_t* flags, void* stream) {
+  int st = check_basis(basis);
+  if (st) return st;
+  if (fused::gram_eligible(N, basis->p, basis->M)) {
+    if (N < 0 || gram == nullptr || (N > 0 && X == nullptr)) return FAGP_EINVAL;
+    return fused::gram(X, y, mean_const, N, basis, 0, fused::gram_chunks(N, basis->p, basis->M), gram, workspace,
+                       workspace_bytes, flags, static_cast<cudaStream_t>(stream));
+  }
+  return fagp_gram_x_chunk(X, N, basis, y, mean_const, 0, gram, workspace, workspace_bytes, flags, stream);
 }
 
 size_t fagp_predict_x_workspace_size(int64_t Ns, const fagp_basis* basis) {

@@ -24,6 +24,7 @@ from .errors import NumericalError
 from .mercer import LAMBDA_FLOOR_REL, Basis, raise_nonfinite
 
 JITTER_ATTEMPTS = 3  # backend.py:165
+_TRACE = None  # diagnostics: set to a list to collect run_host phase times in ms (tools/e2e_probe.py)
 
 
 class PosteriorEngine:
@@ -130,6 +131,117 @@ class PosteriorEngine:
             self.set_mean_weights()
         self.stage_predict(Xs)
         return self.mean, self.var
+
+    # -- the whole step from host memory (the fagp_posterior path) -------------------------
+    PREDICT_CHUNKS = 4
+
+    def _host_buffers(self):
+        import torch
+
+        if getattr(self, "X", None) is None:
+            p = self.basis.p
+            self.X = dev.empty((self.N, p), device=self.device)
+            self.y = dev.empty((self.N,), device=self.device)
+            self.Xs = dev.empty((self.Ns, p), device=self.device)
+            self.s_in = torch.cuda.Stream(device=self.device)
+            self.s_out = torch.cuda.Stream(device=self.device)
+            self._stage = {}
+        return self.X, self.y, self.Xs
+
+    def _pinned(self, a, key, shape):
+        """Host source for an async H2D copy: a pinned CPU tensor as is, anything else staged
+        into an engine-owned pinned buffer (one host memcpy)."""
+        import numpy as np
+        import torch
+
+        if isinstance(a, torch.Tensor) and a.is_pinned() and a.dtype == torch.float64 and a.is_contiguous():
+            return a.reshape(shape)
+        buf = self._stage.get(key)
+        if buf is None or tuple(buf.shape) != tuple(shape):
+            buf = torch.empty(shape, dtype=torch.float64, pin_memory=True)
+            self._stage[key] = buf
+        src = a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a, dtype=np.float64)
+        np.copyto(buf.numpy(), src.reshape(shape), casting="same_kind")
+        return buf
+
+    def run_host(self, Xh, yh, Xsh, fault_flip=False):
+        """One posterior evaluation from HOST inputs to host numpy (mean, var), pipelined:
+
+          * train rows go up in fagp_gram_x_chunks() pieces on a copy stream (sub-range k of every
+            CTA's rows) and Gram chunk k starts as soon as they have landed (bitwise identical
+            to one fagp_gram_x call);
+          * X* goes up behind them and overlaps the Gram tail and the factorisation;
+          * predict runs in row chunks, each chunk's mean/var D2H overlapping the next chunk.
+        Results land in fresh pinned host memory (returned as numpy views)."""
+        import time
+
+        import torch
+
+        trace = [time.perf_counter()] if _TRACE is not None else None
+        L, b = _lib.lib(), self.basis
+        cs = torch.cuda.current_stream(self.device)
+        X, y, Xs = self._host_buffers()
+        p = b.p
+        Xh = self._pinned(Xh, "X", (self.N, p))
+        yh = self._pinned(yh, "y", (self.N,))
+        Xsh = self._pinned(Xsh, "Xs", (self.Ns, p))
+        self.flags.zero_()
+        self.s_in.wait_stream(cs)
+        nch = int(L.fagp_gram_x_chunks(self.N, b.ref))
+        sin = _lib.stream_handle(self.s_in)
+        for k in range(nch):
+            _lib.check(L.fagp_gram_x_upload_chunk(_lib.ptr(Xh), _lib.ptr(yh), self.N, b.ref, k, _lib.ptr(X),
+                                                  _lib.ptr(y), sin), "upload")
+            ev = torch.cuda.Event()
+            ev.record(self.s_in)
+            cs.wait_event(ev)
+            _lib.check(L.fagp_gram_x_chunk(_lib.ptr(X), self.N, b.ref, _lib.ptr(y), self.mean_const, k,
+                                           _lib.ptr(self.packed), _lib.ptr(self.gram_ws), self.gram_ws_bytes,
+                                           self._flag(0), _lib.stream_handle(cs)), "gram")
+        with torch.cuda.stream(self.s_in):
+            if self.Ns:
+                Xs.copy_(Xsh, non_blocking=True)
+            ev_xs = torch.cuda.Event()
+            ev_xs.record(self.s_in)
+        if trace is not None:
+            trace.append(time.perf_counter())
+        self.stage_reduce()
+        st = self.stage_factor()
+        if trace is not None:
+            trace.append(time.perf_counter())
+        cs.wait_event(ev_xs)
+        if st != _lib.FAGP_OK:
+            self.raise_errors(X, Xs, y, factor_failed=True)
+        if fault_flip:
+            self.w.neg_()
+            self.set_mean_weights()
+        rows = 2 if self.want_var else 1
+        out = torch.empty((rows, self.Ns), dtype=torch.float64, pin_memory=True)
+        if trace is not None:
+            trace.append(time.perf_counter())
+        step = -(-max(self.Ns, 1) // (self.PREDICT_CHUNKS * 64)) * 64
+        for a in range(0, self.Ns, step):
+            e = min(self.Ns, a + step)
+            _lib.check(L.fagp_predict_x(_lib.ptr(Xs[a:e]), e - a, b.ref, _lib.ptr(self.predict_op), self.noise_var,
+                                        self.mean_const, _lib.ptr(self.mean[a:e]),
+                                        _lib.ptr(self.var[a:e] if self.want_var else None), self._flag(1),
+                                        _lib.ptr(self.pred_ws), self.pred_ws_bytes, _lib.stream_handle(cs)),
+                       "predict")
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            self.s_out.wait_event(ev)
+            with torch.cuda.stream(self.s_out):
+                out[0, a:e].copy_(self.mean[a:e], non_blocking=True)
+                if self.want_var:
+                    out[1, a:e].copy_(self.var[a:e], non_blocking=True)
+        if trace is not None:
+            trace.append(time.perf_counter())
+        self.s_out.synchronize()
+        if trace is not None:
+            trace.append(time.perf_counter())
+            _TRACE.append([1e3 * (b - a) for a, b in zip(trace, trace[1:])])
+        o = out.numpy()
+        return o[0], (o[1] if self.want_var else None)
 
     def raise_errors(self, X=None, Xs=None, y=None, factor_failed=False, after_predict=False):
         """Raise the reference's exception for whatever went wrong (validation order of

@@ -22,6 +22,7 @@ covariance (``want_cov=True``) is formed from the same factor for modest N*.
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass, replace
 
 import numpy as np
@@ -364,6 +365,9 @@ def fagp_posterior(train, Xstar, model, backend=None, want_cov=False, method="sc
         raise ValueError(f"form must be 'scaled' or 'literal', got {method!r}")
     kernel = as_ard(model.kernel)
     p = kernel.p
+    if (method == "scaled" and not return_device
+            and not any(dev.is_cuda(a) for a in (train.X, train.y, Xstar))):
+        return _posterior_host(train, Xstar, model, kernel, want_cov, memory_cap, delta2_variant, want_var, group)
     X = dev.points(train.X, p, "train.X")
     dev.points_shape(Xstar, p, "Xstar")
     Xs, xs_ready = dev.upload_async(Xstar if dev.is_tensor(Xstar) else np.atleast_2d(np.asarray(Xstar, dtype=float)),
@@ -397,6 +401,49 @@ def fagp_posterior(train, Xstar, model, backend=None, want_cov=False, method="sc
                 predict_op=eng.predict_op, jitter=float(eng.jitter.value))
         cov = _covariance(f, eng.table(Xs))
     return _result(mean, var, cov, return_device)
+
+
+_ENGINES = threading.local()
+
+
+def _engine_for(key, make):
+    """One cached PosteriorEngine per thread (buffers, streams and pinned staging reused across
+    calls of the same shape; thread-local, so concurrent callers never share one)."""
+    cached = getattr(_ENGINES, "entry", None)
+    if cached is not None and cached[0] == key:
+        return cached[1]
+    _ENGINES.entry = None
+    eng = make()
+    _ENGINES.entry = (key, eng)
+    return eng
+
+
+def _posterior_host(train, Xstar, model, kernel, want_cov, memory_cap, delta2_variant, want_var, group):
+    """fagp_posterior for host inputs: PosteriorEngine.run_host pipelines the H2D uploads with
+    the Gram chunks and the D2H of the results with the predict chunks."""
+    from .engine import PosteriorEngine
+
+    p = kernel.p
+    Xh = dev.host_points(train.X, p, "train.X")
+    Xsh = dev.host_points(Xstar, p, "Xstar")
+    N, Ns = int(Xh.shape[0]), int(Xsh.shape[0])
+    yh = dev.host_vector(train.y, N)
+    _budget(N, model.n_eigen, p, memory_cap)
+    _budget(Ns, model.n_eigen, p, memory_cap)
+    device = dev.device_of()
+    key = (kernel, int(model.n_eigen), N, Ns, float(model.noise_var), float(model.mean_const), delta2_variant,
+           str(device), bool(want_var), id(group))
+    eng = _engine_for(key, lambda: PosteriorEngine(kernel, model.n_eigen, N, Ns, model.noise_var, model.mean_const,
+                                                   delta2_variant, device=device, group=group, want_var=want_var))
+    mean, var = eng.run_host(Xh, yh, Xsh, fault_flip=_FAULT_FLIP_MEAN_SIGN)
+    eng.check(eng.X, eng.Xs, eng.y)
+    cov = None
+    if want_cov:
+        f = Fit(basis=eng.basis, noise_var=eng.noise_var, mean_const=eng.mean_const, N=N, lam=eng.lam,
+                lam_floored=eng.lam_floored, sqrt_lam=eng.sqrt_lam, packed=eng.packed, L=eng.L, t=eng.t, w=eng.w,
+                predict_op=eng.predict_op, jitter=float(eng.jitter.value))
+        cov = dev.to_host(_covariance(f, eng.table(eng.Xs)))
+    return PosteriorResult(mean=mean, cov=cov, var=var)
 
 
 def _result(mean, var, cov, return_device):
