@@ -192,6 +192,18 @@ int fagp_factor(const double* gram, const fagp_basis* basis, const double* sqrt_
                 double* jitter, int32_t* pivot_index, void* workspace, size_t workspace_bytes,
                 void* stream);
 
+/* fagp_factor for the modal shapes (2 <= p <= 8) without the Cholesky factor: the same A, jitter
+ * schedule, pivot_index on breakdown, G, t, w and predict operand, with A^{-1} (m x m, full
+ * symmetric, required) from ONE persistent cooperative kernel -- the right-looking blocked
+ * Cholesky of fagp_potrf (same pivot test and LAPACK info), the triangular inverse eliminated
+ * in the same 32-column steps, and X^T X -- instead of ~2 m/32 + 12 launches.  The posterior
+ * hot path needs only A^{-1} (posterior.py:233-235, 252-262).  FAGP_EUNSUPPORTED for p == 1
+ * and for m > 2048, where the blocked route wins (use fagp_factor).  Same workspace as
+ * fagp_factor. */
+int fagp_factor_inv(const double* gram, const fagp_basis* basis, const double* sqrt_lam, double sigma2,
+                    int32_t jitter_attempts, double* Ainv, double* G, double* t, double* w, double* predict_op,
+                    double* jitter, int32_t* pivot_index, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Overwrite the mean weights stored in the predict operand with w (used after the
  * reference's fault-injection hook flips w, posterior.py:245-246). */
 int fagp_set_mean_weights(double* predict_op, const double* w, const fagp_basis* basis, void* stream);
@@ -202,6 +214,14 @@ int fagp_set_mean_weights(double* predict_op, const double* w, const fagp_basis*
 size_t fagp_potrf_workspace_size(int64_t m);
 int fagp_potrf(double* A, int64_t m, int32_t* info_dev, void* workspace, size_t workspace_bytes,
                void* stream);
+
+/* Inverse of a symmetric positive definite m x m matrix (dpotrf + dpotri) by fagp_factor_inv's
+ * persistent kernel: Ainv (full symmetric) = A^{-1}; A is overwritten.  *info_dev
+ * (device int32) = 0, or the 1-based column where dpotrf would report the matrix not positive
+ * definite (Ainv is then unspecified).  A and Ainv must not alias. */
+size_t fagp_spd_inverse_workspace_size(int64_t m);
+int fagp_spd_inverse(double* A, int64_t m, double* Ainv, int32_t* info_dev, void* workspace, size_t workspace_bytes,
+                     void* stream);
 
 /* cho_solve (backend.py:191-193): B <- A^{-1} B given the lower factor L; B is m x nrhs. */
 int fagp_potrs(const double* L, int64_t m, double* B, int64_t nrhs, void* stream);

@@ -80,10 +80,13 @@ SIGNATURES = {
     "fagp_factor_workspace_size": (_SZ, [_I64]),
     "fagp_predict_operand_len": (_I64, [_BASIS]),
     "fagp_factor": (ctypes.c_int, [_P, _BASIS, _P, _D, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "fagp_factor_inv": (ctypes.c_int, [_P, _BASIS, _P, _D, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "fagp_set_mean_weights": (ctypes.c_int, [_P, _P, _BASIS, _P]),
     "fagp_potrf_workspace_size": (_SZ, [_I64]),
     "fagp_potrf": (ctypes.c_int, [_P, _I64, _P, _P, _SZ, _P]),
     "fagp_potrs": (ctypes.c_int, [_P, _I64, _P, _I64, _P]),
+    "fagp_spd_inverse_workspace_size": (_SZ, [_I64]),
+    "fagp_spd_inverse": (ctypes.c_int, [_P, _I64, _P, _P, _P, _SZ, _P]),
     "fagp_dgemm": (ctypes.c_int, [_I32, _I32, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64, _P]),
     "fagp_trtri_workspace_size": (_SZ, [_I64]),
     "fagp_trtri": (ctypes.c_int, [_P, _P, _I64, _P, _P, _SZ, _P]),

@@ -13,5 +13,14 @@ __host__ __device__ inline int64_t chol_scratch_len(int64_t m) { return m + 32 *
 // FAGP_EUNSUPPORTED when the device cannot co-schedule the grid (the caller falls back).
 int potrf_persistent(double* A, int64_t m, int64_t lda, int* info, double* scratch, cudaStream_t s);
 
+// scratch doubles: L_kk^{-1} x 2 | panels (T blocks) | flag
+__host__ __device__ inline int64_t cholinv_scratch_len(int64_t m) { return int64_t(2 + (m + 31) / 32) * 32 * 32 + 2; }
+
+// Dout (ld ldd, full symmetric) = A^{-1} of the SPD m x m matrix A (overwritten) by one
+// persistent kernel (Cholesky, triangular inverse into X (m x m scratch), X^T X); *info
+// (device) = dpotrf's 1-based breakdown column, 0 on success (Dout untouched otherwise).
+int chol_inverse_persistent(double* A, int64_t m, int64_t lda, int* info, double* scratch, double* X, double* Dout,
+                            int64_t ldd, cudaStream_t s);
+
 }  // namespace la
 }  // namespace fagp

@@ -558,6 +558,21 @@ __global__ void set_mean_weights_kernel(double* P, const double* w, int64_t m, i
     P[j * pc + m] = w[j];
 }
 
+// w_i = s_i sum_j D_ij (s_j t_j)  (= s * A^{-1}(s * t), posterior.py:233-235) from the explicit
+// inverse D: one warp per row, lanes stride over j, fixed-order shuffle reduction.
+__global__ void sym_gemv_scaled_kernel(const double* __restrict__ D, int64_t m, const double* __restrict__ s,
+                                       const double* __restrict__ t, double* __restrict__ w) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = int64_t(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (i >= m) return;
+  const double* Di = D + i * m;
+  double acc = 0.0;
+  for (int64_t j = lane; j < m; j += 32) acc = fma(Di[j], __dmul_rn(s[j], t[j]), acc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) w[i] = __dmul_rn(s[i], acc);
+}
+
 // ---------------------------------------------------------------------------------------
 // Workspace carving.
 struct FactorWs {
@@ -569,7 +584,7 @@ struct FactorWs {
   double* X;       // mp2^2
   double* Tmp;     // mp2^2 / 4
   double* D;       // m x m: X^T X for the modal predict operand
-  double* chol;    // chol_scratch_len(m)
+  double* chol;    // max(chol_scratch_len(m), cholinv_scratch_len(m))
   size_t bytes;
 };
 
@@ -593,7 +608,7 @@ inline FactorWs carve(void* base, int64_t m) {
   w.X = reinterpret_cast<double*>(take(size_t(mp) * mp * sizeof(double)));
   w.Tmp = reinterpret_cast<double*>(take(size_t(mp) * mp / 4 * sizeof(double) + sizeof(double)));
   w.D = reinterpret_cast<double*>(take(size_t(m) * m * sizeof(double)));
-  w.chol = reinterpret_cast<double*>(take(size_t(chol_scratch_len(m)) * sizeof(double)));
+  w.chol = reinterpret_cast<double*>(take(size_t(tmax(chol_scratch_len(m), cholinv_scratch_len(m))) * sizeof(double)));
   w.bytes = off;
   return w;
 }
@@ -822,6 +837,101 @@ int fagp_factor(const double* packed, const fagp_basis* basis, const double* sqr
     }
   }
   return FAGP_OK;
+}
+
+
+constexpr int64_t kFactorInvMaxM = 2048;
+
+// The hot-path variant of fagp_factor for the modal shapes: the same A, jitter schedule,
+// breakdown index, w and predict operand, but A^{-1} comes from one persistent kernel (potrf,
+// trtri and X^T X fused, chol.cu) instead of 2 m/32 + 12 launches, and L is not returned.
+int fagp_factor_inv(const double* packed, const fagp_basis* basis, const double* sqrt_lam, double sigma2,
+                    int32_t jitter_attempts, double* Ainv, double* G, double* t, double* w, double* predict_op,
+                    double* jitter_out, int32_t* pivot_out, void* workspace, size_t workspace_bytes, void* stream) {
+  {
+    int st = check_basis(basis);
+    if (st) return st;
+  }
+  const int64_t m = basis->m;
+  // latency-bound systems only: above a few thousand features the blocked route's large
+  // GEMM tiles (fagp_factor) win
+  if (!modal::enabled(basis->p, basis->M) || m > kFactorInvMaxM) return FAGP_EUNSUPPORTED;
+  if (packed == nullptr || sqrt_lam == nullptr || t == nullptr || w == nullptr || Ainv == nullptr ||
+      jitter_attempts < 0)
+    return FAGP_EINVAL;
+  if (!(sigma2 > 0.0) || !std::isfinite(sigma2)) return FAGP_EINVAL;
+  FactorWs ws = carve(workspace, m);
+  if (workspace == nullptr || workspace_bytes < ws.bytes) return FAGP_EWORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (pivot_out) *pivot_out = 0;
+  if (jitter_out) *jitter_out = 0.0;
+  double* D = Ainv;
+  double* A = ws.X;  // m x m (the expansion's temporary until the system is built)
+  int rc = modal::expand(packed, basis, ws.Lp, ws.X, s);
+  if (rc) return rc;
+  rc = modal::system(ws.Lp, packed, sqrt_lam, sigma2, 0.0, basis, nullptr, G, t, s);
+  if (rc) return rc;
+  double base = 0.0;
+  bool have_base = false;
+  int info_h = 0;
+  for (int attempt = 0; attempt <= jitter_attempts; ++attempt) {
+    double jit = 0.0;
+    if (attempt > 0) {
+      if (!have_base) {
+        rc = modal::system(ws.Lp, packed, sqrt_lam, sigma2, 0.0, basis, A, nullptr, nullptr, s);
+        if (rc) return rc;
+        trace_kernel<<<1, 256, 0, s>>>(A, m, ws.vec, ws.scalar);
+        FAGP_LAUNCH_CHECK();
+        double tr = 0.0;
+        FAGP_CUDA_TRY(cudaMemcpyAsync(&tr, ws.scalar, sizeof(double), cudaMemcpyDeviceToHost, s));
+        FAGP_CUDA_TRY(cudaStreamSynchronize(s));
+        base = 1e-12 * tr / double(m);
+        have_base = true;
+      }
+      double p10 = 1.0;
+      for (int k = 1; k < attempt; ++k) p10 *= 10.0;
+      jit = base * p10;
+    }
+    rc = modal::system(ws.Lp, packed, sqrt_lam, sigma2, jit, basis, A, nullptr, nullptr, s);
+    if (rc) return rc;
+    FAGP_CUDA_TRY(cudaMemsetAsync(ws.info, 0, sizeof(int), s));
+    rc = chol_inverse_persistent(A, m, m, ws.info, ws.chol, ws.D, D, m, s);
+    if (rc) return rc;
+    FAGP_CUDA_TRY(cudaMemcpyAsync(&info_h, ws.info, sizeof(int), cudaMemcpyDeviceToHost, s));
+    FAGP_CUDA_TRY(cudaStreamSynchronize(s));
+    if (jitter_out) *jitter_out = jit;
+    if (info_h == 0) break;
+  }
+  if (info_h != 0) {
+    if (pivot_out) *pivot_out = info_h;
+    return FAGP_ENOTPD;
+  }
+  sym_gemv_scaled_kernel<<<unsigned(ceil_div(m, 8)), 256, 0, s>>>(D, m, sqrt_lam, t, w);
+  FAGP_LAUNCH_CHECK();
+  if (predict_op) {
+    rc = modal::build_predict_op(D, sqrt_lam, w, basis, predict_op, ws.Lp, ws.X, s);
+    if (rc) return rc;
+  }
+  return FAGP_OK;
+}
+
+
+size_t fagp_spd_inverse_workspace_size(int64_t m) {
+  if (m < 1) return 0;
+  return align256(sizeof(int)) + align256(size_t(cholinv_scratch_len(m)) * sizeof(double)) +
+         align256(size_t(m) * m * sizeof(double));
+}
+
+int fagp_spd_inverse(double* A, int64_t m, double* Ainv, int32_t* info_dev, void* workspace, size_t workspace_bytes,
+                     void* stream) {
+  if (A == nullptr || Ainv == nullptr || info_dev == nullptr || m < 1 || A == Ainv) return FAGP_EINVAL;
+  if (workspace == nullptr || workspace_bytes < fagp_spd_inverse_workspace_size(m)) return FAGP_EWORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* scratch = reinterpret_cast<double*>(static_cast<char*>(workspace) + align256(sizeof(int)));
+  double* X = reinterpret_cast<double*>(reinterpret_cast<char*>(scratch) +
+                                        align256(size_t(cholinv_scratch_len(m)) * sizeof(double)));
+  FAGP_CUDA_TRY(cudaMemsetAsync(info_dev, 0, sizeof(int32_t), s));
+  return chol_inverse_persistent(A, m, m, info_dev, scratch, X, Ainv, m, s);
 }
 
 }  // extern "C"

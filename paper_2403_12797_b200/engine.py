@@ -47,7 +47,12 @@ class PosteriorEngine:
         self.pred_ws_bytes = int(L.fagp_predict_x_workspace_size(self.Ns, b.ref))
         self.pred_ws = e(max(1, -(-self.pred_ws_bytes // 8)))
         self.lam, self.lam_floored, self.sqrt_lam = e(m), e(m), e(m)
-        self.L = e(m, m)
+        # modal shapes factor through the block sweep (A^{-1} only, fagp_factor_inv); p = 1
+        # keeps the Cholesky route (its predict operand is built from L^{-1})
+        self.inverse_route = bool(L.fagp_factor_inv(None, b.ref, None, 1.0, 0, None, None, None, None, None, None,
+                                                     None, None, 0, None) != _lib.FAGP_EUNSUPPORTED)
+        self.L = None if self.inverse_route else e(m, m)
+        self.Ainv = e(m, m) if self.inverse_route else None
         self.G = e(m, m) if keep_gram else None
         self.t, self.w = e(m), e(m)
         self.predict_op = e(int(L.fagp_predict_operand_len(b.ref)))
@@ -90,6 +95,15 @@ class PosteriorEngine:
 
     def stage_factor(self, stream=None):
         L, s, b = _lib.lib(), _lib.stream_handle(stream), self.basis
+        if self.inverse_route:
+            self.status = L.fagp_factor_inv(_lib.ptr(self.packed), b.ref, _lib.ptr(self.sqrt_lam), self.noise_var,
+                                            JITTER_ATTEMPTS, _lib.ptr(self.Ainv), _lib.ptr(self.G), _lib.ptr(self.t),
+                                            _lib.ptr(self.w), _lib.ptr(self.predict_op), ctypes.byref(self.jitter),
+                                            ctypes.byref(self.pivot), _lib.ptr(self.factor_ws), self.factor_ws_bytes,
+                                            s)
+            if self.status not in (_lib.FAGP_OK, _lib.FAGP_ENOTPD):
+                _lib.check(self.status, "factor")
+            return self.status
         self.status = L.fagp_factor(_lib.ptr(self.packed), b.ref, _lib.ptr(self.sqrt_lam), self.noise_var,
                                     JITTER_ATTEMPTS, _lib.ptr(self.L), _lib.ptr(self.G), _lib.ptr(self.t),
                                     _lib.ptr(self.w), _lib.ptr(self.predict_op), ctypes.byref(self.jitter),

@@ -37,6 +37,20 @@ def potrf(a):
     return L, int(dev.to_host(info)[0])
 
 
+def spd_inverse(a):
+    """A^{-1} of an SPD matrix (Cholesky + triangular inverse + X^T X in one persistent kernel).
+    Returns (Ainv, info) with dpotrf's 1-based info on breakdown."""
+    A = dev.to_device(a).clone()
+    m = int(A.shape[0])
+    Ainv = dev.empty((m, m), device=A.device)
+    info = dev.zeros((1,), dtype="int32", device=A.device)
+    wsz = int(_lib.lib().fagp_spd_inverse_workspace_size(m))
+    ws = dev.empty((max(1, -(-wsz // 8)),), device=A.device)
+    _lib.check(_lib.lib().fagp_spd_inverse(_lib.ptr(A), m, _lib.ptr(Ainv), _lib.ptr(info), _lib.ptr(ws), wsz,
+                                           _lib.stream_handle()), "spd_inverse")
+    return Ainv, int(dev.to_host(info)[0])
+
+
 def potrs(L, b):
     """A^{-1} b given the lower factor (cho_solve, backend.py:191-193)."""
     m = int(L.shape[0])

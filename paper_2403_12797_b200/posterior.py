@@ -115,12 +115,13 @@ class Fit:
     lam_floored: object
     sqrt_lam: object
     packed: object  # packed extended Gram ((m+1)(m+2)/2,)
-    L: object  # (m, m) lower Cholesky factor of A
+    L: object  # (m, m) lower Cholesky factor of A (None on the inverse route)
     t: object  # Phi^T (y - c)
     w: object  # s * A^{-1}(s * t)
     predict_op: object  # [V^T | w] operand of fagp_predict
     jitter: float
     G: object | None = None
+    Ainv: object | None = None  # (m, m) A^{-1} (modal shapes, fagp_factor_inv)
 
     @property
     def m(self):
@@ -177,8 +178,9 @@ def gram_x_packed(basis, Xd, yd=None, mean_const=0.0, flag_ptr=None, stream=None
     return packed
 
 
-def factor_packed(basis, packed, noise_var, mean_const, N, keep_gram=False, stream=None):
-    """fagp_factor: Cholesky with jitter, weights, predict operand.  Returns (Fit, status, pivot)."""
+def factor_packed(basis, packed, noise_var, mean_const, N, keep_gram=False, stream=None, need_L=False):
+    """fagp_factor / fagp_factor_inv: jitter schedule, weights, predict operand.  Modal shapes
+    take the fused inverse route (A^{-1}, no L) unless ``need_L``.  Returns (Fit, status, pivot)."""
     L = _lib.lib()
     s = _lib.stream_handle(stream)
     m = basis.m
@@ -188,7 +190,6 @@ def factor_packed(basis, packed, noise_var, mean_const, N, keep_gram=False, stre
     sq = dev.empty((m,), device=device)
     _lib.check(L.fagp_eigenvalues(basis.ref, LAMBDA_FLOOR_REL, _lib.ptr(lam), _lib.ptr(lam_f), _lib.ptr(sq), s),
                "eigenvalues")
-    Lf = dev.empty((m, m), device=device)
     G = dev.empty((m, m), device=device) if keep_gram else None
     t = dev.empty((m,), device=device)
     w = dev.empty((m,), device=device)
@@ -197,11 +198,22 @@ def factor_packed(basis, packed, noise_var, mean_const, N, keep_gram=False, stre
     ws = dev.empty((max(1, wsz // 8),), device=device)
     jit = ctypes.c_double(0.0)
     piv = ctypes.c_int32(0)
-    st = L.fagp_factor(_lib.ptr(packed), basis.ref, _lib.ptr(sq), float(noise_var), JITTER_ATTEMPTS, _lib.ptr(Lf),
-                       _lib.ptr(G), _lib.ptr(t), _lib.ptr(w), _lib.ptr(P), ctypes.byref(jit), ctypes.byref(piv),
-                       _lib.ptr(ws), wsz, s)
+    Lf = Ainv = None
+    st = _lib.FAGP_EUNSUPPORTED
+    if not need_L:
+        Ainv = dev.empty((m, m), device=device)
+        st = L.fagp_factor_inv(_lib.ptr(packed), basis.ref, _lib.ptr(sq), float(noise_var), JITTER_ATTEMPTS,
+                               _lib.ptr(Ainv), _lib.ptr(G), _lib.ptr(t), _lib.ptr(w), _lib.ptr(P), ctypes.byref(jit),
+                               ctypes.byref(piv), _lib.ptr(ws), wsz, s)
+        if st == _lib.FAGP_EUNSUPPORTED:
+            Ainv = None
+    if st == _lib.FAGP_EUNSUPPORTED:
+        Lf = dev.empty((m, m), device=device)
+        st = L.fagp_factor(_lib.ptr(packed), basis.ref, _lib.ptr(sq), float(noise_var), JITTER_ATTEMPTS, _lib.ptr(Lf),
+                           _lib.ptr(G), _lib.ptr(t), _lib.ptr(w), _lib.ptr(P), ctypes.byref(jit), ctypes.byref(piv),
+                           _lib.ptr(ws), wsz, s)
     f = Fit(basis=basis, noise_var=float(noise_var), mean_const=float(mean_const), N=N, lam=lam, lam_floored=lam_f,
-            sqrt_lam=sq, packed=packed, L=Lf, t=t, w=w, predict_op=P, jitter=float(jit.value), G=G)
+            sqrt_lam=sq, packed=packed, L=Lf, t=t, w=w, predict_op=P, jitter=float(jit.value), G=G, Ainv=Ainv)
     return f, st, int(piv.value)
 
 
@@ -261,7 +273,8 @@ def predict_x_device(f, Xs, want_var=True, flag_ptr=None, stream=None):
 
 
 def _covariance(f, Ts):
-    """Full predictive covariance sigma2 * Z Z^T, Z = Phi* V^T (posterior.py:249-263)."""
+    """Full predictive covariance (posterior.py:249-263): sigma2 * Z Z^T with Z = Phi* V^T on
+    the Cholesky route, sigma2 * (Phi* S) A^{-1} (Phi* S)^T on the inverse route."""
     from .linalg import dgemm
 
     m = f.m
@@ -269,9 +282,14 @@ def _covariance(f, Ts):
     phis = dev.empty((Ns, m), device=Ts.device)
     _lib.check(_lib.lib().fagp_features(_lib.ptr(Ts), Ns, f.basis.ref, _lib.ptr(phis), None, _lib.stream_handle()),
                "features")
-    V = trtri_scaled(f)
-    Z = dgemm(phis, V, trans_b=True)  # Z = Phi* V^T
-    cov = dgemm(Z, Z, trans_b=True, alpha=f.noise_var)
+    if f.L is None:
+        Zs = phis * f.sqrt_lam  # Phi* S
+        Y = dgemm(Zs, f.Ainv)
+        cov = dgemm(Y, Zs, trans_b=True, alpha=f.noise_var)
+    else:
+        V = trtri_scaled(f)
+        Z = dgemm(phis, V, trans_b=True)  # Z = Phi* V^T
+        cov = dgemm(Z, Z, trans_b=True, alpha=f.noise_var)
     cov = 0.5 * (cov + cov.T)
     return cov
 
@@ -396,11 +414,15 @@ def fagp_posterior(train, Xstar, model, backend=None, want_cov=False, method="sc
     eng.check(X, Xs, yd)
     cov = None
     if want_cov:
-        f = Fit(basis=eng.basis, noise_var=eng.noise_var, mean_const=eng.mean_const, N=N, lam=eng.lam,
-                lam_floored=eng.lam_floored, sqrt_lam=eng.sqrt_lam, packed=eng.packed, L=eng.L, t=eng.t, w=eng.w,
-                predict_op=eng.predict_op, jitter=float(eng.jitter.value))
-        cov = _covariance(f, eng.table(Xs))
+        cov = _covariance(_engine_fit(eng, N), eng.table(Xs))
     return _result(mean, var, cov, return_device)
+
+
+def _engine_fit(eng, N):
+    """The Fit view of an engine's factorisation (for the full covariance)."""
+    return Fit(basis=eng.basis, noise_var=eng.noise_var, mean_const=eng.mean_const, N=N, lam=eng.lam,
+               lam_floored=eng.lam_floored, sqrt_lam=eng.sqrt_lam, packed=eng.packed, L=eng.L, t=eng.t, w=eng.w,
+               predict_op=eng.predict_op, jitter=float(eng.jitter.value), Ainv=eng.Ainv)
 
 
 _ENGINES = threading.local()
@@ -439,10 +461,7 @@ def _posterior_host(train, Xstar, model, kernel, want_cov, memory_cap, delta2_va
     eng.check(eng.X, eng.Xs, eng.y)
     cov = None
     if want_cov:
-        f = Fit(basis=eng.basis, noise_var=eng.noise_var, mean_const=eng.mean_const, N=N, lam=eng.lam,
-                lam_floored=eng.lam_floored, sqrt_lam=eng.sqrt_lam, packed=eng.packed, L=eng.L, t=eng.t, w=eng.w,
-                predict_op=eng.predict_op, jitter=float(eng.jitter.value))
-        cov = dev.to_host(_covariance(f, eng.table(eng.Xs)))
+        cov = dev.to_host(_covariance(_engine_fit(eng, N), eng.table(eng.Xs)))
     return PosteriorResult(mean=mean, cov=cov, var=var)
 
 
@@ -494,7 +513,7 @@ class LambdaBarSolve:
         self.noise_var = float(noise_var)
         self._es = es
         packed = gram_x_packed(es.basis, es.X, None, 0.0)
-        f, st, piv = factor_packed(es.basis, packed, noise_var, 0.0, es.N, keep_gram=True)
+        f, st, piv = factor_packed(es.basis, packed, noise_var, 0.0, es.N, keep_gram=True, need_L=True)
         self._fit = f
         self._gram = f.G
         self.lam_floored = dev.to_host(f.lam_floored)

@@ -106,13 +106,19 @@ def test_weights_match_oracle(cases):
     basis = F.Basis(c.kernel(), c.M, c.variant)
     T = _stage_tables(basis, dev.to_device(c.X), None, None)
     packed = gram_packed(basis, T, dev.to_device(c.y), c.mean_const)
-    f, st, _ = factor_packed(basis, packed, c.noise_var, c.mean_const, c.N)
+    f, st, _ = factor_packed(basis, packed, c.noise_var, c.mean_const, c.N, need_L=True)
     G, t = unpack(basis, packed)
     o = O.factor(G, t, c.ref["lam"], c.noise_var)
     assert scaled_err(dev.to_host(f.w), o["w"]) < 1e-10
     Lg = dev.to_host(f.L)
     assert scaled_err(Lg, o["L"]) < 1e-12
     assert np.all(np.triu(Lg, 1) == 0)
+    # the fused inverse route (hot path): same weights, A^{-1} against the oracle's factor
+    fi, st, _ = factor_packed(basis, packed, c.noise_var, c.mean_const, c.N)
+    assert st == 0 and fi.L is None
+    assert scaled_err(dev.to_host(fi.w), o["w"]) < 1e-10
+    Li = np.linalg.inv(o["L"])
+    assert scaled_err(dev.to_host(fi.Ainv), Li.T @ Li) < 1e-9
 
 
 def test_run_to_run_bitwise_determinism(cases):
@@ -342,3 +348,41 @@ def test_host_pipeline_bitwise_equals_device_path(N, Ns):
     assert np.array_equal(a.mean, b.mean) and np.array_equal(a.var, b.var)
     c = F.fagp_posterior(Host, Xs, model, memory_cap=None)  # cached engine, second call
     assert np.array_equal(a.mean, c.mean) and np.array_equal(a.var, c.var)
+
+
+@pytest.mark.parametrize("m", [1, 5, 31, 32, 33, 64, 100, 257, 1000])
+def test_spd_inverse_sweep_matches_lapack(m):
+    """fagp_spd_inverse (persistent Cholesky + trtri + lauum) against numpy's inverse on SPD
+    matrices, Cholesky-grade accuracy on an ill-conditioned one, and LAPACK dpotrf's 1-based
+    info on indefinite ones."""
+    import scipy.linalg as sla
+
+    from paper_2403_12797_b200.linalg import spd_inverse
+
+    rng = np.random.default_rng(100 + m)
+    B = rng.standard_normal((m, m))
+    A = B @ B.T + m * np.eye(m)
+    Ainv, info = spd_inverse(A)
+    assert info == 0
+    got = dev.to_host(Ainv)
+    ref = np.linalg.inv(A)
+    assert np.array_equal(got, got.T)
+    assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) < 1e-12
+    # a badly conditioned SPD matrix (cond ~ 1e10) still matches to the conditioning
+    q, _ = np.linalg.qr(rng.standard_normal((m, m)))
+    ev = np.logspace(0, -10, m)
+    Ac = 0.5 * ((q * ev) @ q.T + ((q * ev) @ q.T).T)
+    inv_c, info_c = spd_inverse(Ac)
+    assert info_c == 0
+    got_c = dev.to_host(inv_c)
+    ref_c = np.linalg.inv(Ac)
+    assert np.max(np.abs(got_c - ref_c)) / np.max(np.abs(ref_c)) < 1e-5
+    if m >= 5:
+        for where in (m // 2, m - 1, 1):
+            ev = np.linspace(1.0, 2.0, m)
+            ev[where] = -1.0
+            Ai = (q * ev) @ q.T
+            Ai = 0.5 * (Ai + Ai.T)
+            _, info_ref = sla.lapack.dpotrf(Ai, lower=1)
+            _, info = spd_inverse(Ai)
+            assert info == info_ref > 0
