@@ -47,7 +47,7 @@ CONFIGS = {
 METRIC = "posterior mean+var samples/s (N=1e6, p=3, M=10); % FP64 tensor peak"
 NOISE_VAR = 0.0025
 FP64_PEAK_FILE = ROOT / "profiles" / "fp64_peak_r01.json"
-NCU_SUMMARY_FILE = ROOT / "profiles" / "ncu_summary_r01m.json"
+NCU_SUMMARY_FILE = ROOT / "profiles" / "ncu_summary_r01w.json"
 
 
 def log(*a):
@@ -348,13 +348,13 @@ def main():
     g_ms, p_ms = statistics.mean(gram_ms), statistics.mean(pred_ms)
     peak, peak_src = fp64_peak()
     if g_ms >= p_ms:
-        dom, dflops, rflops, dms = "fagp_gram (modal DMMA GEMM + reduce + t)" if pair else \
+        dom, dflops, rflops, dms = "fagp_gram_x (eigenfunctions on chip + modal DMMA Gram + t, partial sum)" if pair else \
             "fagp_gram (fused SYRK + reduce)", gram_flops, ref_gram, g_ms
-        traffic = ncu_traffic("modal_gram_kernel" if pair else "gram_kernel_fast")
+        traffic = ncu_traffic("fused_gram_kernel" if pair else "gram_kernel_fast")
     else:
-        dom, dflops, rflops, dms = "fagp_predict (modal variance GEMM + mean)" if pair else \
+        dom, dflops, rflops, dms = "fagp_predict_x (eigenfunctions on chip + modal DMMA variance + mean)" if pair else \
             "fagp_predict (fused triangular GEMM)", pred_flops, ref_pred, p_ms
-        traffic = ncu_traffic("modal_var_kernel" if pair else "predict_kernel_fast")
+        traffic = ncu_traffic("fused_predict_kernel" if pair else "predict_kernel_fast")
     achieved = dflops / (dms / 1e3) / 1e12
     roofline = {"bound": "tensor", "kernel": dom, "achieved": round(achieved, 3), "peak": peak, "unit": "TFLOP/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,

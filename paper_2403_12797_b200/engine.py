@@ -230,7 +230,7 @@ class PosteriorEngine:
             self.w.neg_()
             self.set_mean_weights()
         rows = 2 if self.want_var else 1
-        out = torch.empty((rows, self.Ns), dtype=torch.float64, pin_memory=True)
+        out, o = self._out_buffer(rows)
         if trace is not None:
             trace.append(time.perf_counter())
         step = -(-max(self.Ns, 1) // (self.PREDICT_CHUNKS * 64)) * 64
@@ -254,8 +254,28 @@ class PosteriorEngine:
         if trace is not None:
             trace.append(time.perf_counter())
             _TRACE.append([1e3 * (b - a) for a, b in zip(trace, trace[1:])])
-        o = out.numpy()
         return o[0], (o[1] if self.want_var else None)
+
+    def _out_buffer(self, rows):
+        """A pinned (rows, N*) result buffer no caller still holds: the returned mean/var are
+        views of the pool entry's ndarray, so its refcount says whether it is free.  Avoids a
+        cudaHostAlloc (milliseconds) whenever the host caching allocator misses."""
+        import sys
+
+        import torch
+
+        pool = self.__dict__.setdefault("_out_pool", [])
+        for t, arr in pool:
+            if arr.shape == (rows, self.Ns) and sys.getrefcount(arr) <= 3:  # pool tuple + loop name + argument
+                return t, arr
+        # two at a time: the common `r = fagp_posterior(...)` loop holds one result while the
+        # next call fills the other
+        for _ in range(1 if pool else 2):
+            t = torch.empty((rows, self.Ns), dtype=torch.float64, pin_memory=True)
+            pool.append((t, t.numpy()))
+        while len(pool) > 4:  # forget the oldest (views still held keep their memory alive)
+            pool.pop(0)
+        return pool[-1]
 
     def raise_errors(self, X=None, Xs=None, y=None, factor_failed=False, after_predict=False):
         """Raise the reference's exception for whatever went wrong (validation order of

@@ -27,6 +27,10 @@ for _ in range(3):
 torch.cuda.synchronize()
 import gc  # noqa: E402
 
+import paper_2403_12797_b200.engine as E  # noqa: E402
+
+E._TRACE = []
+gc.callbacks.append(lambda phase, info: print(f"  [gc {phase} gen{info['generation']}]", time.perf_counter()))
 for label in ("gc on", "gc off"):
     if label == "gc off":
         gc.disable()
@@ -36,10 +40,9 @@ for label in ("gc on", "gc off"):
         r = F.fagp_posterior(T, Xsp, model, memory_cap=None)
         t1 = time.perf_counter()
         ts.append(1e3 * (t1 - t0))
+        print(f"  call {rep}: {1e3 * (t1 - t0):.2f} ms, phases", " ".join(f"{x:.2f}" for x in E._TRACE[-1]), t0)
     print(label, "api ms:", " ".join(f"{t:.2f}" for t in ts))
 gc.enable()
-import paper_2403_12797_b200.engine as E  # noqa: E402
-
 E._TRACE = []
 for rep in range(12):
     r = F.fagp_posterior(T, Xsp, model, memory_cap=None)
