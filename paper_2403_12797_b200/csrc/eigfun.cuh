@@ -40,25 +40,71 @@ __device__ __forceinline__ void eval_phi_dim(double x, const BasisView& b, int d
   }
 }
 
-// out[k * stride] = g_{d,k}(x), k < L = 2M - 1 (the modal functions spanning phi_a phi_b)
+// out[k * stride] = g_{d,k}(x), k < L = 2M - 1 (the modal functions spanning phi_a phi_b).
+// g is not a reference quantity (only its span is), so it is evaluated for speed at full
+// accuracy: the Gaussian as the square of phi's own exponential, exp(-2 delta2 x^2) =
+// exp((-delta2 x) x)^2, and the recurrence with one FMA on the dependency chain
+// (h_{k+1} = fma(y c1_k, h_k, -(c2_k h_{k-1})), the c2 product is off the chain).
+__device__ __forceinline__ double g_amp(const BasisView& b, int d, double e1) {
+  const double sb = b.sqrt_beta()[d];
+  return __dmul_rn(__dmul_rn(sb, sb), __dmul_rn(e1, e1));
+}
+
+__device__ __forceinline__ double phi_exp(const BasisView& b, int d, double x) {
+  return exp(__dmul_rn(__dmul_rn(b.neg_delta2()[d], x), x));
+}
+
 __device__ __forceinline__ void eval_g_dim(double x, const BasisView& b, int d, const double* c1, const double* c2,
                                            double* out, int stride = 1) {
   const int L = modal_L(b.M);
-  const double zr = __dmul_rn(b.rho_beta()[d], x);
-  const double sb = b.sqrt_beta()[d];
-  const double amp =
-      __dmul_rn(__dmul_rn(sb, sb), exp(__dmul_rn(__dmul_rn(__dmul_rn(2.0, b.neg_delta2()[d]), x), x)));
-  const double yz = __dmul_rn(zr, kSqrt2);
+  const double amp = g_amp(b, d, phi_exp(b, d, x));
+  const double yz = __dmul_rn(__dmul_rn(b.rho_beta()[d], x), kSqrt2);
   double gm1 = 1.0;
   out[0] = amp;
   if (L > 1) {
     double h = __dmul_rn(yz, kSqrt2);
     out[stride] = __dmul_rn(amp, h);
     for (int k = 1; k < L - 1; ++k) {
-      const double hn = __dsub_rn(__dmul_rn(__dmul_rn(yz, c1[k]), h), __dmul_rn(c2[k], gm1));
+      const double hn = fma(__dmul_rn(yz, c1[k]), h, -__dmul_rn(c2[k], gm1));
       out[(k + 1) * stride] = __dmul_rn(amp, hn);
       gm1 = h;
       h = hn;
+    }
+  }
+}
+
+// phi (reference order, bit-faithful) and g of one (point, dimension) sharing the exponential,
+// the two recurrences advanced in one loop (independent chains); rphi (nullable) <- r * phi.
+__device__ __forceinline__ void eval_phi_g_dim(double x, double r, const BasisView& b, int d, const double* c1,
+                                               const double* c2, double* out_phi, double* out_g, double* out_rphi) {
+  const int M = b.M, L = modal_L(M);
+  const double zr = __dmul_rn(b.rho_beta()[d], x);
+  const double e1 = phi_exp(b, d, x);
+  const double env = __dmul_rn(b.sqrt_beta()[d], e1);
+  const double amp = g_amp(b, d, e1);
+  const double yz = __dmul_rn(zr, kSqrt2);
+  double hp = __dmul_rn(zr, kSqrt2), hpm = 1.0;  // phi chain: h_1, h_0
+  double hg = __dmul_rn(yz, kSqrt2), hgm = 1.0;  // g chain
+  auto put_phi = [&](int k, double h) {
+    const double v = __dmul_rn(env, h);
+    out_phi[k] = v;
+    if (out_rphi) out_rphi[k] = __dmul_rn(r, v);
+  };
+  put_phi(0, 1.0);
+  out_g[0] = amp;
+  if (M > 1) put_phi(1, hp);
+  if (L > 1) out_g[1] = __dmul_rn(amp, hg);
+  for (int k = 1; k < L - 1; ++k) {
+    const double a1 = c1[k], a2 = c2[k];
+    const double hgn = fma(__dmul_rn(yz, a1), hg, -__dmul_rn(a2, hgm));
+    out_g[k + 1] = __dmul_rn(amp, hgn);
+    hgm = hg;
+    hg = hgn;
+    if (k < M - 1) {
+      const double hpn = __dsub_rn(__dmul_rn(__dmul_rn(zr, a1), hp), __dmul_rn(a2, hpm));
+      put_phi(k + 1, hpn);
+      hpm = hp;
+      hp = hpn;
     }
   }
 }
@@ -79,11 +125,13 @@ __device__ __forceinline__ void eval_multi(const double (&x)[T], const int (&d)[
   double zr[T];
 #pragma unroll
   for (int t = 0; t < T; ++t) zr[t] = __dmul_rn(b.rho_beta()[d[t]], x[t]);
+  double e1[T];
   if (want_phi) {
     double env[T], h[T], hm1[T];
 #pragma unroll
     for (int t = 0; t < T; ++t) {
-      env[t] = __dmul_rn(b.sqrt_beta()[d[t]], exp(__dmul_rn(__dmul_rn(b.neg_delta2()[d[t]], x[t]), x[t])));
+      e1[t] = phi_exp(b, d[t], x[t]);
+      env[t] = __dmul_rn(b.sqrt_beta()[d[t]], e1[t]);
       hm1[t] = 1.0;
       h[t] = __dmul_rn(zr[t], kSqrt2);
       if (out_phi[t]) {
@@ -106,9 +154,7 @@ __device__ __forceinline__ void eval_multi(const double (&x)[T], const int (&d)[
     double amp[T], yz[T], h[T], gm1[T];
 #pragma unroll
     for (int t = 0; t < T; ++t) {
-      const double sb = b.sqrt_beta()[d[t]];
-      amp[t] = __dmul_rn(__dmul_rn(sb, sb),
-                         exp(__dmul_rn(__dmul_rn(__dmul_rn(2.0, b.neg_delta2()[d[t]]), x[t]), x[t])));
+      amp[t] = g_amp(b, d[t], want_phi ? e1[t] : phi_exp(b, d[t], x[t]));
       yz[t] = __dmul_rn(zr[t], kSqrt2);
       gm1[t] = 1.0;
       h[t] = __dmul_rn(yz[t], kSqrt2);
@@ -121,7 +167,7 @@ __device__ __forceinline__ void eval_multi(const double (&x)[T], const int (&d)[
       const double a1 = c1[k], a2 = c2[k];
 #pragma unroll
       for (int t = 0; t < T; ++t) {
-        const double hn = __dsub_rn(__dmul_rn(__dmul_rn(yz[t], a1), h[t]), __dmul_rn(a2, gm1[t]));
+        const double hn = fma(__dmul_rn(yz[t], a1), h[t], -__dmul_rn(a2, gm1[t]));
         if (out_g[t]) out_g[t][k + 1] = __dmul_rn(amp[t], hn);
         gm1[t] = h[t];
         h[t] = hn;

@@ -151,6 +151,7 @@ __device__ __forceinline__ double gather_prod(const double* row, const int (&off
 // (j < JT), each against every B fragment: all counts compile-time, no predication.
 constexpr int kGramW = 16;
 constexpr int kGramNT = kGramW * 32;
+constexpr int kGR = 128;                // rows per block (32 k-steps): one barrier per 128 rows
 
 struct GPlan {
   int p, M, L, LC;
@@ -160,10 +161,17 @@ struct GPlan {
   int JK, JT;          // m-fragments per warp
   int64_t Klen, len;   // output layout [K (KA*KB) | t (TA*TB = m)]
   int64_t plen;        // one partial: (kmf NFK + tmf NFT) fragments of 64 doubles
-  int64_t rows_per_cta;  // multiple of kRows
+  int64_t rows_per_cta;  // multiple of kGR
   int S;                 // sub-ranges per CTA = chunks a host pipeline may launch separately
   int grid, nparts;      // nparts = grid * S * G partials
 };
+
+#ifdef FAGP_GRAM_PROFILE
+__device__ long long g_gram_prof[4];
+extern "C" int fagp_debug_gram_profile(long long* out) {  // diagnostics build only
+  return cudaMemcpyFromSymbol(out, g_gram_prof, sizeof(g_gram_prof)) == cudaSuccess ? 0 : 5;
+}
+#endif
 
 template <int FA, int NFK, int NFT, int JK, int JT>
 __global__ void __launch_bounds__(kGramNT, 1)
@@ -173,66 +181,66 @@ fused_gram_kernel(const double* __restrict__ X, const double* __restrict__ y, do
   const RowLayout rl = row_layout(pl.p, pl.M);
   double* c1 = sm;
   double* c2 = sm + pl.LC;
-  double* slabs = sm + 2 * pl.LC;  // [2][kRows * bw]
+  double* slabs = sm + 2 * pl.LC;  // [2][kGR * bw]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int p = pl.p, M = pl.M, L = pl.L;
   for (int k = tid; k < pl.LC; k += kGramNT) {
     c1[k] = herm_c1(k);
     c2[k] = herm_c2(k);
   }
-  // CTA rows [cta rpc, (cta + 1) rpc) = blocks [0, bpc) of kRows rows, cut into pl.S sub-ranges
+  // CTA rows [cta rpc, (cta + 1) rpc) = blocks [0, bpc) of kGR rows, cut into pl.S sub-ranges
   // (sub-range k = blocks [k bpc / S, (k + 1) bpc / S)); this launch covers sub-ranges [k0, k1)
   // and writes one partial per (CTA, sub-range, row group)
   const int cta = int(blockIdx.x);
-  const int bpc = int(pl.rows_per_cta / kRows);
+  const int bpc = int(pl.rows_per_cta / kGR);
   auto sb = [&](int k) { return int(int64_t(k) * bpc / pl.S); };
   const int g0 = sb(k0);
   const int nblk = sb(k1) - g0;
-  auto blk_base = [&](int j) -> int64_t { return int64_t(cta) * pl.rows_per_cta + int64_t(g0 + j) * kRows; };
-  auto blk_end = [&](int j) -> int64_t { return tmin<int64_t>(N, blk_base(j) + kRows); };
+  auto blk_base = [&](int j) -> int64_t { return int64_t(cta) * pl.rows_per_cta + int64_t(g0 + j) * kGR; };
+  auto blk_end = [&](int j) -> int64_t { return tmin<int64_t>(N, blk_base(j) + kGR); };
   bool bad_x = false;
 
-  // production role (lanes < 8p): row 4 warp + lane / 2p, dimension (lane % 2p) / 2, section
-  // phi (even lanes) or g (odd lanes); the phi lane of the last dimension also writes r phi.
-  const bool plane = lane < 8 * p;
-  const int prow = 4 * warp + lane / (2 * p), pdim = (lane % (2 * p)) >> 1;
-  const bool psec_g = lane & 1;
-  auto load_x = [&](int j) -> double {
-    const int64_t r = blk_base(j) + prow;
-    return (plane && r < blk_end(j)) ? X[r * p + pdim] : 0.0;
+  // production: thread t < kGR p evaluates phi and g (one shared exponential, two independent
+  // recurrences) of row t / p, dimension t % p; the last dimension also writes r phi.  x and y of
+  // the next block are loaded one block ahead.
+  const bool plane = tid < kGR * p;
+  const int prow = tid / p, pdim = tid - (tid / p) * p;
+  struct Pre {
+    double x, y;
   };
-  auto produce = [&](double x, int j, double* slab) {
-    if (plane) {
-      double* row = slab + prow * rl.bw;
-      const int64_t rb = blk_base(j);
-      const bool valid = rb + prow < blk_end(j);
-      const double rr = (valid && y != nullptr) ? __dsub_rn(y[rb + prow], c) : 0.0;  // r = y - c (posterior.py:229)
-      if (valid) {
-        bad_x |= not_finite(x);
-        if (psec_g) {
-          eval_g_dim(x, b, pdim, c1, c2, row + rl.goff + pdim * L);
-        } else {
-          eval_phi_dim(x, b, pdim, c1, c2, row + rl.poff + pdim * M);
-          if (pdim == p - 1)
-            for (int k = 0; k < M; ++k) row[rl.rpoff + k] = __dmul_rn(rr, row[rl.poff + pdim * M + k]);
-        }
-      } else if (psec_g) {
-        for (int k = 0; k < L; ++k) row[rl.goff + pdim * L + k] = 0.0;
-      } else {
-        for (int k = 0; k < M; ++k) row[rl.poff + pdim * M + k] = 0.0;
-        if (pdim == p - 1)
-          for (int k = 0; k < M; ++k) row[rl.rpoff + k] = 0.0;
-      }
-      if (pdim == 0 && !psec_g) {
-        row[rl.roff] = rr;
-        row[rl.one] = 1.0;
-        row[rl.zero] = 0.0;
-      }
+  auto load_pre = [&](int j, Pre& pr) {
+    const int64_t r = blk_base(j) + prow;
+    const bool ok = plane && r < blk_end(j);
+    pr.x = ok ? X[r * p + pdim] : 0.0;
+    pr.y = (ok && y != nullptr && pdim == p - 1) ? y[r] : c;
+  };
+  auto produce = [&](const Pre& pr, int j, double* slab) {
+    if (!plane) return;
+    double* row = slab + prow * rl.bw;
+    const bool valid = blk_base(j) + prow < blk_end(j);
+    if (valid) {
+      bad_x |= not_finite(pr.x);
+      const double rr = __dsub_rn(pr.y, c);  // r = y - c (posterior.py:229)
+      eval_phi_g_dim(pr.x, rr, b, pdim, c1, c2, row + rl.poff + pdim * M, row + rl.goff + pdim * L,
+                     pdim == p - 1 ? row + rl.rpoff : nullptr);
+    } else {
+      for (int k = 0; k < M; ++k) row[rl.poff + pdim * M + k] = 0.0;
+      for (int k = 0; k < L; ++k) row[rl.goff + pdim * L + k] = 0.0;
+      if (pdim == p - 1)
+        for (int k = 0; k < M; ++k) row[rl.rpoff + k] = 0.0;
+    }
+    if (pdim == 0) {
+      row[rl.one] = 1.0;
+      row[rl.zero] = 0.0;
     }
   };
   __syncthreads();
-  if (nblk > 0) produce(load_x(0), 0, slabs);
-  double xn = nblk > 1 ? load_x(1) : 0.0;
+  Pre pre;
+  if (nblk > 0) {
+    load_pre(0, pre);
+    produce(pre, 0, slabs);
+  }
+  if (nblk > 1) load_pre(1, pre);
 
   const int grp = warp / pl.WG, wi = warp - grp * pl.WG;
   int offAK[JK][FA], offAT[JT][FA], offBK[NFK], offBT[NFT];
@@ -263,8 +271,7 @@ fused_gram_kernel(const double* __restrict__ X, const double* __restrict__ y, do
   for (int j = 0; j < JT; ++j)
 #pragma unroll
     for (int nf = 0; nf < NFT; ++nf) accT[j][nf][0] = accT[j][nf][1] = 0.0;
-  const int nloc = (kRows / 4 - grp + pl.G - 1) / pl.G;  // k-steps of this warp per block
-  const int sp = ((warp >> 2) & 3) * nloc / 4;           // staggered production point
+  const int nloc = (kGR / 4 - grp + pl.G - 1) / pl.G;  // k-steps of this warp per block
   __syncthreads();
 
   // one k-step = 4 rows: operands (B: K g-values, t r*phi-values; A: products over the first p-1
@@ -332,18 +339,35 @@ fused_gram_kernel(const double* __restrict__ X, const double* __restrict__ y, do
       }
     }
   };
-  for (int n = 0; n < nblk; ++n) {
-    const double* cur = slabs + (n & 1) * (kRows * rl.bw);
-    kloop(cur, 0, sp);
-    if (n + 1 < nblk) {
-      produce(xn, n + 1, slabs + ((n + 1) & 1) * (kRows * rl.bw));
-      xn = n + 2 < nblk ? load_x(n + 2) : 0.0;
-    }
-    kloop(cur, sp, nloc);
-    for (int k = k0; k < k1; ++k)
-      if (g0 + n + 1 == sb(k + 1)) flush(k);
-    __syncthreads();
+#ifdef FAGP_GRAM_PROFILE
+  long long tp[4] = {0, 0, 0, 0};  // kloop, produce, flush, barrier (clock64 cycles)
+#define GPROF(i, stmt)              \
+  {                                 \
+    const long long t_ = clock64(); \
+    stmt;                           \
+    tp[i] += clock64() - t_;        \
   }
+#else
+#define GPROF(i, stmt) stmt;
+#endif
+  // Production of block n + 1 runs as its own phase at the top of block n, all warps together:
+  // overlapped with other warps' DMMAs its FP64 chains starve (DMUL and DMMA share one pipe and
+  // the dependent recurrence waits behind every DMMA), costing ~40% of each warp's time; alone it
+  // is ~1.5k cycles against ~22k of DMMA per block.
+  for (int n = 0; n < nblk; ++n) {
+    const double* cur = slabs + (n & 1) * (kGR * rl.bw);
+    if (n + 1 < nblk) {
+      GPROF(1, produce(pre, n + 1, slabs + ((n + 1) & 1) * (kGR * rl.bw)); if (n + 2 < nblk) load_pre(n + 2, pre))
+    }
+    GPROF(0, kloop(cur, 0, nloc))
+    GPROF(2, for (int k = k0; k < k1; ++k) if (g0 + n + 1 == sb(k + 1)) flush(k))
+    GPROF(3, __syncthreads())
+  }
+#ifdef FAGP_GRAM_PROFILE
+  if (lane == 0)
+    for (int i = 0; i < 4; ++i) atomicAdd(reinterpret_cast<unsigned long long*>(&g_gram_prof[i]), (unsigned long long)tp[i]);
+#endif
+#undef GPROF
   if (bad_x) raise_flag(flags, FAGP_FLAG_X_NONFINITE);
 }
 
@@ -395,7 +419,7 @@ constexpr int kGramShapes[][2] = {{1, 1}, {3, 1}, {4, 2}};
 // Plan for N rows; false when the shape needs the tiled table path.
 static bool make_gplan(int64_t N, int p, int M, GPlan& pl) {
   std::memset(&pl, 0, sizeof(pl));
-  if (!modal_on(p, M) || p > kMaxF || M > 12) return false;
+  if (!modal_on(p, M) || p > kMaxF || M > 12 || kGR * p > kGramNT) return false;
   pl.p = p;
   pl.M = M;
   pl.L = modal_L(M);
@@ -414,7 +438,7 @@ static bool make_gplan(int64_t N, int p, int M, GPlan& pl) {
     const int WG = kGramW / G;
     for (const auto& sh : kGramShapes) {
       if (WG * sh[0] < pl.kmf || WG * sh[1] < pl.tmf) continue;
-      const int cost = ((kRows / 4 + G - 1) / G) * (sh[0] * NFK + sh[1] * NFT);
+      const int cost = ((kGR / 4 + G - 1) / G) * (sh[0] * NFK + sh[1] * NFT);
       if (best < 0 || cost < best) {
         best = cost;
         pl.G = G;
@@ -429,24 +453,24 @@ static bool make_gplan(int64_t N, int p, int M, GPlan& pl) {
   pl.len = pl.Klen + int64_t(pl.TA) * pl.TB;
   pl.plen = (int64_t(pl.kmf) * NFK + int64_t(pl.tmf) * NFT) * 64;
   const RowLayout rl = row_layout(p, M);
-  const size_t smem = (size_t(2) * pl.LC + size_t(2) * kRows * rl.bw) * sizeof(double);
-  if (smem > 220 * 1024) return false;
+  const size_t smem = (size_t(2) * pl.LC + size_t(2) * kGR * rl.bw) * sizeof(double);
+  if (smem > 225 * 1024) return false;
   // rows: one CTA per SM, each a contiguous range of S sub-ranges (S = 4 once every sub-range
   // holds at least 4 blocks, so a host pipeline can upload sub-range k + 1 of every CTA while
   // the Gram contracts sub-range k)
-  const int64_t blocks = tmax<int64_t>(1, ceil_div(N, kRows));
+  const int64_t blocks = tmax<int64_t>(1, ceil_div(N, kGR));
   pl.grid = int(tmin<int64_t>(num_sms(), blocks));
   const int64_t bpc = ceil_div(blocks, pl.grid);  // blocks per CTA
   pl.S = bpc >= 8 ? 4 : 1;
   if (const char* e = getenv("FAGP_GRAM_SUBRANGES")) pl.S = tmax(1, tmin<int>(int(bpc), atoi(e)));  // tuning knob
-  pl.rows_per_cta = bpc * kRows;
+  pl.rows_per_cta = bpc * kGR;
   pl.grid = int(tmax<int64_t>(1, ceil_div(tmax<int64_t>(N, 1), pl.rows_per_cta)));
   pl.nparts = pl.grid * pl.S * pl.G;
   return true;
 }
 
 static size_t gram_smem(const GPlan& pl) {
-  return (size_t(2) * pl.LC + size_t(2) * kRows * row_layout(pl.p, pl.M).bw) * sizeof(double);
+  return (size_t(2) * pl.LC + size_t(2) * kGR * row_layout(pl.p, pl.M).bw) * sizeof(double);
 }
 
 template <int FA, int NFK, int NFT>
@@ -503,9 +527,9 @@ int upload_chunk(const double* Xh, const double* yh, int64_t N, int p, int M, in
     return FAGP_OK;
   }
   if (k < 0 || k >= pl.S) return FAGP_EINVAL;
-  const int64_t bpc = pl.rows_per_cta / kRows;
-  const int64_t off = (int64_t(k) * bpc / pl.S) * kRows;
-  const int64_t sub_rows = ((int64_t(k + 1) * bpc / pl.S) * kRows) - off;
+  const int64_t bpc = pl.rows_per_cta / kGR;
+  const int64_t off = (int64_t(k) * bpc / pl.S) * kGR;
+  const int64_t sub_rows = ((int64_t(k + 1) * bpc / pl.S) * kGR) - off;
   // CTAs c with c rpc + off + sub_rows <= N
   const int64_t head = N - off - sub_rows;
   const int64_t full = head < 0 ? 0 : tmin<int64_t>(pl.grid, head / pl.rows_per_cta + 1);
