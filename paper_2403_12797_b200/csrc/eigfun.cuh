@@ -9,6 +9,8 @@
 // an FMA: phi matches numpy's evaluation order bit for bit except for exp().
 #pragma once
 
+#include <cmath>
+
 #include "common.cuh"
 
 namespace fagp {
@@ -69,6 +71,62 @@ __device__ __forceinline__ void eval_g_dim(double x, const BasisView& b, int d, 
       out[(k + 1) * stride] = __dmul_rn(amp, hn);
       gm1 = h;
       h = hn;
+    }
+  }
+}
+
+// Recurrence coefficients c1[k] = sqrt(2/(k+1)), c2[k] = sqrt(k/(k+1)) computed on the host (IEEE
+// division and sqrt are correctly rounded: the same bits as herm_c1/herm_c2) and passed in the
+// kernel parameters, so a fully unrolled recurrence reads them as constant-bank operands: no
+// shared-memory load on the dependency chain.
+constexpr int kHermMax = 24;  // L = 2M - 1 <= 23 (M <= 12) on the fused path
+struct HermCoef {
+  double c1[kHermMax], c2[kHermMax];
+};
+
+inline HermCoef herm_coef_host() {
+  HermCoef h{};
+  for (int k = 0; k < kHermMax; ++k) {
+    h.c1[k] = std::sqrt(2.0 / double(k + 1));
+    h.c2[k] = std::sqrt(double(k) / double(k + 1));
+  }
+  return h;
+}
+
+// eval_phi_g_dim with the recurrence unrolled to kHermMax steps (guarded by M, L) and the
+// coefficients from `hc` (kernel parameters); identical operations and results.
+__device__ __forceinline__ void eval_phi_g_dim_u(double x, double r, const BasisView& b, int d, const HermCoef& hc,
+                                                 double* out_phi, double* out_g, double* out_rphi) {
+  const int M = b.M, L = modal_L(M);
+  const double zr = __dmul_rn(b.rho_beta()[d], x);
+  const double e1 = phi_exp(b, d, x);
+  const double env = __dmul_rn(b.sqrt_beta()[d], e1);
+  const double amp = g_amp(b, d, e1);
+  const double yz = __dmul_rn(zr, kSqrt2);
+  double hp = __dmul_rn(zr, kSqrt2), hpm = 1.0;
+  double hg = __dmul_rn(yz, kSqrt2), hgm = 1.0;
+  auto put_phi = [&](int k, double h) {
+    const double v = __dmul_rn(env, h);
+    out_phi[k] = v;
+    if (out_rphi) out_rphi[k] = __dmul_rn(r, v);
+  };
+  put_phi(0, 1.0);
+  out_g[0] = amp;
+  if (M > 1) put_phi(1, hp);
+  if (L > 1) out_g[1] = __dmul_rn(amp, hg);
+#pragma unroll
+  for (int k = 1; k < kHermMax - 1; ++k) {
+    if (k < L - 1) {
+      const double hgn = fma(__dmul_rn(yz, hc.c1[k]), hg, -__dmul_rn(hc.c2[k], hgm));
+      out_g[k + 1] = __dmul_rn(amp, hgn);
+      hgm = hg;
+      hg = hgn;
+      if (k < M - 1) {
+        const double hpn = __dsub_rn(__dmul_rn(__dmul_rn(zr, hc.c1[k]), hp), __dmul_rn(hc.c2[k], hpm));
+        put_phi(k + 1, hpn);
+        hpm = hp;
+        hp = hpn;
+      }
     }
   }
 }

@@ -60,53 +60,7 @@ __host__ __device__ inline RowLayout row_layout(int p, int M) {
 }
 
 constexpr int kRows = 64;      // rows per block (16 DMMA k-steps of 4 rows)
-constexpr int kProdWarps = 2;  // producer warps per CTA
 constexpr int kMaxF = 4;       // factors per generated column (p <= 4 on the fused path)
-
-// Producer (predict): rows [0, kRows) of `slab` <- basis of points row0 + i (i < nvalid; the
-// rest zero).  Each of the 64 producer threads owns P (row, dim) tasks and advances their
-// recurrences in lockstep (eval_multi): P independent FP64 chains per thread.
-template <int P>
-__device__ __forceinline__ void produce_rows(const double* __restrict__ X, int64_t row0, int nvalid,
-                                             const BasisView& b, const RowLayout& rl, const double* c1,
-                                             const double* c2, double* slab, int ptid, bool want_g, bool& bad_x) {
-  const int M = b.M, L = modal_L(M);
-  constexpr int NTH = kProdWarps * 32;
-  constexpr int tasks = kRows * P;
-  double xs[P];
-  int ds[P];
-  double* op[P];
-  double* og[P];
-#pragma unroll
-  for (int i = 0; i < P; ++i) {  // all loads first: one HBM round trip per block
-    const int t = ptid + i * NTH;
-    const int r = t / P, d = t - r * P;
-    const bool in = t < tasks, valid = in && r < nvalid;
-    xs[i] = valid ? X[row0 * P + t] : 0.0;
-    ds[i] = in ? d : 0;
-    double* row = slab + (in ? r : 0) * rl.bw;
-    op[i] = valid ? row + rl.poff + d * M : nullptr;
-    og[i] = (valid && want_g) ? row + rl.goff + d * L : nullptr;
-  }
-#pragma unroll
-  for (int i = 0; i < P; ++i) {
-    const int t = ptid + i * NTH;
-    const int r = t / P, d = t - r * P;
-    if (t < tasks && r < nvalid) {
-      bad_x |= not_finite(xs[i]);
-    } else if (t < tasks) {
-      double* row = slab + r * rl.bw;
-      for (int k = 0; k < M; ++k) row[rl.poff + d * M + k] = 0.0;
-      for (int k = 0; k < L; ++k) row[rl.goff + d * L + k] = 0.0;
-    }
-  }
-  eval_multi<P>(xs, ds, b, c1, c2, op, og, true, want_g);
-  for (int r = ptid; r < kRows; r += NTH) {
-    double* row = slab + r * rl.bw;
-    row[rl.one] = 1.0;
-    row[rl.zero] = 0.0;
-  }
-}
 
 // Offsets of the F factors of generated column `col` (< ncols valid): nd digits in `radix`
 // (first dimension slowest) over dims [d0, d0 + nd) of the section at `base`; slot nd takes
@@ -164,6 +118,7 @@ struct GPlan {
   int64_t rows_per_cta;  // multiple of kGR
   int S;                 // sub-ranges per CTA = chunks a host pipeline may launch separately
   int grid, nparts;      // nparts = grid * S * G partials
+  HermCoef hc;           // recurrence coefficients (constant-bank operands)
 };
 
 #ifdef FAGP_GRAM_PROFILE
@@ -221,8 +176,8 @@ fused_gram_kernel(const double* __restrict__ X, const double* __restrict__ y, do
     if (valid) {
       bad_x |= not_finite(pr.x);
       const double rr = __dsub_rn(pr.y, c);  // r = y - c (posterior.py:229)
-      eval_phi_g_dim(pr.x, rr, b, pdim, c1, c2, row + rl.poff + pdim * M, row + rl.goff + pdim * L,
-                     pdim == p - 1 ? row + rl.rpoff : nullptr);
+      eval_phi_g_dim_u(pr.x, rr, b, pdim, pl.hc, row + rl.poff + pdim * M, row + rl.goff + pdim * L,
+                       pdim == p - 1 ? row + rl.rpoff : nullptr);
     } else {
       for (int k = 0; k < M; ++k) row[rl.poff + pdim * M + k] = 0.0;
       for (int k = 0; k < L; ++k) row[rl.goff + pdim * L + k] = 0.0;
@@ -466,6 +421,7 @@ static bool make_gplan(int64_t N, int p, int M, GPlan& pl) {
   pl.rows_per_cta = bpc * kGR;
   pl.grid = int(tmax<int64_t>(1, ceil_div(tmax<int64_t>(N, 1), pl.rows_per_cta)));
   pl.nparts = pl.grid * pl.S * pl.G;
+  pl.hc = herm_coef_host();
   return true;
 }
 
@@ -577,13 +533,17 @@ int gram(const double* X, const double* y, double c, int64_t N, const fagp_basis
 }
 
 // ---------------------------------------------------------------------------------------
-// Fused predict (variance + mean).  8 consumer warps = 2 row groups (32 rows = 4 m-fragments)
-// x 4 K-quarters, plus 2 producer warps.  The variance and mean epilogues are linear in the
-// GEMM outputs, so every warp applies them to its own K-quarter partial (g / phi products
-// gathered from the row slab, 4-lane shuffle reduction) and only one scalar per row and
-// quarter meets in shared memory; the quarters are summed in fixed order.
-constexpr int kPredCW = 8;
-constexpr int kPredNT = (kPredCW + kProdWarps) * 32;  // 320 threads
+// Fused predict (variance + mean).  16 warps = 4 row groups (16 rows = 2 m-fragments) x 4
+// K-quarters.  Each 64-row block starts with a production phase in which all warps evaluate
+// phi and g of the NEXT block (one (row, dim) per thread; kept apart from the DMMA phase, where
+// the dependent FP64 chains would starve behind the shared pipe); then the DMMA phase on the
+// current block.  The variance and mean epilogues are linear in the GEMM outputs, so every warp
+// applies them to its own K-quarter partial (g / phi products gathered from the row slab, 4-lane
+// shuffle reduction) and only one scalar per row and quarter meets in shared memory; the
+// quarters are summed in fixed order.
+constexpr int kPredW = 16;
+constexpr int kPredNT = kPredW * 32;  // 512 threads
+constexpr int kPMF = 2;               // m-fragments per warp
 
 struct VPlan {
   int p, M, L, LC;
@@ -594,6 +554,7 @@ struct VPlan {
   int64_t nblocks;
   int grid;
   size_t smem;
+  HermCoef hc;           // recurrence coefficients (constant-bank operands)
 };
 
 // byte-packed factor offsets of K column kappa (F factors, 8 bits each; offsets < 256)
@@ -608,55 +569,58 @@ __device__ __forceinline__ void unpack_off(uint32_t v, int (&off)[F]) {
 // fragment-major operand.  Software-pipelined: the operands of k-step ks + 1 are loaded and
 // multiplied in program order before the DMMAs of k-step ks, so they overlap.
 template <int F, int NF>
-__device__ __forceinline__ void contract4(const double* row0, int bw, const uint32_t* offs, const double* B, int k0,
-                                          int k1, int lane, double (&acc)[4][NF][2]) {
+__device__ __forceinline__ void contract(const double* row0, int bw, const uint32_t* offs, const double* B, int k0,
+                                         int k1, int lane, double (&acc)[kPMF][NF][2]) {
   if (k0 >= k1) return;
-  auto load = [&](int ks, double (&ao)[4], double (&bo)[NF]) {
+  auto load = [&](int ks, double (&ao)[kPMF], double (&bo)[NF]) {
     int off[F];
     unpack_off<F>(offs[4 * ks + (lane & 3)], off);
 #pragma unroll
-    for (int f = 0; f < 4; ++f) ao[f] = gather_prod<F>(row0 + 8 * f * bw, off);
+    for (int f = 0; f < kPMF; ++f) ao[f] = gather_prod<F>(row0 + 8 * f * bw, off);
 #pragma unroll
     for (int nf = 0; nf < NF; ++nf) bo[nf] = B[(ks * NF + nf) * 32 + lane];
   };
-  double a[4], bb[NF];
+  double a[kPMF], bb[NF];
   load(k0, a, bb);
   for (int ks = k0; ks < k1; ++ks) {
-    double an[4], bn[NF];
+    double an[kPMF], bn[NF];
     load(ks + 1 < k1 ? ks + 1 : ks, an, bn);
 #pragma unroll
-    for (int f = 0; f < 4; ++f)
+    for (int f = 0; f < kPMF; ++f)
 #pragma unroll
       for (int nf = 0; nf < NF; ++nf) dmma_8x8x4(acc[f][nf][0], acc[f][nf][1], a[f], bb[nf]);
 #pragma unroll
-    for (int f = 0; f < 4; ++f) a[f] = an[f];
+    for (int f = 0; f < kPMF; ++f) a[f] = an[f];
 #pragma unroll
     for (int nf = 0; nf < NF; ++nf) bb[nf] = bn[nf];
   }
 }
+
+#ifdef FAGP_GRAM_PROFILE
+__device__ long long g_pred_prof[4];
+extern "C" int fagp_debug_pred_profile(long long* out) {  // diagnostics build only
+  return cudaMemcpyFromSymbol(out, g_pred_prof, sizeof(g_pred_prof)) == cudaSuccess ? 0 : 5;
+}
+#endif
 
 template <int FK, int FE, int FKM, int NFV, int NFM>
 __global__ void __launch_bounds__(kPredNT, 1)
 fused_predict_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView b, const VPlan pl,
                      const double* __restrict__ op, double sigma2, double c, double* __restrict__ mean,
                      double* __restrict__ var, uint32_t* flags) {
+  constexpr int P = FK + FE;
   extern __shared__ double sm[];
   const RowLayout rl = row_layout(pl.p, pl.M);
   const bool want_var = var != nullptr;
-  double* c1 = sm;
-  double* c2 = sm + pl.LC;
-  double* Bv = c2 + pl.LC;                   // [vks][NFV][32]
+  double* Bv = sm;                           // [vks][NFV][32]
   double* Bm = Bv + pl.vks * NFV * 32;       // [mks][NFM][32]
-  double* red = Bm + pl.mks * NFM * 32;      // [4 quarters][kRows][2 (var, mean)]
-  double* slabs = red + 4 * kRows * 2;       // [2][kRows * bw]
+  double* reds = Bm + pl.mks * NFM * 32;     // [2 (block parity)][4 quarters][kRows][2 (var, mean)]
+  double* slabs = reds + 2 * 4 * kRows * 2;  // [2][kRows * bw]
   uint32_t* offV = reinterpret_cast<uint32_t*>(slabs + 2 * kRows * rl.bw);  // [vks * 4]
   uint32_t* offM = offV + pl.vks * 4;                                       // [mks * 4]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int M = pl.M, L = pl.L;
   const double* w = op + pl.KP * pl.NP;
-  for (int k = tid; k < pl.LC; k += kPredNT) {
-    c1[k] = herm_c1(k);
-    c2[k] = herm_c2(k);
-  }
   // operands, fragment-major: B[ks][nf][lane] = Op[4 ks + (lane & 3)][8 nf + (lane >> 2)]
   if (want_var)
     for (int i = tid; i < pl.vks * NFV * 32; i += kPredNT) {
@@ -686,17 +650,36 @@ fused_predict_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView b, con
     for (int f = 0; f < FKM; ++f) v |= uint32_t(off[f]) << (8 * f);
     offM[kap] = v;
   }
-  const bool producer = warp >= kPredCW;
-  const int ptid = tid - kPredCW * 32;
   bool bad_x = false, bad = false;
-  __syncthreads();
+  // production: thread t < 64 P evaluates phi and g of row t / P, dimension t % P
+  const bool plane = tid < kRows * P;
+  const int prow = tid / P, pdim = tid - (tid / P) * P;
+  auto load_x = [&](int64_t blk) -> double {
+    const int64_t r = blk * kRows + prow;
+    return (plane && blk < pl.nblocks && r < Ns) ? Xs[r * P + pdim] : 0.0;
+  };
+  auto produce = [&](double x, int64_t blk, double* slab) {
+    if (!plane) return;
+    double* row = slab + prow * rl.bw;
+    if (blk * kRows + prow < Ns) {
+      bad_x |= not_finite(x);
+      eval_phi_g_dim_u(x, 0.0, b, pdim, pl.hc, row + rl.poff + pdim * M, row + rl.goff + pdim * L, nullptr);
+    } else {
+      for (int k = 0; k < M; ++k) row[rl.poff + pdim * M + k] = 0.0;
+      for (int k = 0; k < L; ++k) row[rl.goff + pdim * L + k] = 0.0;
+    }
+    if (pdim == 0) {
+      row[rl.one] = 1.0;
+      row[rl.zero] = 0.0;
+    }
+  };
   const int64_t blk0 = blockIdx.x, stride = gridDim.x;
-  if (producer && blk0 < pl.nblocks) {
-    const int64_t rr = blk0 * kRows;
-    produce_rows<FK + FE>(Xs, rr, int(tmin<int64_t>(kRows, Ns - rr)), b, rl, c1, c2, slabs, ptid, want_var, bad_x);
-  }
-  // consumer roles: rows [32 mg, 32 mg + 32), K-quarter kq
-  const int mg = warp & 1, kq = (warp >> 1) & 3;
+  __syncthreads();
+  double xn = load_x(blk0);
+  if (blk0 < pl.nblocks) produce(xn, blk0, slabs);
+  xn = load_x(blk0 + stride);
+  // consumer roles: rows [16 mg, 16 mg + 16), K-quarter kq
+  const int mg = warp & 3, kq = warp >> 2;
   const int v0 = kq * pl.vks / 4, v1 = (kq + 1) * pl.vks / 4;
   const int m0 = kq * pl.mks / 4, m1 = (kq + 1) * pl.mks / 4;
   // epilogue factor offsets: variance E[i, nu] = prod_{d < pN} g_d; mean phi_0[i, nu]
@@ -715,76 +698,97 @@ fused_predict_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView b, con
     }
   __syncthreads();
 
+#ifdef FAGP_GRAM_PROFILE
+  long long tp[4] = {0, 0, 0, 0};  // produce, contract, epilogue+final, barrier (clock64 cycles)
+  long long t_ = clock64();
+#define PPROF(i)                    \
+  {                                 \
+    const long long n_ = clock64(); \
+    tp[i] += n_ - t_;               \
+    t_ = n_;                        \
+  }
+#else
+#define PPROF(i)
+#endif
   int it = 0;
   for (int64_t blk = blk0; blk < pl.nblocks; blk += stride, ++it) {
     const double* cur = slabs + (it & 1) * (kRows * rl.bw);
-    if (producer) {
-      const int64_t nb = blk + stride;
-      if (nb < pl.nblocks) {
-        const int64_t rr = nb * kRows;
-        produce_rows<FK + FE>(Xs, rr, int(tmin<int64_t>(kRows, Ns - rr)), b, rl, c1, c2,
-                              slabs + ((it + 1) & 1) * (kRows * rl.bw), ptid, want_var, bad_x);
+    double* red = reds + (it & 1) * (4 * kRows * 2);
+    // production phase: the next block
+    if (blk + stride < pl.nblocks) {
+      produce(xn, blk + stride, slabs + ((it + 1) & 1) * (kRows * rl.bw));
+      xn = load_x(blk + 2 * stride);
+    }
+    PPROF(0)
+    // DMMA phase
+    const double* row0 = cur + (mg * 16 + (lane >> 2)) * rl.bw;  // m-fragment f: + 8 f rows
+    double accV[kPMF][NFV][2], accM[kPMF][NFM][2];
+#pragma unroll
+    for (int f = 0; f < kPMF; ++f) {
+#pragma unroll
+      for (int nf = 0; nf < NFV; ++nf) accV[f][nf][0] = accV[f][nf][1] = 0.0;
+#pragma unroll
+      for (int nf = 0; nf < NFM; ++nf) accM[f][nf][0] = accM[f][nf][1] = 0.0;
+    }
+    if (want_var) contract<FK, NFV>(row0, rl.bw, offV, Bv, v0, v1, lane, accV);
+    contract<FKM, NFM>(row0, rl.bw, offM, Bm, m0, m1, lane, accM);
+    PPROF(1)
+    // this quarter's epilogue contribution per row: sum_nu Y[i, nu] E[i, nu] (var),
+    // sum_nu Z[i, nu] phi_0[i, nu] (mean); the 4 lanes of a row hold disjoint columns
+#pragma unroll
+    for (int f = 0; f < kPMF; ++f) {
+      const double* row = row0 + 8 * f * rl.bw;
+      double vs = 0.0, ms = 0.0;
+#pragma unroll
+      for (int nf = 0; nf < NFV; ++nf)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (want_var) vs = fma(accV[f][nf][e], gather_prod<FE>(row, offE[nf][e]), vs);
+#pragma unroll
+      for (int nf = 0; nf < NFM; ++nf)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) ms = fma(accM[f][nf][e], row[offEm[nf][e]], ms);
+      vs += __shfl_xor_sync(0xffffffffu, vs, 1);
+      vs += __shfl_xor_sync(0xffffffffu, vs, 2);
+      ms += __shfl_xor_sync(0xffffffffu, ms, 1);
+      ms += __shfl_xor_sync(0xffffffffu, ms, 2);
+      if ((lane & 3) == 0) {
+        const int r = mg * 16 + 8 * f + (lane >> 2);
+        red[(kq * kRows + r) * 2 + 0] = vs;
+        red[(kq * kRows + r) * 2 + 1] = ms;
       }
-    } else {
-      const double* row0 = cur + (mg * 32 + (lane >> 2)) * rl.bw;  // m-fragment f: + 8 f rows
-      double accV[4][NFV][2], accM[4][NFM][2];
+    }
+    PPROF(2)
+    __syncthreads();
+    PPROF(3)
+    if (tid < kRows) {
+      const int64_t row_i = blk * kRows + tid;
+      if (row_i < Ns) {
+        double vs = red[tid * 2], ms = red[tid * 2 + 1];
 #pragma unroll
-      for (int f = 0; f < 4; ++f) {
-#pragma unroll
-        for (int nf = 0; nf < NFV; ++nf) accV[f][nf][0] = accV[f][nf][1] = 0.0;
-#pragma unroll
-        for (int nf = 0; nf < NFM; ++nf) accM[f][nf][0] = accM[f][nf][1] = 0.0;
-      }
-      if (want_var) contract4<FK, NFV>(row0, rl.bw, offV, Bv, v0, v1, lane, accV);
-      contract4<FKM, NFM>(row0, rl.bw, offM, Bm, m0, m1, lane, accM);
-      // this quarter's epilogue contribution per row: sum_nu Y[i, nu] E[i, nu] (var),
-      // sum_nu Z[i, nu] phi_0[i, nu] (mean); the 4 lanes of a row hold disjoint columns
-#pragma unroll
-      for (int f = 0; f < 4; ++f) {
-        const double* row = row0 + 8 * f * rl.bw;
-        double vs = 0.0, ms = 0.0;
-#pragma unroll
-        for (int nf = 0; nf < NFV; ++nf)
-#pragma unroll
-          for (int e = 0; e < 2; ++e)
-            if (want_var) vs = fma(accV[f][nf][e], gather_prod<FE>(row, offE[nf][e]), vs);
-#pragma unroll
-        for (int nf = 0; nf < NFM; ++nf)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) ms = fma(accM[f][nf][e], row[offEm[nf][e]], ms);
-        vs += __shfl_xor_sync(0xffffffffu, vs, 1);
-        vs += __shfl_xor_sync(0xffffffffu, vs, 2);
-        ms += __shfl_xor_sync(0xffffffffu, ms, 1);
-        ms += __shfl_xor_sync(0xffffffffu, ms, 2);
-        if ((lane & 3) == 0) {
-          const int r = mg * 32 + 8 * f + (lane >> 2);
-          red[(kq * kRows + r) * 2 + 0] = vs;
-          red[(kq * kRows + r) * 2 + 1] = ms;
+        for (int q = 1; q < 4; ++q) {
+          vs += red[(q * kRows + tid) * 2];
+          ms += red[(q * kRows + tid) * 2 + 1];
         }
-      }
-      asm volatile("bar.sync 1, %0;\n" ::"n"(kPredCW * 32));
-      if (tid < kRows) {
-        const int64_t row_i = blk * kRows + tid;
-        if (row_i < Ns) {
-          double vs = red[tid * 2], ms = red[tid * 2 + 1];
-#pragma unroll
-          for (int q = 1; q < 4; ++q) {
-            vs += red[(q * kRows + tid) * 2];
-            ms += red[(q * kRows + tid) * 2 + 1];
-          }
-          const double mm = c + ms;  // posterior.py:247
-          mean[row_i] = mm;
-          bad |= not_finite(mm);
-          if (want_var) {
-            const double vv = sigma2 * vs;
-            var[row_i] = vv;
-            bad |= not_finite(vv);
-          }
+        const double mm = c + ms;  // posterior.py:247
+        mean[row_i] = mm;
+        bad |= not_finite(mm);
+        if (want_var) {
+          const double vv = sigma2 * vs;
+          var[row_i] = vv;
+          bad |= not_finite(vv);
         }
       }
     }
-    __syncthreads();
+    // red is double-buffered and the slab written next was last read before the barrier above:
+    // one barrier per block
+    PPROF(2)
   }
+#ifdef FAGP_GRAM_PROFILE
+  if (lane == 0)
+    for (int i = 0; i < 4; ++i) atomicAdd(reinterpret_cast<unsigned long long*>(&g_pred_prof[i]), (unsigned long long)tp[i]);
+#endif
+#undef PPROF
   if (bad_x) raise_flag(flags, FAGP_FLAG_X_NONFINITE);
   if (bad) raise_flag(flags, FAGP_FLAG_PHI_NONFINITE);
 }
@@ -811,12 +815,13 @@ static bool make_vplan(int64_t Ns, int p, int M, VPlan& pl) {
   const int NFM = M <= 8 ? 1 : 2;
   const RowLayout rl = row_layout(p, M);
   if (rl.bw > 256) return false;  // byte-packed offsets
-  pl.smem = (size_t(2) * pl.LC + size_t(pl.vks) * NFV * 32 + size_t(pl.mks) * NFM * 32 + size_t(4) * kRows * 2 +
+  pl.smem = (size_t(pl.vks) * NFV * 32 + size_t(pl.mks) * NFM * 32 + size_t(2 * 4) * kRows * 2 +
              size_t(2) * kRows * rl.bw) * sizeof(double) +
             size_t(pl.vks + pl.mks) * 4 * sizeof(uint32_t);
   if (pl.smem > 225 * 1024) return false;
   pl.nblocks = ceil_div(tmax<int64_t>(Ns, 0), kRows);
   pl.grid = int(tmax<int64_t>(1, tmin<int64_t>(num_sms(), pl.nblocks)));
+  pl.hc = herm_coef_host();
   return true;
 }
 

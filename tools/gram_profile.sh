@@ -28,5 +28,16 @@ gram_x_packed(basis, X, y, 0.0); torch.cuda.synchronize()
 L.fagp_debug_gram_profile(out)
 v = [a - b for a, b in zip(out, base)]
 tot = sum(v)
-print("warp-cycles share: kloop %.3f produce %.3f flush %.3f barrier %.3f  (total %.3g per warp)" % tuple([x / tot for x in v] + [tot / (148 * 16)]))
+print("gram warp-cycles share: kloop %.3f produce %.3f flush %.3f barrier %.3f  (total %.3g per warp)" % tuple([x / tot for x in v] + [tot / (148 * 16)]))
+from paper_2403_12797_b200.posterior import factor_packed, predict_x_device
+from paper_2403_12797_b200.datagen import test_inputs
+packed = gram_x_packed(basis, X, y, 0.0)
+f, st, _ = factor_packed(basis, packed, 0.0025, 0.0, 1_000_000)
+Xs = torch.from_numpy(test_inputs(1_000_000, 3)).cuda()
+L.fagp_debug_pred_profile(out); base = list(out)
+predict_x_device(f, Xs); torch.cuda.synchronize()
+L.fagp_debug_pred_profile(out)
+v = [a - b for a, b in zip(out, base)]
+tot = sum(v)
+print("predict warp-cycles share: produce %.3f contract %.3f epilogue+final %.3f barrier %.3f  (total %.3g per warp)" % tuple([x / tot for x in v] + [tot / (148 * 16)]))
 PY
