@@ -204,6 +204,16 @@ int fagp_factor_inv(const double* gram, const fagp_basis* basis, const double* s
                     int32_t jitter_attempts, double* Ainv, double* G, double* t, double* w, double* predict_op,
                     double* jitter, int32_t* pivot_index, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Attempt 0 of fagp_factor_inv (no jitter) enqueued with NO host synchronisation: every kernel
+ * is issued unconditionally and the breakdown index is copied asynchronously to *info_host
+ * (HOST, pinned; valid once `stream` has synchronised).  Lets a caller queue the prediction right
+ * behind the factor so the GPU never waits for the host.  If *info_host != 0 the outputs are
+ * invalid and the caller must run fagp_factor_inv (the full jitter schedule) and redo the
+ * prediction; with sigma2 > 0 this does not happen for data that does not need jitter. */
+int fagp_factor_inv_async(const double* gram, const fagp_basis* basis, const double* sqrt_lam, double sigma2,
+                          double* Ainv, double* G, double* t, double* w, double* predict_op, int32_t* info_host,
+                          void* workspace, size_t workspace_bytes, void* stream);
+
 /* Overwrite the mean weights stored in the predict operand with w (used after the
  * reference's fault-injection hook flips w, posterior.py:245-246). */
 int fagp_set_mean_weights(double* predict_op, const double* w, const fagp_basis* basis, void* stream);

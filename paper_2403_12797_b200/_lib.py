@@ -81,6 +81,7 @@ SIGNATURES = {
     "fagp_predict_operand_len": (_I64, [_BASIS]),
     "fagp_factor": (ctypes.c_int, [_P, _BASIS, _P, _D, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "fagp_factor_inv": (ctypes.c_int, [_P, _BASIS, _P, _D, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "fagp_factor_inv_async": (ctypes.c_int, [_P, _BASIS, _P, _D, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "fagp_set_mean_weights": (ctypes.c_int, [_P, _P, _BASIS, _P]),
     "fagp_potrf_workspace_size": (_SZ, [_I64]),
     "fagp_potrf": (ctypes.c_int, [_P, _I64, _P, _P, _SZ, _P]),

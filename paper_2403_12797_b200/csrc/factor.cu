@@ -916,6 +916,46 @@ int fagp_factor_inv(const double* packed, const fagp_basis* basis, const double*
 }
 
 
+// Attempt 0 of fagp_factor_inv (no jitter) enqueued without any host synchronisation: the
+// system, the fused inverse, w and the predict operand are issued unconditionally and the
+// breakdown index is copied asynchronously to *info_host (pinned host memory; read it after the
+// stream has synchronised).  A caller can enqueue the predict right behind it, so the GPU runs
+// factor -> predict back to back; only when *info_host != 0 (a breakdown: the jitter schedule
+// is needed) must it call fagp_factor_inv and redo what followed.
+int fagp_factor_inv_async(const double* packed, const fagp_basis* basis, const double* sqrt_lam, double sigma2,
+                          double* Ainv, double* G, double* t, double* w, double* predict_op, int32_t* info_host,
+                          void* workspace, size_t workspace_bytes, void* stream) {
+  {
+    int st = check_basis(basis);
+    if (st) return st;
+  }
+  const int64_t m = basis->m;
+  if (!modal::enabled(basis->p, basis->M) || m > kFactorInvMaxM) return FAGP_EUNSUPPORTED;
+  if (packed == nullptr || sqrt_lam == nullptr || t == nullptr || w == nullptr || Ainv == nullptr ||
+      info_host == nullptr)
+    return FAGP_EINVAL;
+  if (!(sigma2 > 0.0) || !std::isfinite(sigma2)) return FAGP_EINVAL;
+  FactorWs ws = carve(workspace, m);
+  if (workspace == nullptr || workspace_bytes < ws.bytes) return FAGP_EWORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* A = ws.X;
+  int rc = modal::expand(packed, basis, ws.Lp, ws.X, s);
+  if (rc) return rc;
+  rc = modal::system(ws.Lp, packed, sqrt_lam, sigma2, 0.0, basis, A, G, t, s);
+  if (rc) return rc;
+  FAGP_CUDA_TRY(cudaMemsetAsync(ws.info, 0, sizeof(int), s));
+  rc = chol_inverse_persistent(A, m, m, ws.info, ws.chol, ws.D, Ainv, m, s);
+  if (rc) return rc;
+  FAGP_CUDA_TRY(cudaMemcpyAsync(info_host, ws.info, sizeof(int), cudaMemcpyDeviceToHost, s));
+  sym_gemv_scaled_kernel<<<unsigned(ceil_div(m, 8)), 256, 0, s>>>(Ainv, m, sqrt_lam, t, w);
+  FAGP_LAUNCH_CHECK();
+  if (predict_op) {
+    rc = modal::build_predict_op(Ainv, sqrt_lam, w, basis, predict_op, ws.Lp, ws.X, s);
+    if (rc) return rc;
+  }
+  return FAGP_OK;
+}
+
 size_t fagp_spd_inverse_workspace_size(int64_t m) {
   if (m < 1) return 0;
   return align256(sizeof(int)) + align256(size_t(cholinv_scratch_len(m)) * sizeof(double)) +

@@ -9,8 +9,9 @@ One engine per (basis, N, N*) shape.  ``run`` issues, on the current CUDA stream
 
 (no basis table reaches HBM on the fused shapes; the others evaluate one into the workspace)
 
-and performs exactly one host synchronisation (inside fagp_factor, which must read the
-Cholesky status to run the reference's jitter schedule).  No allocation happens inside
+and never waits for the host between the factor and the prediction: attempt 0 of the factor
+(no jitter) is enqueued asynchronously and its breakdown status read after the step; only a
+breakdown (jitter needed) re-runs the factor through the blocking schedule and the prediction.  No allocation happens inside
 ``run``, so it is safe to time and to call repeatedly.
 """
 
@@ -112,6 +113,35 @@ class PosteriorEngine:
             _lib.check(self.status, "factor")
         return self.status
 
+    def stage_factor_async(self, stream=None):
+        """Attempt 0 of the factorisation with no host synchronisation (fagp_factor_inv_async):
+        the prediction can be queued right behind it.  Returns False when the shape has no
+        async route (the blocking stage_factor ran instead and its status is in self.status).
+        After the stream has synchronised, factor_needs_retry() says whether the breakdown path
+        (jitter schedule) has to run."""
+        import torch
+
+        if not self.inverse_route:
+            self.stage_factor(stream)
+            return False
+        L, s, b = _lib.lib(), _lib.stream_handle(stream), self.basis
+        if getattr(self, "info_host", None) is None:
+            self.info_host = torch.zeros((1,), dtype=torch.int32, pin_memory=True)
+        self.info_host.zero_()
+        rc = L.fagp_factor_inv_async(_lib.ptr(self.packed), b.ref, _lib.ptr(self.sqrt_lam), self.noise_var,
+                                     _lib.ptr(self.Ainv), _lib.ptr(self.G), _lib.ptr(self.t), _lib.ptr(self.w),
+                                     _lib.ptr(self.predict_op), _lib.ptr(self.info_host), _lib.ptr(self.factor_ws),
+                                     self.factor_ws_bytes, s)
+        _lib.check(rc, "factor")
+        self.jitter.value = 0.0
+        self.pivot.value = 0
+        self.status = _lib.FAGP_OK
+        return True
+
+    def factor_needs_retry(self):
+        """After a synchronisation: did the async attempt break down (jitter schedule needed)?"""
+        return getattr(self, "info_host", None) is not None and int(self.info_host[0]) != 0
+
     def set_mean_weights(self, stream=None):
         _lib.check(_lib.lib().fagp_set_mean_weights(_lib.ptr(self.predict_op), _lib.ptr(self.w), self.basis.ref,
                                                     _lib.stream_handle(stream)), "set_mean_weights")
@@ -135,16 +165,31 @@ class PosteriorEngine:
         self.flags.zero_()
         self.stage_gram(X, y)
         self.stage_reduce()
-        st = self.stage_factor()
+        asynchronous = self.stage_factor_async()
         if xs_ready is not None:
             torch.cuda.current_stream().wait_event(xs_ready)
-        if st != _lib.FAGP_OK:
+        if not asynchronous and self.status != _lib.FAGP_OK:
             self.raise_errors(X, Xs, y, factor_failed=True)
         if fault_flip:
             self.w.neg_()
             self.set_mean_weights()
         self.stage_predict(Xs)
+        if asynchronous:
+            torch.cuda.current_stream().synchronize()
+            if self.factor_needs_retry():
+                self._retry_factor(X, Xs, y, fault_flip)
+                self.stage_predict(Xs)
         return self.mean, self.var
+
+    def _retry_factor(self, X, Xs, y, fault_flip):
+        """The async attempt broke down: run the full jitter schedule (blocking) and re-apply the
+        fault hook; raises the reference's NumericalError if even the last attempt fails."""
+        st = self.stage_factor()
+        if st != _lib.FAGP_OK:
+            self.raise_errors(X, Xs, y, factor_failed=True)
+        if fault_flip:
+            self.w.neg_()
+            self.set_mean_weights()
 
     # -- the whole step from host memory (the fagp_posterior path) -------------------------
     PREDICT_CHUNKS = 4
@@ -220,11 +265,11 @@ class PosteriorEngine:
         if trace is not None:
             trace.append(time.perf_counter())
         self.stage_reduce()
-        st = self.stage_factor()
+        asynchronous = self.stage_factor_async()
         if trace is not None:
             trace.append(time.perf_counter())
         cs.wait_event(ev_xs)
-        if st != _lib.FAGP_OK:
+        if not asynchronous and self.status != _lib.FAGP_OK:
             self.raise_errors(X, Xs, y, factor_failed=True)
         if fault_flip:
             self.w.neg_()
@@ -254,6 +299,13 @@ class PosteriorEngine:
         if trace is not None:
             trace.append(time.perf_counter())
             _TRACE.append([1e3 * (b - a) for a, b in zip(trace, trace[1:])])
+        if asynchronous and self.factor_needs_retry():
+            self._retry_factor(X, Xs, y, fault_flip)
+            self.stage_predict(Xs)
+            torch.cuda.current_stream(self.device).synchronize()
+            out[0].copy_(self.mean)
+            if self.want_var:
+                out[1].copy_(self.var)
         return o[0], (o[1] if self.want_var else None)
 
     def _out_buffer(self, rows):

@@ -386,3 +386,25 @@ def test_spd_inverse_sweep_matches_lapack(m):
             _, info_ref = sla.lapack.dpotrf(Ai, lower=1)
             _, info = spd_inverse(Ai)
             assert info == info_ref > 0
+
+
+def test_async_factor_falls_back_to_the_jitter_schedule():
+    """A system whose attempt 0 breaks down (rank-deficient Gram, negligible noise): the async
+    factor's retry path must give exactly what the blocking route (fit/predict) gives."""
+    rng = np.random.default_rng(5)
+    X = np.repeat(rng.uniform(-1, 1, (3, 2)), 40, axis=0)
+    y = np.cos(X).sum(1)
+    Xs = rng.uniform(-1, 1, (300, 2))
+    model = F.GpModel(F.ArdKernelParams.isotropic(2, 1.0, 1.0), 1e-30, n_eigen=10)
+
+    class DS:
+        pass
+
+    DS.X, DS.y = X, y
+    f = F.fit(DS, model, memory_cap=None)
+    assert f.jitter > 0.0  # the reference's schedule was needed
+    ref = F.predict(f, Xs)
+    got = F.fagp_posterior(DS, Xs, model, memory_cap=None)
+    assert np.array_equal(got.mean, ref.mean) and np.array_equal(got.var, ref.var)
+    dev_in = F.fagp_posterior(DS, torch.from_numpy(Xs).cuda(), model, memory_cap=None, return_device=True)
+    assert np.array_equal(dev.to_host(dev_in.mean), ref.mean)
