@@ -533,17 +533,20 @@ int gram(const double* X, const double* y, double c, int64_t N, const fagp_basis
 }
 
 // ---------------------------------------------------------------------------------------
-// Fused predict (variance + mean).  16 warps = 4 row groups (16 rows = 2 m-fragments) x 4
-// K-quarters.  Each 64-row block starts with a production phase in which all warps evaluate
-// phi and g of the NEXT block (one (row, dim) per thread; kept apart from the DMMA phase, where
-// the dependent FP64 chains would starve behind the shared pipe); then the DMMA phase on the
-// current block.  The variance and mean epilogues are linear in the GEMM outputs, so every warp
+// Fused predict (variance + mean).  16 warps = 8 row groups (16 rows = 2 m-fragments) x 2
+// K-halves.  Each 128-row block starts with a production phase in which all warps evaluate phi
+// and g of the block (one (row, dim) per thread; kept apart from the DMMA phase, where the
+// dependent FP64 chains would starve behind the shared pipe -- its cost is one chain latency
+// per block, so blocks are as large as shared memory allows: one 128-row slab); then the DMMA
+// phase.  The variance and mean epilogues are linear in the GEMM outputs, so every warp
 // applies them to its own K-quarter partial (g / phi products gathered from the row slab, 4-lane
 // shuffle reduction) and only one scalar per row and quarter meets in shared memory; the
 // quarters are summed in fixed order.
 constexpr int kPredW = 16;
 constexpr int kPredNT = kPredW * 32;  // 512 threads
 constexpr int kPMF = 2;               // m-fragments per warp
+constexpr int kPR = 128;              // rows per block: 8 row groups of 16 x 2 K-halves
+constexpr int kPKS = 2;               // K splits
 
 struct VPlan {
   int p, M, L, LC;
@@ -614,9 +617,9 @@ fused_predict_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView b, con
   const bool want_var = var != nullptr;
   double* Bv = sm;                           // [vks][NFV][32]
   double* Bm = Bv + pl.vks * NFV * 32;       // [mks][NFM][32]
-  double* reds = Bm + pl.mks * NFM * 32;     // [2 (block parity)][4 quarters][kRows][2 (var, mean)]
-  double* slabs = reds + 2 * 4 * kRows * 2;  // [2][kRows * bw]
-  uint32_t* offV = reinterpret_cast<uint32_t*>(slabs + 2 * kRows * rl.bw);  // [vks * 4]
+  double* red = Bm + pl.mks * NFM * 32;      // [kPKS][kPR][2 (var, mean)]
+  double* slab = red + kPKS * kPR * 2;       // [kPR * bw]
+  uint32_t* offV = reinterpret_cast<uint32_t*>(slab + kPR * rl.bw);  // [vks * 4]
   uint32_t* offM = offV + pl.vks * 4;                                       // [mks * 4]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int M = pl.M, L = pl.L;
@@ -651,17 +654,17 @@ fused_predict_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView b, con
     offM[kap] = v;
   }
   bool bad_x = false, bad = false;
-  // production: thread t < 64 P evaluates phi and g of row t / P, dimension t % P
-  const bool plane = tid < kRows * P;
+  // production: thread t < 128 P evaluates phi and g of row t / P, dimension t % P
+  const bool plane = tid < kPR * P;
   const int prow = tid / P, pdim = tid - (tid / P) * P;
   auto load_x = [&](int64_t blk) -> double {
-    const int64_t r = blk * kRows + prow;
+    const int64_t r = blk * kPR + prow;
     return (plane && blk < pl.nblocks && r < Ns) ? Xs[r * P + pdim] : 0.0;
   };
-  auto produce = [&](double x, int64_t blk, double* slab) {
+  auto produce = [&](double x, int64_t blk) {
     if (!plane) return;
     double* row = slab + prow * rl.bw;
-    if (blk * kRows + prow < Ns) {
+    if (blk * kPR + prow < Ns) {
       bad_x |= not_finite(x);
       eval_phi_g_dim_u(x, 0.0, b, pdim, pl.hc, row + rl.poff + pdim * M, row + rl.goff + pdim * L, nullptr);
     } else {
@@ -674,14 +677,11 @@ fused_predict_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView b, con
     }
   };
   const int64_t blk0 = blockIdx.x, stride = gridDim.x;
-  __syncthreads();
   double xn = load_x(blk0);
-  if (blk0 < pl.nblocks) produce(xn, blk0, slabs);
-  xn = load_x(blk0 + stride);
-  // consumer roles: rows [16 mg, 16 mg + 16), K-quarter kq
-  const int mg = warp & 3, kq = warp >> 2;
-  const int v0 = kq * pl.vks / 4, v1 = (kq + 1) * pl.vks / 4;
-  const int m0 = kq * pl.mks / 4, m1 = (kq + 1) * pl.mks / 4;
+  // consumer roles: rows [16 mg, 16 mg + 16), K-split kq
+  const int mg = warp % (kPredW / kPKS), kq = warp / (kPredW / kPKS);
+  const int v0 = kq * pl.vks / kPKS, v1 = (kq + 1) * pl.vks / kPKS;
+  const int m0 = kq * pl.mks / kPKS, m1 = (kq + 1) * pl.mks / kPKS;
   // epilogue factor offsets: variance E[i, nu] = prod_{d < pN} g_d; mean phi_0[i, nu]
   int offE[NFV][2][FE], offEm[NFM][2];
 #pragma unroll
@@ -710,18 +710,14 @@ fused_predict_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView b, con
 #else
 #define PPROF(i)
 #endif
-  int it = 0;
-  for (int64_t blk = blk0; blk < pl.nblocks; blk += stride, ++it) {
-    const double* cur = slabs + (it & 1) * (kRows * rl.bw);
-    double* red = reds + (it & 1) * (4 * kRows * 2);
-    // production phase: the next block
-    if (blk + stride < pl.nblocks) {
-      produce(xn, blk + stride, slabs + ((it + 1) & 1) * (kRows * rl.bw));
-      xn = load_x(blk + 2 * stride);
-    }
+  for (int64_t blk = blk0; blk < pl.nblocks; blk += stride) {
+    // production phase
+    produce(xn, blk);
+    xn = load_x(blk + stride);
+    __syncthreads();
     PPROF(0)
     // DMMA phase
-    const double* row0 = cur + (mg * 16 + (lane >> 2)) * rl.bw;  // m-fragment f: + 8 f rows
+    const double* row0 = slab + (mg * 16 + (lane >> 2)) * rl.bw;  // m-fragment f: + 8 f rows
     double accV[kPMF][NFV][2], accM[kPMF][NFM][2];
 #pragma unroll
     for (int f = 0; f < kPMF; ++f) {
@@ -733,7 +729,7 @@ fused_predict_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView b, con
     if (want_var) contract<FK, NFV>(row0, rl.bw, offV, Bv, v0, v1, lane, accV);
     contract<FKM, NFM>(row0, rl.bw, offM, Bm, m0, m1, lane, accM);
     PPROF(1)
-    // this quarter's epilogue contribution per row: sum_nu Y[i, nu] E[i, nu] (var),
+    // this K-split's epilogue contribution per row: sum_nu Y[i, nu] E[i, nu] (var),
     // sum_nu Z[i, nu] phi_0[i, nu] (mean); the 4 lanes of a row hold disjoint columns
 #pragma unroll
     for (int f = 0; f < kPMF; ++f) {
@@ -754,21 +750,21 @@ fused_predict_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView b, con
       ms += __shfl_xor_sync(0xffffffffu, ms, 2);
       if ((lane & 3) == 0) {
         const int r = mg * 16 + 8 * f + (lane >> 2);
-        red[(kq * kRows + r) * 2 + 0] = vs;
-        red[(kq * kRows + r) * 2 + 1] = ms;
+        red[(kq * kPR + r) * 2 + 0] = vs;
+        red[(kq * kPR + r) * 2 + 1] = ms;
       }
     }
     PPROF(2)
-    __syncthreads();
+    __syncthreads();  // red complete; the slab is free for the next production
     PPROF(3)
-    if (tid < kRows) {
-      const int64_t row_i = blk * kRows + tid;
+    if (tid < kPR) {
+      const int64_t row_i = blk * kPR + tid;
       if (row_i < Ns) {
         double vs = red[tid * 2], ms = red[tid * 2 + 1];
 #pragma unroll
-        for (int q = 1; q < 4; ++q) {
-          vs += red[(q * kRows + tid) * 2];
-          ms += red[(q * kRows + tid) * 2 + 1];
+        for (int q = 1; q < kPKS; ++q) {
+          vs += red[(q * kPR + tid) * 2];
+          ms += red[(q * kPR + tid) * 2 + 1];
         }
         const double mm = c + ms;  // posterior.py:247
         mean[row_i] = mm;
@@ -780,8 +776,8 @@ fused_predict_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView b, con
         }
       }
     }
-    // red is double-buffered and the slab written next was last read before the barrier above:
-    // one barrier per block
+    // red is next written after the next block's first barrier, which these threads pass only
+    // after finishing here
     PPROF(2)
   }
 #ifdef FAGP_GRAM_PROFILE
@@ -815,11 +811,12 @@ static bool make_vplan(int64_t Ns, int p, int M, VPlan& pl) {
   const int NFM = M <= 8 ? 1 : 2;
   const RowLayout rl = row_layout(p, M);
   if (rl.bw > 256) return false;  // byte-packed offsets
-  pl.smem = (size_t(pl.vks) * NFV * 32 + size_t(pl.mks) * NFM * 32 + size_t(2 * 4) * kRows * 2 +
-             size_t(2) * kRows * rl.bw) * sizeof(double) +
+  pl.smem = (size_t(pl.vks) * NFV * 32 + size_t(pl.mks) * NFM * 32 + size_t(kPKS) * kPR * 2 +
+             size_t(kPR) * rl.bw) * sizeof(double) +
             size_t(pl.vks + pl.mks) * 4 * sizeof(uint32_t);
   if (pl.smem > 225 * 1024) return false;
-  pl.nblocks = ceil_div(tmax<int64_t>(Ns, 0), kRows);
+  if (kPR * p > kPredNT) return false;
+  pl.nblocks = ceil_div(tmax<int64_t>(Ns, 0), kPR);
   pl.grid = int(tmax<int64_t>(1, tmin<int64_t>(num_sms(), pl.nblocks)));
   pl.hc = herm_coef_host();
   return true;
