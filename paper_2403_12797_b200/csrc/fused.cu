@@ -119,6 +119,11 @@ struct GPlan {
   int S;                 // sub-ranges per CTA = chunks a host pipeline may launch separately
   int grid, nparts;      // nparts = grid * S * G partials
   HermCoef hc;           // recurrence coefficients (constant-bank operands)
+  // split layout (p = 3, M = 10): the ragged last n-fragment of K / t contracted with the
+  // roles of the last two dimensions swapped (see fused_gram_split_kernel)
+  int split, W1, R, R2;          // warps in role 1; L - 16; M - 8
+  int kmf1, kmf2, tmf1, tmf2;    // m-fragments of K1, K2, T1, T2
+  int baseK2, baseT1, baseT2;    // fragment offsets of the sections in a partial
 };
 
 #ifdef FAGP_GRAM_PROFILE
@@ -326,6 +331,204 @@ fused_gram_kernel(const double* __restrict__ X, const double* __restrict__ y, do
   if (bad_x) raise_flag(flags, FAGP_FLAG_X_NONFINITE);
 }
 
+// ---------------------------------------------------------------------------------------
+// Split-layout fused Gram for p = 3 (M = 10: L = 19 = 16 + 3, M = 8 + 2).  The last dimension's
+// 8-column fragments leave 3 of L (2 of M) columns ragged; instead of padding them to a full
+// fragment against all L^2 (M^2) A columns, they are contracted with the roles of dims 1 and 2
+// swapped:
+//   K1: A = g0 g1 (L^2 columns) x B = g2[0, 16)            K2: A = (g0, g2[16, L)) x B = g1
+//   T1: A = phi0 phi1 (M^2)     x B = r phi2[0, 8)         T2: A = (phi0, r phi2[8, M)) x B = phi1
+// 135 DMMA per 4-row k-step at C3 instead of 164.  Role 1 warps (w < W1) own JK1 K1 and JT1A T1
+// m-fragments, role 2 warps JK2 K2, JT2 T2 and JT1B T1 m-fragments (fragment ids strided by the
+// role's warp count), 9 DMMA per warp per k-step each.  Production, blocks, sub-ranges and the
+// partial flush are those of fused_gram_kernel.
+template <int JK1, int JT1A, int JK2, int JT2, int JT1B>
+__global__ void __launch_bounds__(kGramNT, 1)
+fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__ y, double c, int64_t N,
+                        BasisView b, const GPlan pl, int k0, int k1, double* __restrict__ ws, uint32_t* flags) {
+  extern __shared__ double sm[];
+  constexpr int p = 3;
+  const RowLayout rl = row_layout(p, pl.M);
+  double* slabs = sm;  // [2][kGR * bw]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int M = pl.M, L = pl.L;
+  const int cta = int(blockIdx.x);
+  const int bpc = int(pl.rows_per_cta / kGR);
+  auto sb = [&](int k) { return int(int64_t(k) * bpc / pl.S); };
+  const int g0 = sb(k0);
+  const int nblk = sb(k1) - g0;
+  auto blk_base = [&](int j) -> int64_t { return int64_t(cta) * pl.rows_per_cta + int64_t(g0 + j) * kGR; };
+  auto blk_end = [&](int j) -> int64_t { return tmin<int64_t>(N, blk_base(j) + kGR); };
+  bool bad_x = false;
+  const bool plane = tid < kGR * p;
+  const int prow = tid / p, pdim = tid - (tid / p) * p;
+  struct Pre {
+    double x, y;
+  };
+  auto load_pre = [&](int j, Pre& pr) {
+    const int64_t r = blk_base(j) + prow;
+    const bool ok = plane && r < blk_end(j);
+    pr.x = ok ? X[r * p + pdim] : 0.0;
+    pr.y = (ok && y != nullptr && pdim == p - 1) ? y[r] : c;
+  };
+  auto produce = [&](const Pre& pr, int j, double* slab) {
+    if (!plane) return;
+    double* row = slab + prow * rl.bw;
+    const bool valid = blk_base(j) + prow < blk_end(j);
+    if (valid) {
+      bad_x |= not_finite(pr.x);
+      const double rr = __dsub_rn(pr.y, c);  // r = y - c (posterior.py:229)
+      eval_phi_g_dim_u(pr.x, rr, b, pdim, pl.hc, row + rl.poff + pdim * M, row + rl.goff + pdim * L,
+                       pdim == p - 1 ? row + rl.rpoff : nullptr);
+    } else {
+      for (int k = 0; k < M; ++k) row[rl.poff + pdim * M + k] = 0.0;
+      for (int k = 0; k < L; ++k) row[rl.goff + pdim * L + k] = 0.0;
+      if (pdim == p - 1)
+        for (int k = 0; k < M; ++k) row[rl.rpoff + k] = 0.0;
+    }
+    if (pdim == 0) {
+      row[rl.one] = 1.0;
+      row[rl.zero] = 0.0;
+    }
+  };
+  __syncthreads();
+  Pre pre;
+  if (nblk > 0) {
+    load_pre(0, pre);
+    produce(pre, 0, slabs);
+  }
+  if (nblk > 1) load_pre(1, pre);
+
+  // A-operand offsets of an m-fragment: 2 factors; invalid columns -> (0, 1)
+  const int col = lane >> 2;
+  auto offs2 = [&](int m, int nvalid, int o0, int o1, int (&off)[2]) {
+    if (m < nvalid) {
+      off[0] = o0;
+      off[1] = o1;
+    } else {
+      off[0] = rl.zero;
+      off[1] = rl.one;
+    }
+  };
+  const bool role1 = warp < pl.W1;
+  const int wi = role1 ? warp : warp - pl.W1, WR = role1 ? pl.W1 : kGramW - pl.W1;
+  constexpr int NJ = (JK1 + JT1A) > (JK2 + JT2 + JT1B) ? (JK1 + JT1A) : (JK2 + JT2 + JT1B);
+  constexpr int NACC = (2 * JK1 + JT1A) > (3 * JK2 + 2 * JT2 + JT1B) ? (2 * JK1 + JT1A) : (3 * JK2 + 2 * JT2 + JT1B);
+  int offA[NJ][2], offB[5];
+  int fragOf[NACC];  // partial fragment index of each accumulator (-1: dummy)
+#pragma unroll
+  for (int q = 0; q < NACC; ++q) fragOf[q] = -1;
+  if (role1) {
+#pragma unroll
+    for (int j = 0; j < JK1; ++j) {
+      const int mf = wi + WR * j, m = mf * 8 + col;
+      offs2(m, L * L, rl.goff + m / L, rl.goff + L + m % L, offA[j]);
+#pragma unroll
+      for (int nf = 0; nf < 2; ++nf) fragOf[2 * j + nf] = mf < pl.kmf1 ? mf * 2 + nf : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < JT1A; ++j) {
+      const int mf = wi + WR * j, m = mf * 8 + col;
+      offs2(m, M * M, rl.poff + m / M, rl.poff + M + m % M, offA[JK1 + j]);
+      fragOf[2 * JK1 + j] = mf < pl.tmf1 ? pl.baseT1 + mf : -1;
+    }
+    offB[0] = rl.goff + 2 * L + col;      // g2[0, 8)
+    offB[1] = rl.goff + 2 * L + 8 + col;  // g2[8, 16)
+    offB[2] = rl.rpoff + col;             // r phi2[0, 8)
+  } else {
+#pragma unroll
+    for (int j = 0; j < JK2; ++j) {
+      const int mf = wi + WR * j, m = mf * 8 + col;
+      offs2(m, L * pl.R, rl.goff + m / pl.R, rl.goff + 2 * L + 16 + m % pl.R, offA[j]);
+#pragma unroll
+      for (int nf = 0; nf < 3; ++nf) fragOf[3 * j + nf] = mf < pl.kmf2 ? pl.baseK2 + mf * 3 + nf : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < JT2; ++j) {
+      const int mf = wi + WR * j, m = mf * 8 + col;
+      offs2(m, M * pl.R2, rl.poff + m / pl.R2, rl.rpoff + 8 + m % pl.R2, offA[JK2 + j]);
+#pragma unroll
+      for (int nf = 0; nf < 2; ++nf) fragOf[3 * JK2 + 2 * j + nf] = mf < pl.tmf2 ? pl.baseT2 + mf * 2 + nf : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < JT1B; ++j) {
+      const int mf = pl.W1 * JT1A + wi + WR * j, m = mf * 8 + col;
+      offs2(m, M * M, rl.poff + m / M, rl.poff + M + m % M, offA[JK2 + JT2 + j]);
+      fragOf[3 * JK2 + 2 * JT2 + j] = mf < pl.tmf1 ? pl.baseT1 + mf : -1;
+    }
+#pragma unroll
+    for (int nf = 0; nf < 3; ++nf) offB[nf] = nf * 8 + col < L ? rl.goff + L + nf * 8 + col : rl.zero;  // g1
+#pragma unroll
+    for (int nf = 0; nf < 2; ++nf) offB[3 + nf] = nf * 8 + col < M ? rl.poff + M + nf * 8 + col : rl.zero;  // phi1
+  }
+  if (role1) offB[3] = offB[4] = rl.zero;
+  double acc[NACC][2];
+#pragma unroll
+  for (int q = 0; q < NACC; ++q) acc[q][0] = acc[q][1] = 0.0;
+  __syncthreads();
+
+  auto kstep = [&](const double* cur, int i) {
+    const double* row = cur + (i * 4 + (lane & 3)) * rl.bw;
+    if (role1) {
+      const double b0 = row[offB[0]], b1 = row[offB[1]], bt = row[offB[2]];
+#pragma unroll
+      for (int j = 0; j < JK1; ++j) {
+        const double a = __dmul_rn(row[offA[j][0]], row[offA[j][1]]);
+        dmma_8x8x4(acc[2 * j][0], acc[2 * j][1], a, b0);
+        dmma_8x8x4(acc[2 * j + 1][0], acc[2 * j + 1][1], a, b1);
+      }
+#pragma unroll
+      for (int j = 0; j < JT1A; ++j) {
+        const double a = __dmul_rn(row[offA[JK1 + j][0]], row[offA[JK1 + j][1]]);
+        dmma_8x8x4(acc[2 * JK1 + j][0], acc[2 * JK1 + j][1], a, bt);
+      }
+    } else {
+      const double b0 = row[offB[0]], b1 = row[offB[1]], b2 = row[offB[2]], p0 = row[offB[3]], p1 = row[offB[4]];
+      const double bt = row[rl.rpoff + col];
+#pragma unroll
+      for (int j = 0; j < JK2; ++j) {
+        const double a = __dmul_rn(row[offA[j][0]], row[offA[j][1]]);
+        dmma_8x8x4(acc[3 * j][0], acc[3 * j][1], a, b0);
+        dmma_8x8x4(acc[3 * j + 1][0], acc[3 * j + 1][1], a, b1);
+        dmma_8x8x4(acc[3 * j + 2][0], acc[3 * j + 2][1], a, b2);
+      }
+#pragma unroll
+      for (int j = 0; j < JT2; ++j) {
+        const double a = __dmul_rn(row[offA[JK2 + j][0]], row[offA[JK2 + j][1]]);
+        dmma_8x8x4(acc[3 * JK2 + 2 * j][0], acc[3 * JK2 + 2 * j][1], a, p0);
+        dmma_8x8x4(acc[3 * JK2 + 2 * j + 1][0], acc[3 * JK2 + 2 * j + 1][1], a, p1);
+      }
+#pragma unroll
+      for (int j = 0; j < JT1B; ++j) {
+        const double a = __dmul_rn(row[offA[JK2 + JT2 + j][0]], row[offA[JK2 + JT2 + j][1]]);
+        dmma_8x8x4(acc[3 * JK2 + 2 * JT2 + j][0], acc[3 * JK2 + 2 * JT2 + j][1], a, bt);
+      }
+    }
+  };
+  auto flush = [&](int k) {
+    double* out = ws + (int64_t(cta) * pl.S + k) * pl.plen;
+#pragma unroll
+    for (int q = 0; q < NACC; ++q) {
+      if (fragOf[q] >= 0)
+        *reinterpret_cast<double2*>(out + int64_t(fragOf[q]) * 64 + 2 * lane) = make_double2(acc[q][0], acc[q][1]);
+      acc[q][0] = acc[q][1] = 0.0;
+    }
+  };
+  for (int n = 0; n < nblk; ++n) {
+    const double* cur = slabs + (n & 1) * (kGR * rl.bw);
+    if (n + 1 < nblk) {
+      produce(pre, n + 1, slabs + ((n + 1) & 1) * (kGR * rl.bw));
+      if (n + 2 < nblk) load_pre(n + 2, pre);
+    }
+#pragma unroll 2
+    for (int i = 0; i < kGR / 4; ++i) kstep(cur, i);
+    for (int k = k0; k < k1; ++k)
+      if (g0 + n + 1 == sb(k + 1)) flush(k);
+    __syncthreads();
+  }
+  if (bad_x) raise_flag(flags, FAGP_FLAG_X_NONFINITE);
+}
+
 // out[e] = sum over the partials (fixed order: deterministic) of entry e of [K | t], read from
 // the fragment-major partial layout; non-finite -> PHI flag
 __global__ void partial_sum_kernel(const double* __restrict__ ws, const GPlan pl, double* __restrict__ out,
@@ -335,7 +538,31 @@ __global__ void partial_sum_kernel(const double* __restrict__ ws, const GPlan pl
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < pl.len;
        e += int64_t(gridDim.x) * blockDim.x) {
     int64_t m, n, frag;
-    if (e < pl.Klen) {
+    if (pl.split) {
+      if (e < pl.Klen) {
+        const int64_t ka = e / pl.L, k2 = e - ka * pl.L;
+        if (k2 < 16) {
+          m = ka;
+          n = k2;
+          frag = (m >> 3) * 2 + (n >> 3);
+        } else {
+          m = (ka / pl.L) * pl.R + (k2 - 16);
+          n = ka % pl.L;
+          frag = pl.baseK2 + (m >> 3) * 3 + (n >> 3);
+        }
+      } else {
+        const int64_t q = e - pl.Klen, aa = q / pl.M, a2 = q - aa * pl.M;
+        if (a2 < 8) {
+          m = aa;
+          n = a2;
+          frag = pl.baseT1 + (m >> 3);
+        } else {
+          m = (aa / pl.M) * pl.R2 + (a2 - 8);
+          n = aa % pl.M;
+          frag = pl.baseT2 + (m >> 3) * 2 + (n >> 3);
+        }
+      }
+    } else if (e < pl.Klen) {
       m = e / pl.KB;
       n = e - m * pl.KB;
       frag = (m >> 3) * NFK + (n >> 3);
@@ -422,10 +649,30 @@ static bool make_gplan(int64_t N, int p, int M, GPlan& pl) {
   pl.grid = int(tmax<int64_t>(1, ceil_div(tmax<int64_t>(N, 1), pl.rows_per_cta)));
   pl.nparts = pl.grid * pl.S * pl.G;
   pl.hc = herm_coef_host();
+  // split layout (fused_gram_split_kernel): p = 3, M = 10 (the BASELINE C3 shape)
+  const char* se = getenv("FAGP_GRAM_SPLIT");
+  if (p == 3 && M == 10 && !(se && se[0] == '0')) {
+    pl.split = 1;
+    pl.W1 = 12;
+    pl.R = pl.L - 16;
+    pl.R2 = M - 8;
+    pl.kmf1 = int(ceil_div(int64_t(pl.L) * pl.L, 8));
+    pl.kmf2 = int(ceil_div(int64_t(pl.L) * pl.R, 8));
+    pl.tmf1 = int(ceil_div(int64_t(M) * M, 8));
+    pl.tmf2 = int(ceil_div(int64_t(M) * pl.R2, 8));
+    pl.baseK2 = pl.kmf1 * 2;
+    pl.baseT1 = pl.baseK2 + pl.kmf2 * 3;
+    pl.baseT2 = pl.baseT1 + pl.tmf1;
+    pl.plen = int64_t(pl.baseT2 + pl.tmf2 * 2) * 64;
+    pl.G = 1;
+    pl.WG = kGramW;
+    pl.nparts = pl.grid * pl.S;
+  }
   return true;
 }
 
 static size_t gram_smem(const GPlan& pl) {
+  if (pl.split) return size_t(2) * kGR * row_layout(pl.p, pl.M).bw * sizeof(double);
   return (size_t(2) * pl.LC + size_t(2) * kGR * row_layout(pl.p, pl.M).bw) * sizeof(double);
 }
 
@@ -516,7 +763,13 @@ int gram(const double* X, const double* y, double c, int64_t N, const fagp_basis
   if (k0 < 0 || k1 > pl.S || k0 >= k1) return FAGP_EINVAL;
   double* w = static_cast<double*>(ws);
   int rc;
-  switch (b->p - 1) {
+  if (pl.split) {
+    const size_t smem = gram_smem(pl);
+    auto kern = fused_gram_split_kernel<4, 1, 2, 1, 1>;
+    FAGP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    kern<<<pl.grid, kGramNT, smem, s>>>(X, y, c, N, view(b), pl, k0, k1, w, flags);
+    rc = FAGP_OK;
+  } else switch (b->p - 1) {
     case 1: rc = launch_gram_fa<1>(X, y, c, N, b, pl, k0, k1, w, flags, s); break;
     case 2: rc = launch_gram_fa<2>(X, y, c, N, b, pl, k0, k1, w, flags, s); break;
     case 3: rc = launch_gram_fa<3>(X, y, c, N, b, pl, k0, k1, w, flags, s); break;
