@@ -47,7 +47,7 @@ CONFIGS = {
 METRIC = "posterior mean+var samples/s (N=1e6, p=3, M=10); % FP64 tensor peak"
 NOISE_VAR = 0.0025
 FP64_PEAK_FILE = ROOT / "profiles" / "fp64_peak_r01.json"
-NCU_SUMMARY_FILE = ROOT / "profiles" / "ncu_summary_r01z.json"
+NCU_SUMMARY_FILE = ROOT / "profiles" / "ncu_summary_r02a.json"
 
 
 def log(*a):
@@ -60,8 +60,14 @@ def useful_flops(N, Ns, m):
     return N * m * (m + 1) + 2 * N * m + 2 * m**3 / 3 + 2 * Ns * m + Ns * m * (m + 1) + 2 * Ns * m
 
 
-def launches_per_step(m, pair, p=1, fused=False):
-    """Kernels of ours launched by one PosteriorEngine.run() (no jitter retry)."""
+def launches_per_step(m, pair, p=1, fused=False, inverse=False):
+    """Kernels of ours launched by one timed step (no jitter retry), as the ncu launch list of
+    the same step shows (profiles/ncu_summary_*.json)."""
+    if pair and fused and inverse:
+        # fagp_gram_x: fused Gram + partial sum; fagp_factor_inv_async: p mode products (K -> H),
+        # pair_system + t copy, fused Cholesky inverse, w GEMV, ctilde, p mode products
+        # (-> C''), scatter, w copy; fagp_predict_x: one fused kernel
+        return 2 + (p + 2 + 1 + 1 + 1 + p + 1 + 1) + 1
     nblk = -(-m // 32)
     potrf = nblk + (nblk - 1)  # fused diag+panel kernel per step, trailing GEMM between steps
     mp = 32
@@ -74,12 +80,9 @@ def launches_per_step(m, pair, p=1, fused=False):
         h *= 2
     trtri = 1 + 1 + 2 * levels  # pad, diag_inv, 2 GEMMs per level
     if pair:
-        # K -> H expansion (p mode products), t copy, build A, persistent potrf (1 cooperative
-        # launch), zero upper, trtri, w GEMVs x2, D = X^T X, Ct, Ct -> C'' (p mode products),
-        # scatter, w copy
         factor = p + 1 + 1 + 1 + 1 + trtri + 2 + 1 + 1 + p + 1 + 1
         if fused:
-            return 2 + factor + 1  # fused Gram + partial sum, factor, fused mean + variance
+            return 2 + factor + 1
         return 2 + 2 + factor + 2  # basis_eval x2, modal GEMM + reduce, factor, var + mean
     factor = 1 + 1 + potrf + 1 + trtri + 2 + 1  # build G/t, build A, potrf, zero upper, trtri, GEMVs, operand
     return 2 + 2 + factor + 1  # basis_eval x2, gram + reduce, factor, predict
@@ -351,7 +354,7 @@ def main():
     if g_ms >= p_ms:
         dom, dflops, rflops, dms = "fagp_gram_x (eigenfunctions on chip + modal DMMA Gram + t, partial sum)" if pair else \
             "fagp_gram (fused SYRK + reduce)", gram_flops, ref_gram, g_ms
-        traffic = ncu_traffic("fused_gram_kernel" if pair else "gram_kernel_fast")
+        traffic = ncu_traffic("fused_gram_split_kernel" if pair and p == 3 and M == 10 else "fused_gram_kernel" if pair else "gram_kernel_fast")
     else:
         dom, dflops, rflops, dms = "fagp_predict_x (eigenfunctions on chip + modal DMMA variance + mean)" if pair else \
             "fagp_predict (fused triangular GEMM)", pred_flops, ref_pred, p_ms
@@ -412,7 +415,8 @@ def main():
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator)",
                "config": config_dict(args, world), "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
-               "clocks": clk.summary(), "gpu_launches": launches_per_step(m, 2 <= p <= 8, p, fused=eng.pred_ws_bytes == 0) * args.steps,
+               "clocks": clk.summary(), "gpu_launches": launches_per_step(m, 2 <= p <= 8, p, fused=eng.pred_ws_bytes == 0,
+                                                inverse=eng.inverse_route) * args.steps,
                "phases_ms": {"gram": round(g_ms, 3),
                              "allreduce+factor": round(statistics.mean(factor_ms), 3), "predict": round(p_ms, 3)},
                "step_reference_equivalent_tflops": round(step_tf, 3),
