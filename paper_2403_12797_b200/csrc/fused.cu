@@ -1042,6 +1042,187 @@ fused_predict_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView b, con
   if (bad) raise_flag(flags, FAGP_FLAG_PHI_NONFINITE);
 }
 
+// Split-layout fused predict for p = 3, M in [9, 12] (the C3 shape): the ragged last n-fragment of
+// the variance (nu = kappa_0 in [16, L)) and of the mean (a_0 in [8, M)) is contracted with the
+// roles of dims 0 and 1 swapped, as in fused_gram_split_kernel:
+//   var1:  A = g1 g2 (L^2)            x B = C''[.][0, 16)       epilogue g0[nu]
+//   var2:  A = (g0[16, L), g2) ((L-16) L)  x B = C''[(k1,k2)][16 + k0'] over k1   epilogue g1[k1]
+//   mean1: A = phi1 phi2 (M^2)        x B = w[a0 < 8][.]        epilogue phi0[a0]
+//   mean2: A = (phi0[8, M), phi2)     x B = w[8 + a0'][a1][a2] over a1            epilogue phi1[a1]
+// (19% fewer DMMA at C3).  Same blocks, production, warp split and reduction as
+// fused_predict_kernel.
+__global__ void __launch_bounds__(kPredNT, 1)
+fused_predict_split_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView b, const VPlan pl,
+                           const double* __restrict__ op, double sigma2, double c, double* __restrict__ mean,
+                           double* __restrict__ var, uint32_t* flags) {
+  constexpr int P = 3;
+  extern __shared__ double sm[];
+  const RowLayout rl = row_layout(P, pl.M);
+  const bool want_var = var != nullptr;
+  const int M = pl.M, L = pl.L, R = L - 16, R2 = M - 8;
+  const int vk1 = (L * L + 3) / 4, vk2 = (R * L + 3) / 4, mk1 = (M * M + 3) / 4, mk2 = (R2 * M + 3) / 4;
+  double* Bv1 = sm;                      // [vk1][2][32]
+  double* Bv2 = Bv1 + vk1 * 2 * 32;      // [vk2][3][32]
+  double* Bm1 = Bv2 + vk2 * 3 * 32;      // [mk1][1][32]
+  double* Bm2 = Bm1 + mk1 * 32;          // [mk2][2][32]
+  double* red = Bm2 + mk2 * 2 * 32;      // [kPKS][kPR][2]
+  double* slab = red + kPKS * kPR * 2;   // [kPR * bw]
+  uint32_t* offV1 = reinterpret_cast<uint32_t*>(slab + kPR * rl.bw);
+  uint32_t* offV2 = offV1 + vk1 * 4;
+  uint32_t* offM1 = offV2 + vk2 * 4;
+  uint32_t* offM2 = offM1 + mk1 * 4;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const double* w = op + pl.KP * pl.NP;
+  const int64_t KM = int64_t(M) * M;
+  auto pack2 = [&](int o0, int o1) { return uint32_t(o0) | (uint32_t(o1) << 8); };
+  for (int i = tid; i < vk1 * 2 * 32; i += kPredNT) {  // C''[kappa = (k1, k2)][nu < 16]
+    const int ln = i & 31, q = i >> 5, nf = q & 1, ks = q >> 1;
+    const int kap = 4 * ks + (ln & 3), nu = 8 * nf + (ln >> 2);
+    Bv1[i] = (want_var && kap < L * L) ? op[int64_t(kap) * pl.NP + nu] : 0.0;
+  }
+  for (int i = tid; i < vk2 * 3 * 32; i += kPredNT) {  // C''[(k1, k2)][16 + k0'], kappa' = k0' L + k2, column k1
+    const int ln = i & 31, q = i >> 5, nf = q % 3, ks = q / 3;
+    const int kap = 4 * ks + (ln & 3), k1 = 8 * nf + (ln >> 2);
+    Bv2[i] = (want_var && kap < R * L && k1 < L) ? op[int64_t(k1 * L + kap % L) * pl.NP + 16 + kap / L] : 0.0;
+  }
+  for (int i = tid; i < mk1 * 32; i += kPredNT) {  // w[a0 < 8][(a1, a2)]
+    const int ln = i & 31, ks = i >> 5;
+    const int kap = 4 * ks + (ln & 3), a0 = ln >> 2;
+    Bm1[i] = kap < M * M ? w[int64_t(a0) * KM + kap] : 0.0;
+  }
+  for (int i = tid; i < mk2 * 2 * 32; i += kPredNT) {  // w[8 + a0'][a1][a2], kappa' = a0' M + a2, column a1
+    const int ln = i & 31, q = i >> 5, nf = q & 1, ks = q >> 1;
+    const int kap = 4 * ks + (ln & 3), a1 = 8 * nf + (ln >> 2);
+    Bm2[i] = (kap < R2 * M && a1 < M) ? w[int64_t(8 + kap / M) * KM + int64_t(a1) * M + kap % M] : 0.0;
+  }
+  for (int k = tid; k < vk1 * 4; k += kPredNT)
+    offV1[k] = k < L * L ? pack2(rl.goff + L + k / L, rl.goff + 2 * L + k % L) : pack2(rl.zero, rl.one);
+  for (int k = tid; k < vk2 * 4; k += kPredNT)
+    offV2[k] = k < R * L ? pack2(rl.goff + 16 + k / L, rl.goff + 2 * L + k % L) : pack2(rl.zero, rl.one);
+  for (int k = tid; k < mk1 * 4; k += kPredNT)
+    offM1[k] = k < M * M ? pack2(rl.poff + M + k / M, rl.poff + 2 * M + k % M) : pack2(rl.zero, rl.one);
+  for (int k = tid; k < mk2 * 4; k += kPredNT)
+    offM2[k] = k < R2 * M ? pack2(rl.poff + 8 + k / M, rl.poff + 2 * M + k % M) : pack2(rl.zero, rl.one);
+  bool bad_x = false, bad = false;
+  const bool plane = tid < kPR * P;
+  const int prow = tid / P, pdim = tid - (tid / P) * P;
+  auto load_x = [&](int64_t blk) -> double {
+    const int64_t r = blk * kPR + prow;
+    return (plane && blk < pl.nblocks && r < Ns) ? Xs[r * P + pdim] : 0.0;
+  };
+  auto produce = [&](double x, int64_t blk) {
+    if (!plane) return;
+    double* row = slab + prow * rl.bw;
+    if (blk * kPR + prow < Ns) {
+      bad_x |= not_finite(x);
+      eval_phi_g_dim_u(x, 0.0, b, pdim, pl.hc, row + rl.poff + pdim * M, row + rl.goff + pdim * L, nullptr);
+    } else {
+      for (int k = 0; k < M; ++k) row[rl.poff + pdim * M + k] = 0.0;
+      for (int k = 0; k < L; ++k) row[rl.goff + pdim * L + k] = 0.0;
+    }
+    if (pdim == 0) {
+      row[rl.one] = 1.0;
+      row[rl.zero] = 0.0;
+    }
+  };
+  const int64_t blk0 = blockIdx.x, stride = gridDim.x;
+  double xn = load_x(blk0);
+  const int mg = warp % (kPredW / kPKS), kq = warp / (kPredW / kPKS);
+  auto half = [&](int n, int q) { return q * n / kPKS; };
+  // epilogue offsets: var1 g0[nu < 16], var2 g1[k1 < L], mean1 phi0[a0 < 8], mean2 phi1[a1 < M]
+  int oE1[2][2], oE2[3][2], oM1[1][2], oM2[2][2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int cc = 2 * (lane & 3) + e;
+#pragma unroll
+    for (int nf = 0; nf < 2; ++nf) oE1[nf][e] = rl.goff + nf * 8 + cc;
+#pragma unroll
+    for (int nf = 0; nf < 3; ++nf) oE2[nf][e] = nf * 8 + cc < L ? rl.goff + L + nf * 8 + cc : rl.zero;
+    oM1[0][e] = rl.poff + cc;
+#pragma unroll
+    for (int nf = 0; nf < 2; ++nf) oM2[nf][e] = nf * 8 + cc < M ? rl.poff + M + nf * 8 + cc : rl.zero;
+  }
+  __syncthreads();
+
+  for (int64_t blk = blk0; blk < pl.nblocks; blk += stride) {
+    produce(xn, blk);
+    xn = load_x(blk + stride);
+    __syncthreads();
+    const double* row0 = slab + (mg * 16 + (lane >> 2)) * rl.bw;
+    double aV1[kPMF][2][2], aV2[kPMF][3][2], aM1[kPMF][1][2], aM2[kPMF][2][2];
+#pragma unroll
+    for (int f = 0; f < kPMF; ++f)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        aV1[f][0][e] = aV1[f][1][e] = aV2[f][0][e] = aV2[f][1][e] = aV2[f][2][e] = 0.0;
+        aM1[f][0][e] = aM2[f][0][e] = aM2[f][1][e] = 0.0;
+      }
+    if (want_var) {
+      contract<2, 2>(row0, rl.bw, offV1, Bv1, half(vk1, kq), half(vk1, kq + 1), lane, aV1);
+      contract<2, 3>(row0, rl.bw, offV2, Bv2, half(vk2, kq), half(vk2, kq + 1), lane, aV2);
+    }
+    contract<2, 1>(row0, rl.bw, offM1, Bm1, half(mk1, kq), half(mk1, kq + 1), lane, aM1);
+    contract<2, 2>(row0, rl.bw, offM2, Bm2, half(mk2, kq), half(mk2, kq + 1), lane, aM2);
+#pragma unroll
+    for (int f = 0; f < kPMF; ++f) {
+      const double* row = row0 + 8 * f * rl.bw;
+      double vs = 0.0, ms = 0.0;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (want_var) {
+#pragma unroll
+          for (int nf = 0; nf < 2; ++nf) vs = fma(aV1[f][nf][e], row[oE1[nf][e]], vs);
+#pragma unroll
+          for (int nf = 0; nf < 3; ++nf) vs = fma(aV2[f][nf][e], row[oE2[nf][e]], vs);
+        }
+        ms = fma(aM1[f][0][e], row[oM1[0][e]], ms);
+#pragma unroll
+        for (int nf = 0; nf < 2; ++nf) ms = fma(aM2[f][nf][e], row[oM2[nf][e]], ms);
+      }
+      vs += __shfl_xor_sync(0xffffffffu, vs, 1);
+      vs += __shfl_xor_sync(0xffffffffu, vs, 2);
+      ms += __shfl_xor_sync(0xffffffffu, ms, 1);
+      ms += __shfl_xor_sync(0xffffffffu, ms, 2);
+      if ((lane & 3) == 0) {
+        const int r = mg * 16 + 8 * f + (lane >> 2);
+        red[(kq * kPR + r) * 2 + 0] = vs;
+        red[(kq * kPR + r) * 2 + 1] = ms;
+      }
+    }
+    __syncthreads();
+    if (tid < kPR) {
+      const int64_t row_i = blk * kPR + tid;
+      if (row_i < Ns) {
+        double vs = red[tid * 2], ms = red[tid * 2 + 1];
+#pragma unroll
+        for (int q = 1; q < kPKS; ++q) {
+          vs += red[(q * kPR + tid) * 2];
+          ms += red[(q * kPR + tid) * 2 + 1];
+        }
+        const double mm = c + ms;  // posterior.py:247
+        mean[row_i] = mm;
+        bad |= not_finite(mm);
+        if (want_var) {
+          const double vv = sigma2 * vs;
+          var[row_i] = vv;
+          bad |= not_finite(vv);
+        }
+      }
+    }
+  }
+  if (bad_x) raise_flag(flags, FAGP_FLAG_X_NONFINITE);
+  if (bad) raise_flag(flags, FAGP_FLAG_PHI_NONFINITE);
+}
+
+static size_t split_predict_smem(int M) {
+  const int L = 2 * M - 1, R = L - 16, R2 = M - 8;
+  const int vk1 = (L * L + 3) / 4, vk2 = (R * L + 3) / 4, mk1 = (M * M + 3) / 4, mk2 = (R2 * M + 3) / 4;
+  const RowLayout rl = row_layout(3, M);
+  return (size_t(vk1) * 2 * 32 + size_t(vk2) * 3 * 32 + size_t(mk1) * 32 + size_t(mk2) * 2 * 32 +
+          size_t(kPKS) * kPR * 2 + size_t(kPR) * rl.bw) * sizeof(double) +
+         size_t(vk1 + vk2 + mk1 + mk2) * 4 * sizeof(uint32_t);
+}
+
 static bool make_vplan(int64_t Ns, int p, int M, VPlan& pl) {
   std::memset(&pl, 0, sizeof(pl));
   if (!modal_on(p, M) || p > kMaxF || M > 12) return false;
@@ -1106,6 +1287,15 @@ int predict(const double* Xs, int64_t Ns, const fagp_basis* b, const double* op,
   VPlan pl;
   if (!make_vplan(Ns, b->p, b->M, pl)) return FAGP_EUNSUPPORTED;
   if (Ns == 0) return FAGP_OK;
+  const char* se = getenv("FAGP_PREDICT_SPLIT");
+  if (b->p == 3 && pl.pN == 1 && b->M >= 9 && b->M <= 12 && !(se && se[0] == '0')) {
+    const size_t smem = split_predict_smem(b->M);
+    FAGP_CUDA_TRY(cudaFuncSetAttribute(fused_predict_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(smem)));
+    fused_predict_split_kernel<<<pl.grid, kPredNT, smem, s>>>(Xs, Ns, view(b), pl, op, sigma2, c, mean, var, flags);
+    FAGP_LAUNCH_CHECK();
+    return FAGP_OK;
+  }
   int rc;
   switch (b->p - pl.pN) {
     case 1: rc = launch_pred_fk<1>(Xs, Ns, b, pl, op, sigma2, c, mean, var, flags, s); break;
