@@ -131,6 +131,61 @@ __device__ __forceinline__ void eval_phi_g_dim_u(double x, double r, const Basis
   }
 }
 
+// eval_phi_g_dim_u for T independent (point, dimension) tasks advanced in lockstep (T chains
+// per thread hide each other's FP64 latency); identical operations and results per task.
+template <int T>
+__device__ __forceinline__ void eval_phi_g_dim_uT(const double (&x)[T], const double (&r)[T], const BasisView& b,
+                                                  const int (&d)[T], const HermCoef& hc, double* const (&out_phi)[T],
+                                                  double* const (&out_g)[T], double* const (&out_rphi)[T]) {
+  const int M = b.M, L = modal_L(M);
+  double zr[T], env[T], amp[T], yz[T], hp[T], hpm[T], hg[T], hgm[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    zr[t] = __dmul_rn(b.rho_beta()[d[t]], x[t]);
+    const double e1 = phi_exp(b, d[t], x[t]);
+    env[t] = __dmul_rn(b.sqrt_beta()[d[t]], e1);
+    amp[t] = g_amp(b, d[t], e1);
+    yz[t] = __dmul_rn(zr[t], kSqrt2);
+    hp[t] = __dmul_rn(zr[t], kSqrt2);
+    hpm[t] = 1.0;
+    hg[t] = __dmul_rn(yz[t], kSqrt2);
+    hgm[t] = 1.0;
+  }
+  auto put_phi = [&](int t, int k, double h) {
+    const double v = __dmul_rn(env[t], h);
+    out_phi[t][k] = v;
+    if (out_rphi[t]) out_rphi[t][k] = __dmul_rn(r[t], v);
+  };
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    put_phi(t, 0, 1.0);
+    out_g[t][0] = amp[t];
+    if (M > 1) put_phi(t, 1, hp[t]);
+    if (L > 1) out_g[t][1] = __dmul_rn(amp[t], hg[t]);
+  }
+#pragma unroll
+  for (int k = 1; k < kHermMax - 1; ++k) {
+    if (k < L - 1) {
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const double hgn = fma(__dmul_rn(yz[t], hc.c1[k]), hg[t], -__dmul_rn(hc.c2[k], hgm[t]));
+        out_g[t][k + 1] = __dmul_rn(amp[t], hgn);
+        hgm[t] = hg[t];
+        hg[t] = hgn;
+      }
+      if (k < M - 1) {
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+          const double hpn = __dsub_rn(__dmul_rn(__dmul_rn(zr[t], hc.c1[k]), hp[t]), __dmul_rn(hc.c2[k], hpm[t]));
+          put_phi(t, k + 1, hpn);
+          hpm[t] = hp[t];
+          hp[t] = hpn;
+        }
+      }
+    }
+  }
+}
+
 // phi (reference order, bit-faithful) and g of one (point, dimension) sharing the exponential,
 // the two recurrences advanced in one loop (independent chains); rphi (nullable) <- r * phi.
 __device__ __forceinline__ void eval_phi_g_dim(double x, double r, const BasisView& b, int d, const double* c1,

@@ -280,8 +280,20 @@ __global__ void mode_kernel(const double* __restrict__ in, double* __restrict__ 
     const int64_t a = aj / nout;
     const double* src = in + a * nin * post + c;
     const double* bj = B + int64_t(j) * ldj;
+    // loads issued 8 at a time (an L2 round trip each otherwise); the sum keeps the order of i
     double acc = 0.0;
-    for (int i = 0; i < nin; ++i) acc = fma(src[int64_t(i) * post], bj[int64_t(i) * ldi], acc);
+    int i = 0;
+    for (; i + 8 <= nin; i += 8) {
+      double v[8], w[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        v[u] = src[int64_t(i + u) * post];
+        w[u] = bj[int64_t(i + u) * ldi];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc = fma(v[u], w[u], acc);
+    }
+    for (; i < nin; ++i) acc = fma(src[int64_t(i) * post], bj[int64_t(i) * ldi], acc);
     out[o] = acc;
   }
 }
