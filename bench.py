@@ -358,7 +358,7 @@ def main():
     else:
         dom, dflops, rflops, dms = "fagp_predict_x (eigenfunctions on chip + modal DMMA variance + mean)" if pair else \
             "fagp_predict (fused triangular GEMM)", pred_flops, ref_pred, p_ms
-        traffic = ncu_traffic("fused_predict_kernel" if pair else "predict_kernel_fast")
+        traffic = ncu_traffic(("fused_predict_split_kernel" if p == 3 and 9 <= M <= 12 else "fused_predict_kernel") if pair else "predict_kernel_fast")
     achieved = dflops / (dms / 1e3) / 1e12
     roofline = {"bound": "tensor", "kernel": dom, "achieved": round(achieved, 3), "peak": peak, "unit": "TFLOP/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,

@@ -559,18 +559,51 @@ __global__ void set_mean_weights_kernel(double* P, const double* w, int64_t m, i
 }
 
 // w_i = s_i sum_j D_ij (s_j t_j)  (= s * A^{-1}(s * t), posterior.py:233-235) from the explicit
-// inverse D: one warp per row, lanes stride over j, fixed-order shuffle reduction.
-__global__ void sym_gemv_scaled_kernel(const double* __restrict__ D, int64_t m, const double* __restrict__ s,
-                                       const double* __restrict__ t, double* __restrict__ w) {
-  const int lane = threadIdx.x & 31;
-  const int64_t i = int64_t(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
-  if (i >= m) return;
+// inverse D: one 128-thread CTA per row, every load of a thread issued together (one round trip),
+// thread-strided partial sums combined in a fixed order (shuffle tree, then the 4 warps in order).
+constexpr int kGemvNT = 128;
+__global__ void __launch_bounds__(kGemvNT) sym_gemv_scaled_kernel(const double* __restrict__ D, int64_t m,
+                                                                  const double* __restrict__ s,
+                                                                  const double* __restrict__ t,
+                                                                  double* __restrict__ w) {
+  __shared__ double red[kGemvNT / 32];
+  const int tid = int(threadIdx.x), lane = tid & 31, warp = tid >> 5;
+  const int64_t i = blockIdx.x;
   const double* Di = D + i * m;
   double acc = 0.0;
-  for (int64_t j = lane; j < m; j += 32) acc = fma(Di[j], __dmul_rn(s[j], t[j]), acc);
+  int64_t j = tid;
+  for (; j + 7 * kGemvNT < m; j += 8 * kGemvNT) {
+    double d[8], u[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      d[q] = Di[j + kGemvNT * q];
+      u[q] = __dmul_rn(s[j + kGemvNT * q], t[j + kGemvNT * q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc = fma(d[q], u[q], acc);
+  }
+  {
+    double d[8], u[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const bool ok = j + kGemvNT * q < m;
+      d[q] = ok ? Di[j + kGemvNT * q] : 0.0;
+      u[q] = ok ? __dmul_rn(s[j + kGemvNT * q], t[j + kGemvNT * q]) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (j + kGemvNT * q < m) acc = fma(d[q], u[q], acc);
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) w[i] = __dmul_rn(s[i], acc);
+  if (lane == 0) red[warp] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    double v = red[0];
+#pragma unroll
+    for (int q = 1; q < kGemvNT / 32; ++q) v += red[q];
+    w[i] = __dmul_rn(s[i], v);
+  }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -906,7 +939,7 @@ int fagp_factor_inv(const double* packed, const fagp_basis* basis, const double*
     if (pivot_out) *pivot_out = info_h;
     return FAGP_ENOTPD;
   }
-  sym_gemv_scaled_kernel<<<unsigned(ceil_div(m, 8)), 256, 0, s>>>(D, m, sqrt_lam, t, w);
+  sym_gemv_scaled_kernel<<<unsigned(m), kGemvNT, 0, s>>>(D, m, sqrt_lam, t, w);
   FAGP_LAUNCH_CHECK();
   if (predict_op) {
     rc = modal::build_predict_op(D, sqrt_lam, w, basis, predict_op, ws.Lp, ws.X, s);
@@ -947,7 +980,7 @@ int fagp_factor_inv_async(const double* packed, const fagp_basis* basis, const d
   rc = chol_inverse_persistent(A, m, m, ws.info, ws.chol, ws.D, Ainv, m, s);
   if (rc) return rc;
   FAGP_CUDA_TRY(cudaMemcpyAsync(info_host, ws.info, sizeof(int), cudaMemcpyDeviceToHost, s));
-  sym_gemv_scaled_kernel<<<unsigned(ceil_div(m, 8)), 256, 0, s>>>(Ainv, m, sqrt_lam, t, w);
+  sym_gemv_scaled_kernel<<<unsigned(m), kGemvNT, 0, s>>>(Ainv, m, sqrt_lam, t, w);
   FAGP_LAUNCH_CHECK();
   if (predict_op) {
     rc = modal::build_predict_op(Ainv, sqrt_lam, w, basis, predict_op, ws.Lp, ws.X, s);

@@ -106,6 +106,7 @@ __device__ __forceinline__ double gather_prod(const double* row, const int (&off
 constexpr int kGramW = 16;
 constexpr int kGramNT = kGramW * 32;
 constexpr int kGR = 128;                // rows per block (32 k-steps): one barrier per 128 rows
+constexpr int kSR = 256;                // rows per block of the split kernel (one slab, 2 rows per producer)
 
 struct GPlan {
   int p, M, L, LC;
@@ -115,7 +116,8 @@ struct GPlan {
   int JK, JT;          // m-fragments per warp
   int64_t Klen, len;   // output layout [K (KA*KB) | t (TA*TB = m)]
   int64_t plen;        // one partial: (kmf NFK + tmf NFT) fragments of 64 doubles
-  int64_t rows_per_cta;  // multiple of kGR
+  int br;                // rows per block (kGR, or kSR for the split kernel)
+  int64_t rows_per_cta;  // multiple of br
   int S;                 // sub-ranges per CTA = chunks a host pipeline may launch separately
   int grid, nparts;      // nparts = grid * S * G partials
   HermCoef hc;           // recurrence coefficients (constant-bank operands)
@@ -342,62 +344,85 @@ fused_gram_kernel(const double* __restrict__ X, const double* __restrict__ y, do
 // m-fragments, role 2 warps JK2 K2, JT2 T2 and JT1B T1 m-fragments (fragment ids strided by the
 // role's warp count), 9 DMMA per warp per k-step each.  Production, blocks, sub-ranges and the
 // partial flush are those of fused_gram_kernel.
-template <int JK1, int JT1A, int JK2, int JT2, int JT1B>
+template <int JK1, int JT1A, int JK2, int JT2, int JT1B, int BR>
 __global__ void __launch_bounds__(kGramNT, 1)
 fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__ y, double c, int64_t N,
                         BasisView b, const GPlan pl, int k0, int k1, double* __restrict__ ws, uint32_t* flags) {
   extern __shared__ double sm[];
   constexpr int p = 3;
+  // BR = kGR: two slabs, block n + 1 produced while block n is contracted; BR = kSR: one slab of
+  // 256 rows, each producer thread evaluating two rows in lockstep (two independent recurrence
+  // chains hide each other's FP64 latency), then a barrier, then 64 k-steps
+  constexpr int PR = BR / kGR;
+  constexpr int NSLAB = PR == 1 ? 2 : 1;
   const RowLayout rl = row_layout(p, pl.M);
-  double* slabs = sm;  // [2][kGR * bw]
+  double* slabs = sm;  // [NSLAB][BR * bw]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int M = pl.M, L = pl.L;
   const int cta = int(blockIdx.x);
-  const int bpc = int(pl.rows_per_cta / kGR);
+  const int bpc = int(pl.rows_per_cta / BR);
   auto sb = [&](int k) { return int(int64_t(k) * bpc / pl.S); };
   const int g0 = sb(k0);
   const int nblk = sb(k1) - g0;
-  auto blk_base = [&](int j) -> int64_t { return int64_t(cta) * pl.rows_per_cta + int64_t(g0 + j) * kGR; };
-  auto blk_end = [&](int j) -> int64_t { return tmin<int64_t>(N, blk_base(j) + kGR); };
+  auto blk_base = [&](int j) -> int64_t { return int64_t(cta) * pl.rows_per_cta + int64_t(g0 + j) * BR; };
+  auto blk_end = [&](int j) -> int64_t { return tmin<int64_t>(N, blk_base(j) + BR); };
   bool bad_x = false;
   const bool plane = tid < kGR * p;
   const int prow = tid / p, pdim = tid - (tid / p) * p;
   struct Pre {
-    double x, y;
+    double x[PR], y[PR];
   };
   auto load_pre = [&](int j, Pre& pr) {
-    const int64_t r = blk_base(j) + prow;
-    const bool ok = plane && r < blk_end(j);
-    pr.x = ok ? X[r * p + pdim] : 0.0;
-    pr.y = (ok && y != nullptr && pdim == p - 1) ? y[r] : c;
+#pragma unroll
+    for (int t = 0; t < PR; ++t) {
+      const int64_t r = blk_base(j) + prow + t * kGR;
+      const bool ok = plane && r < blk_end(j);
+      pr.x[t] = ok ? X[r * p + pdim] : 0.0;
+      pr.y[t] = (ok && y != nullptr && pdim == p - 1) ? y[r] : c;
+    }
   };
   auto produce = [&](const Pre& pr, int j, double* slab) {
     if (!plane) return;
-    double* row = slab + prow * rl.bw;
-    const bool valid = blk_base(j) + prow < blk_end(j);
-    if (valid) {
-      bad_x |= not_finite(pr.x);
-      const double rr = __dsub_rn(pr.y, c);  // r = y - c (posterior.py:229)
-      eval_phi_g_dim_u(pr.x, rr, b, pdim, pl.hc, row + rl.poff + pdim * M, row + rl.goff + pdim * L,
-                       pdim == p - 1 ? row + rl.rpoff : nullptr);
-    } else {
-      for (int k = 0; k < M; ++k) row[rl.poff + pdim * M + k] = 0.0;
-      for (int k = 0; k < L; ++k) row[rl.goff + pdim * L + k] = 0.0;
-      if (pdim == p - 1)
-        for (int k = 0; k < M; ++k) row[rl.rpoff + k] = 0.0;
+    double rr[PR];
+    int dd[PR];
+    double *ophi[PR], *og[PR], *orphi[PR];
+    bool valid[PR];
+#pragma unroll
+    for (int t = 0; t < PR; ++t) {
+      double* row = slab + (prow + t * kGR) * rl.bw;
+      valid[t] = blk_base(j) + prow + t * kGR < blk_end(j);
+      if (valid[t]) bad_x |= not_finite(pr.x[t]);
+      rr[t] = __dsub_rn(pr.y[t], c);  // r = y - c (posterior.py:229)
+      dd[t] = pdim;
+      ophi[t] = row + rl.poff + pdim * M;
+      og[t] = row + rl.goff + pdim * L;
+      orphi[t] = pdim == p - 1 ? row + rl.rpoff : nullptr;
+      if (pdim == 0) {
+        row[rl.one] = 1.0;
+        row[rl.zero] = 0.0;
+      }
     }
-    if (pdim == 0) {
-      row[rl.one] = 1.0;
-      row[rl.zero] = 0.0;
+    eval_phi_g_dim_uT<PR>(pr.x, rr, b, dd, pl.hc, ophi, og, orphi);  // padding rows: x = 0, then zeroed
+#pragma unroll
+    for (int t = 0; t < PR; ++t) {
+      if (valid[t]) continue;
+      for (int k = 0; k < M; ++k) ophi[t][k] = 0.0;
+      for (int k = 0; k < L; ++k) og[t][k] = 0.0;
+      if (orphi[t])
+        for (int k = 0; k < M; ++k) orphi[t][k] = 0.0;
     }
   };
   __syncthreads();
   Pre pre;
-  if (nblk > 0) {
-    load_pre(0, pre);
-    produce(pre, 0, slabs);
+  if constexpr (NSLAB == 2) {
+    if (nblk > 0) {
+      load_pre(0, pre);
+      produce(pre, 0, slabs);
+    }
+    if (nblk > 1) load_pre(1, pre);
+  } else {
+    if (nblk > 0) load_pre(0, pre);
   }
-  if (nblk > 1) load_pre(1, pre);
 
   // A-operand offsets of an m-fragment: 2 factors; invalid columns -> (0, 1)
   const int col = lane >> 2;
@@ -515,13 +540,21 @@ fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__
     }
   };
   for (int n = 0; n < nblk; ++n) {
-    const double* cur = slabs + (n & 1) * (kGR * rl.bw);
-    if (n + 1 < nblk) {
-      produce(pre, n + 1, slabs + ((n + 1) & 1) * (kGR * rl.bw));
-      if (n + 2 < nblk) load_pre(n + 2, pre);
+    const double* cur;
+    if constexpr (NSLAB == 2) {
+      cur = slabs + (n & 1) * (BR * rl.bw);
+      if (n + 1 < nblk) {
+        produce(pre, n + 1, slabs + ((n + 1) & 1) * (BR * rl.bw));
+        if (n + 2 < nblk) load_pre(n + 2, pre);
+      }
+    } else {
+      cur = slabs;
+      produce(pre, n, slabs);
+      if (n + 1 < nblk) load_pre(n + 1, pre);
+      __syncthreads();
     }
 #pragma unroll 2
-    for (int i = 0; i < kGR / 4; ++i) kstep(cur, i);
+    for (int i = 0; i < BR / 4; ++i) kstep(cur, i);
     for (int k = k0; k < k1; ++k)
       if (g0 + n + 1 == sb(k + 1)) flush(k);
     __syncthreads();
@@ -531,12 +564,15 @@ fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__
 
 // out[e] = sum over the partials (fixed order: deterministic) of entry e of [K | t], read from
 // the fragment-major partial layout; non-finite -> PHI flag
-__global__ void partial_sum_kernel(const double* __restrict__ ws, const GPlan pl, double* __restrict__ out,
-                                   uint32_t* flags) {
+constexpr int kPSE = 32, kPSG = 16;  // partial_sum: entries per CTA x partial groups
+__global__ void __launch_bounds__(kPSE * kPSG) partial_sum_kernel(const double* __restrict__ ws, const GPlan pl,
+                                                                  double* __restrict__ out, uint32_t* flags) {
+  __shared__ double red[kPSG][kPSE];
   const int NFK = int(ceil_div(pl.KB, 8)), NFT = int(ceil_div(pl.TB, 8));
-  bool bad = false;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < pl.len;
-       e += int64_t(gridDim.x) * blockDim.x) {
+  const int grp = int(threadIdx.x) / kPSE, el = int(threadIdx.x) % kPSE;
+  const int64_t e = int64_t(blockIdx.x) * kPSE + el;
+  double s = 0.0;
+  if (e < pl.len) {
     int64_t m, n, frag;
     if (pl.split) {
       if (e < pl.Klen) {
@@ -572,21 +608,28 @@ __global__ void partial_sum_kernel(const double* __restrict__ ws, const GPlan pl
       frag = int64_t(pl.kmf) * NFK + (m >> 3) * NFT + (n >> 3);
     }
     const int64_t idx = frag * 64 + ((m & 7) * 4 + ((n & 7) >> 1)) * 2 + (n & 1);
-    // loads batched 16 at a time (latency-bound otherwise); the sum stays in partial order
-    double s = 0.0;
-    int q = 0;
-    for (; q + 16 <= pl.nparts; q += 16) {
-      double v[16];
+    // group grp sums partials [q0, q1) in order (loads batched 8 at a time: latency-bound
+    // otherwise); the kPSG group sums are then added in group order -- a fixed order
+    const int q0 = int(int64_t(grp) * pl.nparts / kPSG), q1 = int(int64_t(grp + 1) * pl.nparts / kPSG);
+    int q = q0;
+    for (; q + 8 <= q1; q += 8) {
+      double v[8];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) v[u] = ws[int64_t(q + u) * pl.plen + idx];
+      for (int u = 0; u < 8; ++u) v[u] = ws[int64_t(q + u) * pl.plen + idx];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) s += v[u];
+      for (int u = 0; u < 8; ++u) s += v[u];
     }
-    for (; q < pl.nparts; ++q) s += ws[int64_t(q) * pl.plen + idx];
-    out[e] = s;
-    bad |= not_finite(s);
+    for (; q < q1; ++q) s += ws[int64_t(q) * pl.plen + idx];
   }
-  if (bad) raise_flag(flags, FAGP_FLAG_PHI_NONFINITE);
+  red[grp][el] = s;
+  __syncthreads();
+  if (grp == 0 && e < pl.len) {
+    double t = red[0][el];
+#pragma unroll
+    for (int g = 1; g < kPSG; ++g) t += red[g][el];
+    out[e] = t;
+    if (not_finite(t)) raise_flag(flags, FAGP_FLAG_PHI_NONFINITE);
+  }
 }
 
 static int64_t ipow(int64_t b, int e) {
@@ -637,21 +680,28 @@ static bool make_gplan(int64_t N, int p, int M, GPlan& pl) {
   const RowLayout rl = row_layout(p, M);
   const size_t smem = (size_t(2) * pl.LC + size_t(2) * kGR * rl.bw) * sizeof(double);
   if (smem > 225 * 1024) return false;
+  // split layout (fused_gram_split_kernel): p = 3, M = 10 (the BASELINE C3 shape)
+  const char* se = getenv("FAGP_GRAM_SPLIT");
+  const bool split = p == 3 && M == 10 && !(se && se[0] == '0');
+  pl.br = kGR;
+  if (split) {
+    const char* be = getenv("FAGP_GRAM_BR");  // tuning knob: 128 = double-buffered 128-row slabs
+    pl.br = (be && atoi(be) == kGR) ? kGR : kSR;
+    if (size_t(pl.br) * rl.bw * sizeof(double) > 225 * 1024) pl.br = kGR;
+  }
   // rows: one CTA per SM, each a contiguous range of S sub-ranges (S = 4 once every sub-range
   // holds at least 4 blocks, so a host pipeline can upload sub-range k + 1 of every CTA while
   // the Gram contracts sub-range k)
-  const int64_t blocks = tmax<int64_t>(1, ceil_div(N, kGR));
+  const int64_t blocks = tmax<int64_t>(1, ceil_div(N, pl.br));
   pl.grid = int(tmin<int64_t>(num_sms(), blocks));
   const int64_t bpc = ceil_div(blocks, pl.grid);  // blocks per CTA
   pl.S = bpc >= 8 ? 4 : 1;
   if (const char* e = getenv("FAGP_GRAM_SUBRANGES")) pl.S = tmax(1, tmin<int>(int(bpc), atoi(e)));  // tuning knob
-  pl.rows_per_cta = bpc * kGR;
+  pl.rows_per_cta = bpc * pl.br;
   pl.grid = int(tmax<int64_t>(1, ceil_div(tmax<int64_t>(N, 1), pl.rows_per_cta)));
   pl.nparts = pl.grid * pl.S * pl.G;
   pl.hc = herm_coef_host();
-  // split layout (fused_gram_split_kernel): p = 3, M = 10 (the BASELINE C3 shape)
-  const char* se = getenv("FAGP_GRAM_SPLIT");
-  if (p == 3 && M == 10 && !(se && se[0] == '0')) {
+  if (split) {
     pl.split = 1;
     pl.W1 = 12;
     pl.R = pl.L - 16;
@@ -672,7 +722,7 @@ static bool make_gplan(int64_t N, int p, int M, GPlan& pl) {
 }
 
 static size_t gram_smem(const GPlan& pl) {
-  if (pl.split) return size_t(2) * kGR * row_layout(pl.p, pl.M).bw * sizeof(double);
+  if (pl.split) return size_t(pl.br == kGR ? 2 : 1) * pl.br * row_layout(pl.p, pl.M).bw * sizeof(double);
   return (size_t(2) * pl.LC + size_t(2) * kGR * row_layout(pl.p, pl.M).bw) * sizeof(double);
 }
 
@@ -730,9 +780,9 @@ int upload_chunk(const double* Xh, const double* yh, int64_t N, int p, int M, in
     return FAGP_OK;
   }
   if (k < 0 || k >= pl.S) return FAGP_EINVAL;
-  const int64_t bpc = pl.rows_per_cta / kGR;
-  const int64_t off = (int64_t(k) * bpc / pl.S) * kGR;
-  const int64_t sub_rows = ((int64_t(k + 1) * bpc / pl.S) * kGR) - off;
+  const int64_t bpc = pl.rows_per_cta / pl.br;
+  const int64_t off = (int64_t(k) * bpc / pl.S) * pl.br;
+  const int64_t sub_rows = ((int64_t(k + 1) * bpc / pl.S) * pl.br) - off;
   // CTAs c with c rpc + off + sub_rows <= N
   const int64_t head = N - off - sub_rows;
   const int64_t full = head < 0 ? 0 : tmin<int64_t>(pl.grid, head / pl.rows_per_cta + 1);
@@ -765,7 +815,7 @@ int gram(const double* X, const double* y, double c, int64_t N, const fagp_basis
   int rc;
   if (pl.split) {
     const size_t smem = gram_smem(pl);
-    auto kern = fused_gram_split_kernel<4, 1, 2, 1, 1>;
+    auto kern = pl.br == kGR ? fused_gram_split_kernel<4, 1, 2, 1, 1, kGR> : fused_gram_split_kernel<4, 1, 2, 1, 1, kSR>;
     FAGP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     kern<<<pl.grid, kGramNT, smem, s>>>(X, y, c, N, view(b), pl, k0, k1, w, flags);
     rc = FAGP_OK;
@@ -778,8 +828,7 @@ int gram(const double* X, const double* y, double c, int64_t N, const fagp_basis
   if (rc) return rc;
   FAGP_LAUNCH_CHECK();
   if (k1 == pl.S) {
-    const int grid = int(tmax<int64_t>(1, tmin<int64_t>(ceil_div(pl.len, 256), 4 * num_sms())));
-    partial_sum_kernel<<<grid, 256, 0, s>>>(w, pl, out, flags);
+    partial_sum_kernel<<<unsigned(ceil_div(pl.len, kPSE)), kPSE * kPSG, 0, s>>>(w, pl, out, flags);
     FAGP_LAUNCH_CHECK();
   }
   return FAGP_OK;

@@ -314,21 +314,69 @@ __device__ __forceinline__ int64_t h_index(int64_t i, int64_t j, int p, int M, i
   return key;
 }
 
+// one CTA per row i (grid-stride), threads over j; the per-dimension pair keys come from a shared
+// M x M table (M <= 64; computed inline beyond) and 32-bit digit arithmetic
 __global__ void pair_system_kernel(const double* __restrict__ H, const double* __restrict__ s, double sigma2,
                                    double jit, BasisView b, int P, double* __restrict__ A, double* __restrict__ G) {
-  const int64_t m = b.m, total = m * m;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
-       e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t i = e / m, j = e - (e / m) * m;
-    const double g = H[h_index(i, j, b.p, b.M, P)];
-    if (G) G[e] = g;
-    if (A) {
-      double a = __dmul_rn(__dmul_rn(s[i], g), s[j]);
-      if (i == j) {
-        a = __dadd_rn(a, sigma2);
-        if (jit != 0.0) a = __dadd_rn(a, jit);
+  constexpr int kTab = 64;
+  __shared__ int pk[kTab * kTab];
+  const int M = b.M, p = b.p;
+  const int64_t m = b.m;
+  const bool tab = M <= kTab;
+  auto pkey = [&](int a, int c) {
+    const int lo = a < c ? a : c, hi = a < c ? c : a;
+    return lo * M - lo * (lo - 1) / 2 + (hi - lo);
+  };
+  if (tab)
+    for (int e = threadIdx.x; e < M * M; e += blockDim.x) pk[e] = pkey(e / M, e % M);
+  __syncthreads();
+  for (int64_t i = blockIdx.x; i < m; i += gridDim.x) {
+    int di[FAGP_MAX_P];
+    {
+      int64_t q = i;
+      for (int d = p - 1; d >= 0; --d) {
+        di[d] = int(q % M);
+        q /= M;
       }
-      A[e] = a;
+    }
+    const double si = s ? s[i] : 1.0;
+    // 4 columns per thread per pass: keys first, then the 4 gathers in flight together
+    for (int64_t jb = threadIdx.x; jb < m; jb += 4 * int64_t(blockDim.x)) {
+      int64_t key[4];
+      double g[4], sj[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t j = jb + u * int64_t(blockDim.x);
+        unsigned q = unsigned(j < m ? j : 0);
+        int64_t k = 0, pw = 1;
+        for (int d = p - 1; d >= 0; --d) {
+          const unsigned c = q % unsigned(M);
+          q /= unsigned(M);
+          k += pw * (tab ? pk[di[d] * M + int(c)] : pkey(di[d], int(c)));
+          pw *= P;
+        }
+        key[u] = k;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t j = jb + u * int64_t(blockDim.x);
+        g[u] = H[key[u]];
+        sj[u] = (A && j < m) ? s[j] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t j = jb + u * int64_t(blockDim.x);
+        if (j >= m) continue;
+        if (G) G[i * m + j] = g[u];
+        if (A) {
+          double a = __dmul_rn(__dmul_rn(si, g[u]), sj[u]);
+          if (i == j) {
+            a = __dadd_rn(a, sigma2);
+            if (jit != 0.0) a = __dadd_rn(a, jit);
+          }
+          A[i * m + j] = a;
+        }
+      }
     }
   }
 }
@@ -336,10 +384,9 @@ __global__ void pair_system_kernel(const double* __restrict__ H, const double* _
 // ---------------------------------------------------------------------------------------
 // KM4: Ct[pi] (canonical pair order, first dimension slowest) = sum over the orderings of every
 // pi_d of (s_j D_jj') s_j' (or D_jj' when s is NULL).
-__global__ void ctilde_kernel(const double* __restrict__ D, int64_t ldd, const double* __restrict__ s, BasisView b,
-                              int P, int64_t Hlen, double* __restrict__ Ct) {
-  const int M = b.M, p = b.p;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < Hlen; e += int64_t(gridDim.x) * blockDim.x) {
+__device__ __forceinline__ double ctilde_entry(int64_t e, const double* __restrict__ D, int64_t ldd,
+                                               const double* __restrict__ s, int M, int p, int P) {
+  {
     int lo[FAGP_MAX_P], hi[FAGP_MAX_P];
     int64_t q = e;
     for (int d = p - 1; d >= 0; --d) {
@@ -365,7 +412,166 @@ __global__ void ctilde_kernel(const double* __restrict__ D, int64_t ldd, const d
       }
       v += s ? __dmul_rn(__dmul_rn(s[j], D[j * ldd + jj]), s[jj]) : D[j * ldd + jj];
     }
-    Ct[e] = v;
+    return v;
+  }
+}
+
+__global__ void ctilde_kernel(const double* __restrict__ D, int64_t ldd, const double* __restrict__ s, BasisView b,
+                              int P, int64_t Hlen, double* __restrict__ Ct) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < Hlen; e += int64_t(gridDim.x) * blockDim.x)
+    Ct[e] = ctilde_entry(e, D, ldd, s, b.M, b.p, P);
+}
+
+// ---------------------------------------------------------------------------------------
+// p = 3 fused mode products (one launch instead of three, intermediates in shared memory).
+// Small shared-memory products out[r][c] = sum_i A(r, i) B(c, i), i in order, 2 x 2 outputs per
+// thread (four independent fma chains; latency-bound otherwise).
+__device__ __forceinline__ void smem_nt(double* out, int ldo, const double* A, int sar, int sai, const double* B,
+                                        int sbc, int sbi, int R, int C, int K, int tid, int nt) {
+  const int nC = (C + 1) >> 1, tiles = ((R + 1) >> 1) * nC;
+  for (int t = tid; t < tiles; t += nt) {
+    const int r0 = (t / nC) * 2, c0 = (t - (t / nC) * nC) * 2;
+    const int r1 = r0 + 1 < R ? r0 + 1 : r0, c1 = c0 + 1 < C ? c0 + 1 : c0;
+    double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0;
+#pragma unroll 4
+    for (int i = 0; i < K; ++i) {
+      const double x0 = A[r0 * sar + i * sai], x1 = A[r1 * sar + i * sai];
+      const double y0 = B[c0 * sbc + i * sbi], y1 = B[c1 * sbc + i * sbi];
+      a00 = fma(x0, y0, a00);
+      a01 = fma(x0, y1, a01);
+      a10 = fma(x1, y0, a10);
+      a11 = fma(x1, y1, a11);
+    }
+    out[r0 * ldo + c0] = a00;
+    if (c0 + 1 < C) out[r0 * ldo + c0 + 1] = a01;
+    if (r0 + 1 < R) {
+      out[(r0 + 1) * ldo + c0] = a10;
+      if (c0 + 1 < C) out[(r0 + 1) * ldo + c0 + 1] = a11;
+    }
+  }
+}
+
+constexpr int kModeSplit = 4;  // CTAs per leading pair index
+
+// expand3: CTA (pi0, s) computes H[pi0][pi1][.] for its quarter of pi1 from K, with the stage
+// order and per-output fma order of the three mode_kernel launches of expand() (bitwise the same H):
+//   T1[k1][k2] = sum_k0 K[k0][k1][k2] V[pi0][k0];  T2[pi1][k2] = sum_k1 T1[k1][k2] V[pi1][k1];
+//   H[pi0][pi1][pi2] = sum_k2 T2[pi1][k2] V[pi2][k2]
+__global__ void __launch_bounds__(256) expand3_kernel(const double* __restrict__ K, const double* __restrict__ Vg,
+                                                      int P, int L, double* __restrict__ H) {
+  extern __shared__ double sm[];
+  double* V = sm;              // [P][L]
+  double* T1 = V + P * L;      // [L][L]
+  double* T2 = T1 + L * L;     // [P][L] (rows of this CTA)
+  const int pi0 = int(blockIdx.x), tid = int(threadIdx.x), nt = int(blockDim.x);
+  const int j0 = int(blockIdx.y) * P / kModeSplit, j1 = (int(blockIdx.y) + 1) * P / kModeSplit;
+  for (int e = tid; e < P * L; e += nt) V[e] = Vg[e];
+  __syncthreads();
+  for (int c = tid; c < L * L; c += nt) {
+    double acc = 0.0;
+    int i = 0;
+    for (; i + 4 <= L; i += 4) {
+      double k[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) k[u] = K[int64_t(i + u) * L * L + c];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc = fma(k[u], V[pi0 * L + i + u], acc);
+    }
+    for (; i < L; ++i) acc = fma(K[int64_t(i) * L * L + c], V[pi0 * L + i], acc);
+    T1[c] = acc;
+  }
+  __syncthreads();
+  // T2[j][c] = sum_i T1[i][c] V[j][i]  (rows j in [j0, j1))
+  smem_nt(T2, L, V + j0 * L, L, 1, T1, 1, L, j1 - j0, L, L, tid, nt);
+  __syncthreads();
+  // H[pi0][j][q] = sum_i T2[j][i] V[q][i]
+  smem_nt(H + (int64_t(pi0) * P + j0) * P, P, T2, L, 1, V, L, 1, j1 - j0, P, L, tid, nt);
+}
+
+// ctc3 (C'' for p = 3, stage 1 of 2): CTA (pi0 = {a0, b0}, s) stages the scaled block
+// B[(x1 x2)][(y1 y2)] = s_j D_jj' s_j' (j = (a0 x1 x2), j' = (b0 y1 y2)) -- the block of
+// (b0, a0) is its transpose (D = X^T X is symmetric; its mirrored entries are not re-read) -- folds it to
+//   Ct[pi0][pi1][pi2] = (1 + [a0 != b0]) sum over the orderings of pi1, pi2 of B
+// and contracts the last two pair indices for its quarter of k2:
+//   W1[pi1][k2] = sum_pi2 Ct[pi0][pi1][pi2] V[pi2][k2];  Z[pi0][k1][k2] = sum_pi1 V[pi1][k1] W1[pi1][k2]
+__global__ void __launch_bounds__(256) ctc3_kernel(const double* __restrict__ D, int64_t ldd,
+                                                   const double* __restrict__ s, BasisView b, int P,
+                                                   double* __restrict__ Z) {
+  extern __shared__ double sm[];
+  const int M = b.M, L = modal_L(M), M2 = M * M;
+  double* V = sm;           // [P][L]
+  double* Ct = V + P * L;   // [P][P]
+  double* W1 = Ct + P * P;  // [P][L] (columns of this CTA, ld L)
+  double* B = W1 + P * L;   // [M2][M2]
+  const int pi0 = int(blockIdx.x), tid = int(threadIdx.x), nt = int(blockDim.x);
+  const int k0 = int(blockIdx.y) * L / kModeSplit, k1 = (int(blockIdx.y) + 1) * L / kModeSplit;
+  int a0, b0;
+  pair_decode(pi0, M, a0, b0);
+  const double* Vg = b.modal();
+  for (int e = tid; e < P * L; e += nt) V[e] = Vg[e];
+  // the block, 8 loads per thread in flight (one L2 round trip per 8 entries, not per entry)
+  for (int e0 = tid; e0 < M2 * M2; e0 += 8 * nt) {
+    double d[8], sa[8], sb[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * nt < M2 * M2 ? e0 + u * nt : 0;
+      const int r = e / M2, c = e - (e / M2) * M2;
+      const int64_t j = int64_t(a0) * M2 + r, jj = int64_t(b0) * M2 + c;
+      d[u] = D[j * ldd + jj];
+      sa[u] = s ? s[j] : 1.0;
+      sb[u] = s ? s[jj] : 1.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (e0 + u * nt < M2 * M2) B[e0 + u * nt] = s ? __dmul_rn(__dmul_rn(sa[u], d[u]), sb[u]) : d[u];
+  }
+  __syncthreads();
+  const double f0 = a0 != b0 ? 2.0 : 1.0;
+  for (int e = tid; e < P * P; e += nt) {
+    int l1, h1, l2, h2;
+    pair_decode(e / P, M, l1, h1);
+    pair_decode(e - (e / P) * P, M, l2, h2);
+    double v = B[(l1 * M + l2) * M2 + h1 * M + h2];
+    if (l2 != h2) v += B[(l1 * M + h2) * M2 + h1 * M + l2];
+    if (l1 != h1) {
+      v += B[(h1 * M + l2) * M2 + l1 * M + h2];
+      if (l2 != h2) v += B[(h1 * M + h2) * M2 + l1 * M + l2];
+    }
+    Ct[e] = f0 * v;
+  }
+  __syncthreads();
+  // W1[a][k] = sum_i Ct[a][i] V[i][k]  (k in [k0, k1))
+  smem_nt(W1 + k0, L, Ct, P, 1, V + k0, 1, L, P, k1 - k0, P, tid, nt);
+  __syncthreads();
+  // Z[pi0][q][k] = sum_i V[i][q] W1[i][k]
+  smem_nt(Z + int64_t(pi0) * L * L + k0, L, V, 1, L, W1 + k0, 1, L, L, k1 - k0, P, tid, nt);
+}
+
+// ctc3 stage 2: C''[k0][k1 k2] = sum_pi0 V[pi0][k0] Z[pi0][k1 k2], written straight into the
+// padded predict-operand layout op[kap][nu] (canonical index nu KR + kap), zeros in the padding
+__global__ void ctc3_op_kernel(const double* __restrict__ Z, const double* __restrict__ Vg, int P, int L, Plan pl,
+                               double* __restrict__ op) {
+  const int64_t total = pl.KP * pl.NP;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t kap = e / pl.NP, nu = e - (e / pl.NP) * pl.NP;
+    double acc = 0.0;
+    if (kap < pl.KR && nu < pl.NR) {
+      const int64_t c = nu * pl.KR + kap;
+      const int k0 = int(c / (L * L)), k12 = int(c - int64_t(k0) * L * L);
+      int i = 0;
+      for (; i + 16 <= P; i += 16) {
+        double z[16], v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          z[u] = Z[int64_t(i + u) * L * L + k12];
+          v[u] = Vg[(i + u) * L + k0];
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) acc = fma(v[u], z[u], acc);
+      }
+      for (; i < P; ++i) acc = fma(Vg[i * L + k0], Z[int64_t(i) * L * L + k12], acc);
+    }
+    op[e] = acc;
   }
 }
 
@@ -760,10 +966,23 @@ static int launch_mode(const double* in, double* out, int64_t pre, int nin, int6
   return FAGP_OK;
 }
 
+static size_t expand3_smem(int P, int L) { return size_t(2 * P * L + L * L) * sizeof(double); }
+static size_t ctc3_smem(int P, int L, int M) {
+  return size_t(2 * P * L + P * P + M * M * M * M) * sizeof(double);
+}
+constexpr size_t kFusedModeSmem = 200 * 1024;
+
 int expand(const double* gram, const fagp_basis* b, double* H, double* tmp, cudaStream_t s) {
   const Plan pl = make_plan(0, b->p, b->M);
   const int p = b->p;
   const double* V = view(b).modal();
+  if (p == 3 && expand3_smem(pl.P, pl.L) <= kFusedModeSmem && !getenv("FAGP_MODE_UNFUSED")) {
+    const size_t smem = expand3_smem(pl.P, pl.L);
+    FAGP_CUDA_TRY(cudaFuncSetAttribute(expand3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    expand3_kernel<<<dim3(unsigned(pl.P), kModeSplit), 256, smem, s>>>(gram, V, pl.P, pl.L, H);
+    FAGP_LAUNCH_CHECK();
+    return FAGP_OK;
+  }
   const double* cur = gram;  // K: [L]^p
   for (int d = 0; d < p; ++d) {
     // [P^d][L][L^(p-1-d)] -> [P^d][P][L^(p-1-d)], B[pi][kappa] = V[pi * L + kappa]
@@ -780,7 +999,7 @@ int system(const double* H, const double* g, const double* sqrt_lam, double sigm
   const Plan pl = make_plan(0, b->p, b->M);
   const int64_t m = b->m;
   if (A || G) {
-    const int grid = int(tmin<int64_t>(ceil_div(m * m, 256), 8 * num_sms()));
+    const int grid = int(tmin<int64_t>(m, 8 * num_sms()));
     pair_system_kernel<<<grid, 256, 0, s>>>(H, sqrt_lam, sigma2, jit, view(b), pl.P, A, G);
     FAGP_LAUNCH_CHECK();
   }
@@ -801,6 +1020,17 @@ int build_predict_op(const double* D, const double* sqrt_lam, const double* w, c
   const Plan pl = make_plan(0, b->p, b->M);
   const int p = b->p;
   const double* V = view(b).modal();
+  if (p == 3 && ctc3_smem(pl.P, pl.L, b->M) <= kFusedModeSmem && !getenv("FAGP_MODE_UNFUSED")) {
+    // Z = S0 [P][L^2]
+    const size_t smem = ctc3_smem(pl.P, pl.L, b->M);
+    FAGP_CUDA_TRY(cudaFuncSetAttribute(ctc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    ctc3_kernel<<<dim3(unsigned(pl.P), kModeSplit), 256, smem, s>>>(D, b->m, sqrt_lam, view(b), pl.P, S0);
+    FAGP_LAUNCH_CHECK();
+    const int grid = int(tmax<int64_t>(1, ceil_div(pl.KP * pl.NP, 128)));
+    ctc3_op_kernel<<<grid, 128, 0, s>>>(S0, V, pl.P, pl.L, pl, op);
+    FAGP_LAUNCH_CHECK();
+    return set_weights(op, w, b, s);
+  }
   {
     const int grid = int(tmax<int64_t>(1, tmin<int64_t>(ceil_div(pl.Hlen, 256), 16 * num_sms())));
     ctilde_kernel<<<grid, 256, 0, s>>>(D, b->m, sqrt_lam, view(b), pl.P, pl.Hlen, S0);
