@@ -44,6 +44,7 @@ typedef enum fagp_status {
 /* Device flag bits written by the feature-generating kernels (fagp_read_flags). */
 #define FAGP_FLAG_X_NONFINITE 1u   /* an input coordinate is not finite  (mercer.py:334-335) */
 #define FAGP_FLAG_PHI_NONFINITE 2u /* a feature value is not finite      (mercer.py:371-376) */
+#define FAGP_FLAG_STALLED 4u       /* a pipelined Gram waited > ~2 s for an input chunk signal */
 
 /*
  * Basis description: the truncated tensor-product SE eigenbasis (mercer.py:1-45).
@@ -160,14 +161,27 @@ int fagp_gram_x(const double* X, int64_t N, const fagp_basis* basis, const doubl
  * cut into that many sub-ranges, chunk k contracts sub-range k of every CTA (all SMs busy),
  * and fagp_gram_x_upload_chunk(k) is the matching H2D copy (HOST X_host / y_host, pinned for
  * an asynchronous copy; one 2-D cudaMemcpy per array).  Chunks are issued in order on one
- * stream; the last one writes `gram`.  Bitwise identical to fagp_gram_x (the same per
- * (CTA, sub-range) partials summed in the same fixed order).  Table-path shapes: 1 chunk. */
+ * stream; the last one writes `gram`.  Deterministic (per (CTA, sub-range) partials summed in
+ * a fixed order); equal to fagp_gram_x within rounding (fagp_gram_x keeps one partial per CTA).
+ * Table-path shapes: 1 chunk. */
 int32_t fagp_gram_x_chunks(int64_t N, const fagp_basis* basis);
 int fagp_gram_x_upload_chunk(const double* X_host, const double* y_host, int64_t N, const fagp_basis* basis,
                              int32_t k, double* X, double* y, void* stream);
 int fagp_gram_x_chunk(const double* X, int64_t N, const fagp_basis* basis, const double* y, double mean_const,
                       int32_t k, double* gram, void* workspace, size_t workspace_bytes, uint32_t* flags,
                       void* stream);
+
+/* The pipelined form: ONE fused Gram launch that overlaps the uploads.  Before contracting
+ * sub-range k, its CTAs wait (acquire) for ready[k] != 0; the host issues, on a copy stream,
+ * fagp_gram_x_upload_chunk(k) followed by fagp_gram_x_signal(ready, k) (a 4-byte
+ * stream-ordered H2D copy -- a copy engine, not a kernel, so it runs beside the waiting Gram).
+ * `ready` is fagp_gram_x_chunks(N, basis) zeroed device words; the launch re-arms them (zeroes
+ * them after the Gram).  Bitwise identical to fagp_gram_x.  A signal that never comes raises
+ * FAGP_FLAG_STALLED after ~2 s instead of hanging.  Fused shapes only (else FAGP_EUNSUPPORTED). */
+int fagp_gram_x_pipelined(const double* X, int64_t N, const fagp_basis* basis, const double* y, double mean_const,
+                          uint32_t* ready, double* gram, void* workspace, size_t workspace_bytes, uint32_t* flags,
+                          void* stream);
+int fagp_gram_x_signal(uint32_t* ready, int32_t k, void* stream);
 
 /* Expand a `gram` buffer into the full symmetric G (m x m, nullable) and t (m, nullable).
  * The modal form needs fagp_gram_unpack_workspace_size(basis) bytes of workspace for G. */
@@ -268,6 +282,10 @@ int fagp_predict(const double* Ts, int64_t Ns, const fagp_basis* basis, const do
  * fits shared memory (p <= 4, M <= 24, e.g. BASELINE C2/C3); other shapes evaluate a table
  * into the workspace (fagp_predict_x_workspace_size bytes, 0 on the fused path) and run
  * fagp_predict.  var may be NULL. */
+/* Rows one full wave of the fused predict covers (SMs x rows per block; 0 for table-path
+ * shapes): a host pipeline that predicts in chunks cuts them at multiples of this, so only the
+ * last chunk has a partial wave. */
+int64_t fagp_predict_x_wave_rows(const fagp_basis* basis);
 size_t fagp_predict_x_workspace_size(int64_t Ns, const fagp_basis* basis);
 int fagp_predict_x(const double* Xs, int64_t Ns, const fagp_basis* basis, const double* predict_op,
                    double sigma2, double mean_const, double* mean, double* var, uint32_t* flags,

@@ -27,6 +27,7 @@ FAGP_EUNSUPPORTED = 7
 
 FLAG_X_NONFINITE = 1
 FLAG_PHI_NONFINITE = 2
+FLAG_STALLED = 4  # a pipelined Gram never saw an input chunk's signal
 
 MAX_P = 16
 ABI_VERSION = 1
@@ -75,6 +76,9 @@ SIGNATURES = {
     "fagp_gram_x_chunks": (_I32, [_I64, _BASIS]),
     "fagp_gram_x_upload_chunk": (ctypes.c_int, [_P, _P, _I64, _BASIS, _I32, _P, _P, _P]),
     "fagp_gram_x_chunk": (ctypes.c_int, [_P, _I64, _BASIS, _P, _D, _I32, _P, _P, _SZ, _P, _P]),
+    "fagp_gram_x_pipelined": (ctypes.c_int, [_P, _I64, _BASIS, _P, _D, _P, _P, _P, _SZ, _P, _P]),
+    "fagp_gram_x_signal": (ctypes.c_int, [_P, _I32, _P]),
+    "fagp_predict_x_wave_rows": (_I64, [_BASIS]),
     "fagp_predict_x_workspace_size": (_SZ, [_I64, _BASIS]),
     "fagp_predict_x": (ctypes.c_int, [_P, _I64, _BASIS, _P, _D, _D, _P, _P, _P, _P, _SZ, _P]),
     "fagp_factor_workspace_size": (_SZ, [_I64]),

@@ -126,7 +126,28 @@ struct GPlan {
   int split, W1, R, R2;          // warps in role 1; L - 16; M - 8
   int kmf1, kmf2, tmf1, tmf2;    // m-fragments of K1, K2, T1, T2
   int baseK2, baseT1, baseT2;    // fragment offsets of the sections in a partial
+  // launch mode: once = one partial per (CTA, row group) flushed at the end of the launch
+  // (slot cta G + grp) instead of one per sub-range; ready (nullable) = per-sub-range words a
+  // host pipeline sets non-zero (by a stream-ordered H2D copy) once the sub-range's rows landed
+  int once;
+  const unsigned* ready;
 };
+
+// Wait until *r != 0 (acquire).  Bounded: after ~2 s the STALLED flag is raised and the kernel
+// carries on (garbage results, reported), so a lost signal cannot hang the device.
+__device__ __noinline__ void wait_ready(const unsigned* r, uint32_t* flags) {
+  const long long t0 = clock64();
+  for (;;) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(r) : "memory");
+    if (v) return;
+    if (clock64() - t0 > (4ll << 30)) {
+      raise_flag(flags, FAGP_FLAG_STALLED);
+      return;
+    }
+    __nanosleep(500);
+  }
+}
 
 #ifdef FAGP_GRAM_PROFILE
 __device__ long long g_gram_prof[4];
@@ -170,7 +191,30 @@ fused_gram_kernel(const double* __restrict__ X, const double* __restrict__ y, do
   struct Pre {
     double x, y;
   };
-  auto load_pre = [&](int j, Pre& pr) {
+  // pipelined launch: block j's rows may only be read once its sub-range's ready word is set.
+  // The look-ahead load probes the word; if it is not set yet the load is deferred (pend = j)
+  // and done, waiting, right before block j is produced -- never stalling the contraction of
+  // the block already staged.
+  int seen = k0 - 1;  // last sub-range whose ready word this thread has observed
+  int pend = -1;
+  auto load_pre = [&](int j, Pre& pr, bool block = false) {
+    if (pl.ready && plane) {
+      int k = k0;
+      while (k + 1 < k1 && g0 + j >= sb(k + 1)) ++k;
+      if (k > seen) {
+        if (block) {
+          wait_ready(pl.ready + k, flags);
+        } else {
+          unsigned v;
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(pl.ready + k) : "memory");
+          if (!v) {
+            pend = j;
+            return;
+          }
+        }
+        seen = k;
+      }
+    }
     const int64_t r = blk_base(j) + prow;
     const bool ok = plane && r < blk_end(j);
     pr.x = ok ? X[r * p + pdim] : 0.0;
@@ -199,7 +243,7 @@ fused_gram_kernel(const double* __restrict__ X, const double* __restrict__ y, do
   __syncthreads();
   Pre pre;
   if (nblk > 0) {
-    load_pre(0, pre);
+    load_pre(0, pre, true);
     produce(pre, 0, slabs);
   }
   if (nblk > 1) load_pre(1, pre);
@@ -277,7 +321,7 @@ fused_gram_kernel(const double* __restrict__ X, const double* __restrict__ y, do
   // partial of sub-range k in fragment-major order (coalesced: one 256 B store per fragment
   // half), then restart the accumulators; partial_sum_kernel maps it back to [K | t]
   auto flush = [&](int k) {
-    double* out = ws + ((int64_t(cta) * pl.S + k) * pl.G + grp) * pl.plen;
+    double* out = ws + ((pl.once ? int64_t(cta) : int64_t(cta) * pl.S + k) * pl.G + grp) * pl.plen;
 #pragma unroll
     for (int j = 0; j < JK; ++j) {
       const int mf = wi + pl.WG * j;
@@ -319,10 +363,18 @@ fused_gram_kernel(const double* __restrict__ X, const double* __restrict__ y, do
   for (int n = 0; n < nblk; ++n) {
     const double* cur = slabs + (n & 1) * (kGR * rl.bw);
     if (n + 1 < nblk) {
+      if (pend == n + 1) {
+        load_pre(n + 1, pre, true);
+        pend = -1;
+      }
       GPROF(1, produce(pre, n + 1, slabs + ((n + 1) & 1) * (kGR * rl.bw)); if (n + 2 < nblk) load_pre(n + 2, pre))
     }
     GPROF(0, kloop(cur, 0, nloc))
-    GPROF(2, for (int k = k0; k < k1; ++k) if (g0 + n + 1 == sb(k + 1)) flush(k))
+    if (pl.once) {
+      if (n + 1 == nblk) flush(0);
+    } else {
+      GPROF(2, for (int k = k0; k < k1; ++k) if (g0 + n + 1 == sb(k + 1)) flush(k))
+    }
     GPROF(3, __syncthreads())
   }
 #ifdef FAGP_GRAM_PROFILE
@@ -372,7 +424,30 @@ fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__
   struct Pre {
     double x[PR], y[PR];
   };
-  auto load_pre = [&](int j, Pre& pr) {
+  // pipelined launch: block j's rows may only be read once its sub-range's ready word is set.
+  // The look-ahead load probes the word; if it is not set yet the load is deferred (pend = j)
+  // and done, waiting, right before block j is produced -- never stalling the contraction of
+  // the block already staged.
+  int seen = k0 - 1;  // last sub-range whose ready word this thread has observed
+  int pend = -1;
+  auto load_pre = [&](int j, Pre& pr, bool block = false) {
+    if (pl.ready && plane) {
+      int k = k0;
+      while (k + 1 < k1 && g0 + j >= sb(k + 1)) ++k;
+      if (k > seen) {
+        if (block) {
+          wait_ready(pl.ready + k, flags);
+        } else {
+          unsigned v;
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(pl.ready + k) : "memory");
+          if (!v) {
+            pend = j;
+            return;
+          }
+        }
+        seen = k;
+      }
+    }
 #pragma unroll
     for (int t = 0; t < PR; ++t) {
       const int64_t r = blk_base(j) + prow + t * kGR;
@@ -416,12 +491,12 @@ fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__
   Pre pre;
   if constexpr (NSLAB == 2) {
     if (nblk > 0) {
-      load_pre(0, pre);
+      load_pre(0, pre, true);
       produce(pre, 0, slabs);
     }
     if (nblk > 1) load_pre(1, pre);
   } else {
-    if (nblk > 0) load_pre(0, pre);
+    if (nblk > 0) load_pre(0, pre, true);
   }
 
   // A-operand offsets of an m-fragment: 2 factors; invalid columns -> (0, 1)
@@ -531,7 +606,7 @@ fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__
     }
   };
   auto flush = [&](int k) {
-    double* out = ws + (int64_t(cta) * pl.S + k) * pl.plen;
+    double* out = ws + (pl.once ? int64_t(cta) : int64_t(cta) * pl.S + k) * pl.plen;
 #pragma unroll
     for (int q = 0; q < NACC; ++q) {
       if (fragOf[q] >= 0)
@@ -544,19 +619,31 @@ fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__
     if constexpr (NSLAB == 2) {
       cur = slabs + (n & 1) * (BR * rl.bw);
       if (n + 1 < nblk) {
+        if (pend == n + 1) {
+          load_pre(n + 1, pre, true);
+          pend = -1;
+        }
         produce(pre, n + 1, slabs + ((n + 1) & 1) * (BR * rl.bw));
         if (n + 2 < nblk) load_pre(n + 2, pre);
       }
     } else {
       cur = slabs;
+      if (pend == n) {
+        load_pre(n, pre, true);
+        pend = -1;
+      }
       produce(pre, n, slabs);
       if (n + 1 < nblk) load_pre(n + 1, pre);
       __syncthreads();
     }
 #pragma unroll 2
     for (int i = 0; i < BR / 4; ++i) kstep(cur, i);
-    for (int k = k0; k < k1; ++k)
-      if (g0 + n + 1 == sb(k + 1)) flush(k);
+    if (pl.once) {
+      if (n + 1 == nblk) flush(0);
+    } else {
+      for (int k = k0; k < k1; ++k)
+        if (g0 + n + 1 == sb(k + 1)) flush(k);
+    }
     __syncthreads();
   }
   if (bad_x) raise_flag(flags, FAGP_FLAG_X_NONFINITE);
@@ -622,6 +709,8 @@ __global__ void __launch_bounds__(kPSE * kPSG) partial_sum_kernel(const double* 
     for (; q < q1; ++q) s += ws[int64_t(q) * pl.plen + idx];
   }
   red[grp][el] = s;
+  if (pl.ready && blockIdx.x == 0 && threadIdx.x < unsigned(pl.S))
+    const_cast<unsigned*>(pl.ready)[threadIdx.x] = 0u;  // re-arm for the next pipelined call
   __syncthreads();
   if (grp == 0 && e < pl.len) {
     double t = red[0][el];
@@ -689,13 +778,14 @@ static bool make_gplan(int64_t N, int p, int M, GPlan& pl) {
     pl.br = (be && atoi(be) == kGR) ? kGR : kSR;
     if (size_t(pl.br) * rl.bw * sizeof(double) > 225 * 1024) pl.br = kGR;
   }
-  // rows: one CTA per SM, each a contiguous range of S sub-ranges (S = 4 once every sub-range
-  // holds at least 4 blocks, so a host pipeline can upload sub-range k + 1 of every CTA while
-  // the Gram contracts sub-range k)
+  // rows: one CTA per SM, each a contiguous range of S sub-ranges (S = 4 / 8 once every
+  // sub-range holds at least 2 blocks), so a host pipeline can upload sub-range k + 1 of every
+  // CTA while the Gram contracts sub-range k -- the first chunk, the only upload not hidden
+  // behind the contraction, is 1/S of the rows
   const int64_t blocks = tmax<int64_t>(1, ceil_div(N, pl.br));
   pl.grid = int(tmin<int64_t>(num_sms(), blocks));
   const int64_t bpc = ceil_div(blocks, pl.grid);  // blocks per CTA
-  pl.S = bpc >= 8 ? 4 : 1;
+  pl.S = bpc >= 16 ? 8 : bpc >= 8 ? 4 : 1;
   if (const char* e = getenv("FAGP_GRAM_SUBRANGES")) pl.S = tmax(1, tmin<int>(int(bpc), atoi(e)));  // tuning knob
   pl.rows_per_cta = bpc * pl.br;
   pl.grid = int(tmax<int64_t>(1, ceil_div(tmax<int64_t>(N, 1), pl.rows_per_cta)));
@@ -806,11 +896,25 @@ int upload_chunk(const double* Xh, const double* yh, int64_t N, int p, int M, in
 
 // chunks [k0, k1) of the plan; the last chunk also sums the partials into `out`
 int gram(const double* X, const double* y, double c, int64_t N, const fagp_basis* b, int k0, int k1, double* out,
-         void* ws, size_t ws_bytes, uint32_t* flags, cudaStream_t s) {
+         void* ws, size_t ws_bytes, uint32_t* flags, cudaStream_t s, const unsigned* ready) {
   GPlan pl;
   if (!make_gplan(N, b->p, b->M, pl)) return FAGP_EUNSUPPORTED;
   if (ws == nullptr || ws_bytes < size_t(pl.nparts) * size_t(pl.plen) * sizeof(double)) return FAGP_EWORKSPACE;
   if (k0 < 0 || k1 > pl.S || k0 >= k1) return FAGP_EINVAL;
+  // one launch over every sub-range: one partial per CTA (and row group)
+  pl.once = (k0 == 0 && k1 == pl.S) ? 1 : 0;
+  pl.ready = pl.once ? ready : nullptr;
+  if (pl.ready) {
+    // load partial_sum_kernel now: with lazy module loading its first launch (queued behind a
+    // Gram that is still waiting for its input signals) could block this thread until the
+    // device is idle -- before the caller has issued the signals
+    static bool loaded = false;
+    if (!loaded) {
+      cudaFuncAttributes fa;
+      FAGP_CUDA_TRY(cudaFuncGetAttributes(&fa, partial_sum_kernel));
+      loaded = true;
+    }
+  }
   double* w = static_cast<double*>(ws);
   int rc;
   if (pl.split) {
@@ -828,6 +932,7 @@ int gram(const double* X, const double* y, double c, int64_t N, const fagp_basis
   if (rc) return rc;
   FAGP_LAUNCH_CHECK();
   if (k1 == pl.S) {
+    if (pl.once) pl.nparts = pl.grid * pl.G;
     partial_sum_kernel<<<unsigned(ceil_div(pl.len, kPSE)), kPSE * kPSG, 0, s>>>(w, pl, out, flags);
     FAGP_LAUNCH_CHECK();
   }
@@ -1394,7 +1499,7 @@ int fagp_gram_x_chunk(const double* X, int64_t N, const fagp_basis* basis, const
   if (N < 0 || gram == nullptr || (N > 0 && X == nullptr)) return FAGP_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (fused::gram_eligible(N, basis->p, basis->M))
-    return fused::gram(X, y, mean_const, N, basis, k, k + 1, gram, workspace, workspace_bytes, flags, s);
+    return fused::gram(X, y, mean_const, N, basis, k, k + 1, gram, workspace, workspace_bytes, flags, s, nullptr);
   if (k != 0) return FAGP_EINVAL;
   const size_t table = round_up(size_t(N) * table_width(basis->p, basis->M) * sizeof(double), 256);
   if (workspace == nullptr || workspace_bytes < table + fagp_gram_workspace_size(N, basis)) return FAGP_EWORKSPACE;
@@ -1413,9 +1518,41 @@ int fagp_gram_x(const double* X, int64_t N, const fagp_basis* basis, const doubl
   if (fused::gram_eligible(N, basis->p, basis->M)) {
     if (N < 0 || gram == nullptr || (N > 0 && X == nullptr)) return FAGP_EINVAL;
     return fused::gram(X, y, mean_const, N, basis, 0, fused::gram_chunks(N, basis->p, basis->M), gram, workspace,
-                       workspace_bytes, flags, static_cast<cudaStream_t>(stream));
+                       workspace_bytes, flags, static_cast<cudaStream_t>(stream), nullptr);
   }
   return fagp_gram_x_chunk(X, N, basis, y, mean_const, 0, gram, workspace, workspace_bytes, flags, stream);
+}
+
+int fagp_gram_x_pipelined(const double* X, int64_t N, const fagp_basis* basis, const double* y, double mean_const,
+                          uint32_t* ready, double* gram, void* workspace, size_t workspace_bytes, uint32_t* flags,
+                          void* stream) {
+  int st = check_basis(basis);
+  if (st) return st;
+  if (!fused::gram_eligible(N, basis->p, basis->M)) return FAGP_EUNSUPPORTED;
+  if (N < 0 || gram == nullptr || ready == nullptr || (N > 0 && X == nullptr)) return FAGP_EINVAL;
+  return fused::gram(X, y, mean_const, N, basis, 0, fused::gram_chunks(N, basis->p, basis->M), gram, workspace,
+                     workspace_bytes, flags, static_cast<cudaStream_t>(stream), ready);
+}
+
+int fagp_gram_x_signal(uint32_t* ready, int32_t k, void* stream) {
+  // a stream-ordered 4-byte H2D copy: executed by a copy engine behind the chunk's rows (a
+  // memset would be a kernel, which could not start beside the Gram that waits for it)
+  static uint32_t* one = nullptr;
+  if (one == nullptr) {
+    void* h = nullptr;
+    FAGP_CUDA_TRY(cudaHostAlloc(&h, sizeof(uint32_t), cudaHostAllocPortable));
+    *static_cast<uint32_t*>(h) = 1u;
+    one = static_cast<uint32_t*>(h);
+  }
+  if (ready == nullptr || k < 0) return FAGP_EINVAL;
+  FAGP_CUDA_TRY(cudaMemcpyAsync(ready + k, one, sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                static_cast<cudaStream_t>(stream)));
+  return FAGP_OK;
+}
+
+int64_t fagp_predict_x_wave_rows(const fagp_basis* basis) {
+  if (check_basis(basis) || !fused::predict_eligible(basis->p, basis->M)) return 0;
+  return int64_t(num_sms()) * fused::kPR;
 }
 
 size_t fagp_predict_x_workspace_size(int64_t Ns, const fagp_basis* basis) {

@@ -17,6 +17,8 @@ breakdown (jitter needed) re-runs the factor through the blocking schedule and t
 
 from __future__ import annotations
 
+import os
+
 import ctypes
 
 from . import _device as dev
@@ -25,6 +27,7 @@ from .errors import NumericalError
 from .mercer import LAMBDA_FLOOR_REL, Basis, raise_nonfinite
 
 JITTER_ATTEMPTS = 3  # backend.py:165
+_GPU_TRACE = None  # diagnostics: a list collects [(mark, ms since entry)] per run_host call (CUDA events)
 _TRACE = None  # diagnostics: set to a list to collect run_host phase times in ms (tools/e2e_probe.py)
 
 
@@ -52,6 +55,10 @@ class PosteriorEngine:
         # keeps the Cholesky route (its predict operand is built from L^{-1})
         self.inverse_route = bool(L.fagp_factor_inv(None, b.ref, None, 1.0, 0, None, None, None, None, None, None,
                                                      None, None, 0, None) != _lib.FAGP_EUNSUPPORTED)
+        # fused Gram shapes take the one-launch pipelined upload path in run_host (probe: the
+        # shape check comes before the argument checks)
+        self.pipelined_gram = bool(L.fagp_gram_x_pipelined(None, self.N, b.ref, None, 0.0, None, None, None, 0,
+                                                           None, None) != _lib.FAGP_EUNSUPPORTED)
         self.L = None if self.inverse_route else e(m, m)
         self.Ainv = e(m, m) if self.inverse_route else None
         self.G = e(m, m) if keep_gram else None
@@ -192,7 +199,7 @@ class PosteriorEngine:
             self.set_mean_weights()
 
     # -- the whole step from host memory (the fagp_posterior path) -------------------------
-    PREDICT_CHUNKS = 4
+    PREDICT_CHUNKS = int(os.environ.get("FAGP_PREDICT_CHUNKS", "6"))  # tuning knob
 
     def _host_buffers(self):
         import torch
@@ -239,33 +246,61 @@ class PosteriorEngine:
         trace = [time.perf_counter()] if _TRACE is not None else None
         L, b = _lib.lib(), self.basis
         cs = torch.cuda.current_stream(self.device)
+        gev = [] if _GPU_TRACE is not None else None
+
+        def mark(name, stream):
+            if gev is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(stream)
+                gev.append((name, e))
+
+        mark("start", cs)
         X, y, Xs = self._host_buffers()
         p = b.p
         Xh = self._pinned(Xh, "X", (self.N, p))
         yh = self._pinned(yh, "y", (self.N,))
         Xsh = self._pinned(Xsh, "Xs", (self.Ns, p))
         self.flags.zero_()
-        self.s_in.wait_stream(cs)
         nch = int(L.fagp_gram_x_chunks(self.N, b.ref))
+        ready = self._ready_words(nch)  # (first call: zeroed on cs before s_in is ordered behind it)
+        self.s_in.wait_stream(cs)
         sin = _lib.stream_handle(self.s_in)
-        for k in range(nch):
-            _lib.check(L.fagp_gram_x_upload_chunk(_lib.ptr(Xh), _lib.ptr(yh), self.N, b.ref, k, _lib.ptr(X),
-                                                  _lib.ptr(y), sin), "upload")
-            ev = torch.cuda.Event()
-            ev.record(self.s_in)
-            cs.wait_event(ev)
-            _lib.check(L.fagp_gram_x_chunk(_lib.ptr(X), self.N, b.ref, _lib.ptr(y), self.mean_const, k,
-                                           _lib.ptr(self.packed), _lib.ptr(self.gram_ws), self.gram_ws_bytes,
-                                           self._flag(0), _lib.stream_handle(cs)), "gram")
+        if self.pipelined_gram:
+            # the copy stream uploads chunk k and then sets ready word k (a stream-ordered 4-byte
+            # H2D copy); ONE Gram launch waits on the words chunk by chunk.  The copies are
+            # queued first, so nothing the host does after the launch can hold them back.
+            for k in range(nch):
+                _lib.check(L.fagp_gram_x_upload_chunk(_lib.ptr(Xh), _lib.ptr(yh), self.N, b.ref, k, _lib.ptr(X),
+                                                      _lib.ptr(y), sin), "upload")
+                _lib.check(L.fagp_gram_x_signal(_lib.ptr(ready), k, sin), "signal")
+                mark(f"up{k}", self.s_in)
+            _lib.check(L.fagp_gram_x_pipelined(_lib.ptr(X), self.N, b.ref, _lib.ptr(y), self.mean_const,
+                                               _lib.ptr(ready), _lib.ptr(self.packed), _lib.ptr(self.gram_ws),
+                                               self.gram_ws_bytes, self._flag(0), _lib.stream_handle(cs)), "gram")
+            mark("gram", cs)
+        else:  # table-path shapes: chunk launches behind events
+            for k in range(nch):
+                _lib.check(L.fagp_gram_x_upload_chunk(_lib.ptr(Xh), _lib.ptr(yh), self.N, b.ref, k, _lib.ptr(X),
+                                                      _lib.ptr(y), sin), "upload")
+                ev = torch.cuda.Event()
+                ev.record(self.s_in)
+                mark(f"up{k}", self.s_in)
+                cs.wait_event(ev)
+                _lib.check(L.fagp_gram_x_chunk(_lib.ptr(X), self.N, b.ref, _lib.ptr(y), self.mean_const, k,
+                                               _lib.ptr(self.packed), _lib.ptr(self.gram_ws), self.gram_ws_bytes,
+                                               self._flag(0), _lib.stream_handle(cs)), "gram")
+                mark(f"gram{k}", cs)
         with torch.cuda.stream(self.s_in):
             if self.Ns:
                 Xs.copy_(Xsh, non_blocking=True)
             ev_xs = torch.cuda.Event()
             ev_xs.record(self.s_in)
+        mark("xs_up", self.s_in)
         if trace is not None:
             trace.append(time.perf_counter())
         self.stage_reduce()
         asynchronous = self.stage_factor_async()
+        mark("factor", cs)
         if trace is not None:
             trace.append(time.perf_counter())
         cs.wait_event(ev_xs)
@@ -278,9 +313,7 @@ class PosteriorEngine:
         out, o = self._out_buffer(rows)
         if trace is not None:
             trace.append(time.perf_counter())
-        step = -(-max(self.Ns, 1) // (self.PREDICT_CHUNKS * 64)) * 64
-        for a in range(0, self.Ns, step):
-            e = min(self.Ns, a + step)
+        for ci, (a, e) in enumerate(self._predict_chunks()):
             _lib.check(L.fagp_predict_x(_lib.ptr(Xs[a:e]), e - a, b.ref, _lib.ptr(self.predict_op), self.noise_var,
                                         self.mean_const, _lib.ptr(self.mean[a:e]),
                                         _lib.ptr(self.var[a:e] if self.want_var else None), self._flag(1),
@@ -288,14 +321,18 @@ class PosteriorEngine:
                        "predict")
             ev = torch.cuda.Event()
             ev.record(cs)
+            mark(f"pred{ci}", cs)
             self.s_out.wait_event(ev)
             with torch.cuda.stream(self.s_out):
                 out[0, a:e].copy_(self.mean[a:e], non_blocking=True)
                 if self.want_var:
                     out[1, a:e].copy_(self.var[a:e], non_blocking=True)
+            mark(f"d2h{ci}", self.s_out)
         if trace is not None:
             trace.append(time.perf_counter())
         self.s_out.synchronize()
+        if gev is not None:
+            _GPU_TRACE.append([(n, gev[0][1].elapsed_time(e)) for n, e in gev])
         if trace is not None:
             trace.append(time.perf_counter())
             _TRACE.append([1e3 * (b - a) for a, b in zip(trace, trace[1:])])
@@ -307,6 +344,22 @@ class PosteriorEngine:
             if self.want_var:
                 out[1].copy_(self.var)
         return o[0], (o[1] if self.want_var else None)
+
+    def _predict_chunks(self):
+        """Row ranges of the chunked predict: cut at whole waves of the fused predict (every
+        chunk but the last fills all SMs to the end), else at multiples of 64 rows."""
+        Ns, pc = self.Ns, self.PREDICT_CHUNKS
+        wave = int(_lib.lib().fagp_predict_x_wave_rows(self.basis.ref)) or 64
+        nw = -(-max(Ns, 1) // wave)
+        cuts = sorted({min(Ns, (i * nw // pc) * wave) for i in range(pc + 1)} | {Ns})
+        return [(a, e) for a, e in zip(cuts, cuts[1:]) if e > a]
+
+    def _ready_words(self, n):
+        """Zeroed device words for fagp_gram_x_pipelined (re-armed by the launch itself)."""
+        r = getattr(self, "_ready", None)
+        if r is None or r.numel() != n:
+            r = self._ready = dev.zeros((n,), dtype="int32", device=self.device)
+        return r
 
     def _out_buffer(self, rows):
         """A pinned (rows, N*) result buffer no caller still holds: the returned mean/var are
@@ -334,6 +387,8 @@ class PosteriorEngine:
         fagp_posterior: train X, train Phi, test X, test Phi, then the factorisation)."""
         fl = [int(v) for v in dev.to_host(self.flags)]
         b = self.basis
+        if fl[0] & _lib.FLAG_STALLED:
+            raise RuntimeError("pipelined Gram: an input chunk was never signalled (FAGP_FLAG_STALLED)")
         if fl[0] & _lib.FLAG_X_NONFINITE:
             raise ValueError("X must be finite")
         if fl[0] & _lib.FLAG_PHI_NONFINITE:

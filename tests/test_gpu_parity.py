@@ -408,3 +408,63 @@ def test_async_factor_falls_back_to_the_jitter_schedule():
     assert np.array_equal(got.mean, ref.mean) and np.array_equal(got.var, ref.var)
     dev_in = F.fagp_posterior(DS, torch.from_numpy(Xs).cuda(), model, memory_cap=None, return_device=True)
     assert np.array_equal(dev.to_host(dev_in.mean), ref.mean)
+
+
+@pytest.mark.parametrize("N", [1, 4_097, 300_001])
+def test_pipelined_gram_bitwise_equals_gram_x(N):
+    """fagp_gram_x_pipelined: one launch waiting on per-chunk ready words, the chunks uploaded
+    (in reverse order, to exercise the waits) and signalled from a copy stream -- bitwise the
+    fagp_gram_x buffer, the ready words re-armed, twice in a row."""
+    from paper_2403_12797_b200 import _lib
+    from paper_2403_12797_b200.posterior import gram_x_packed
+
+    rng = np.random.default_rng(N)
+    X = rng.uniform(-1, 1, (N, 3))
+    y = np.cos(X).sum(1) + 0.05 * rng.standard_normal(N)
+    basis = F.Basis(F.ArdKernelParams.isotropic(3, 1.0, 1.0), 10)
+    ref = dev.to_host(gram_x_packed(basis, dev.to_device(X), dev.to_device(y), 0.2))
+    L = _lib.lib()
+    nch = int(L.fagp_gram_x_chunks(N, basis.ref))
+    Xh, yh = torch.from_numpy(X).pin_memory(), torch.from_numpy(y).pin_memory()
+    Xd, yd = dev.empty((N, 3)), dev.empty((N,))
+    ready = dev.zeros((nch,), dtype="int32")
+    flags = dev.zeros((1,), dtype="int32")
+    wsz = int(L.fagp_gram_x_workspace_size(N, basis.ref))
+    ws = dev.empty((max(1, -(-wsz // 8)),))
+    side = torch.cuda.Stream()
+    for _ in range(2):
+        out = dev.empty((int(L.fagp_gram_len(basis.ref)),))
+        side.wait_stream(torch.cuda.current_stream())
+        cs = _lib.stream_handle(torch.cuda.current_stream())
+        _lib.check(L.fagp_gram_x_pipelined(_lib.ptr(Xd), N, basis.ref, _lib.ptr(yd), 0.2, _lib.ptr(ready),
+                                           _lib.ptr(out), _lib.ptr(ws), wsz, _lib.ptr(flags), cs), "pipelined")
+        sin = _lib.stream_handle(side)
+        for k in reversed(range(nch)):
+            _lib.check(L.fagp_gram_x_upload_chunk(_lib.ptr(Xh), _lib.ptr(yh), N, basis.ref, k, _lib.ptr(Xd),
+                                                  _lib.ptr(yd), sin), "upload")
+            _lib.check(L.fagp_gram_x_signal(_lib.ptr(ready), k, sin), "signal")
+        torch.cuda.synchronize()
+        assert int(dev.to_host(flags)[0]) == 0
+        assert np.array_equal(dev.to_host(out), ref)
+        assert not dev.to_host(ready).any()
+
+
+def test_pipelined_gram_without_signal_reports_stall():
+    """A ready word that is never set: the launch gives up after its bounded wait (~2 s) and
+    raises FAGP_FLAG_STALLED instead of hanging the device."""
+    from paper_2403_12797_b200 import _lib
+
+    N = 50_000
+    basis = F.Basis(F.ArdKernelParams.isotropic(3, 1.0, 1.0), 10)
+    L = _lib.lib()
+    nch = int(L.fagp_gram_x_chunks(N, basis.ref))
+    Xd, yd = dev.zeros((N, 3)), dev.zeros((N,))
+    ready = dev.zeros((nch,), dtype="int32")
+    flags = dev.zeros((1,), dtype="int32")
+    wsz = int(L.fagp_gram_x_workspace_size(N, basis.ref))
+    ws = dev.empty((max(1, -(-wsz // 8)),))
+    out = dev.empty((int(L.fagp_gram_len(basis.ref)),))
+    _lib.check(L.fagp_gram_x_pipelined(_lib.ptr(Xd), N, basis.ref, _lib.ptr(yd), 0.0, _lib.ptr(ready), _lib.ptr(out),
+                                       _lib.ptr(ws), wsz, _lib.ptr(flags), None), "pipelined")
+    torch.cuda.synchronize()
+    assert int(dev.to_host(flags)[0]) & _lib.FLAG_STALLED
