@@ -614,6 +614,17 @@ fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__
       acc[q][0] = acc[q][1] = 0.0;
     }
   };
+#ifdef FAGP_GRAM_PROFILE
+  long long tp[4] = {0, 0, 0, 0};  // kloop, produce, flush, barrier (clock64 cycles)
+#define SPROF(i, stmt)              \
+  {                                 \
+    const long long t_ = clock64(); \
+    stmt;                           \
+    tp[i] += clock64() - t_;        \
+  }
+#else
+#define SPROF(i, stmt) stmt;
+#endif
   for (int n = 0; n < nblk; ++n) {
     const double* cur;
     if constexpr (NSLAB == 2) {
@@ -628,24 +639,26 @@ fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__
       }
     } else {
       cur = slabs;
-      if (pend == n) {
+      SPROF(1, if (pend == n) {
         load_pre(n, pre, true);
         pend = -1;
-      }
-      produce(pre, n, slabs);
-      if (n + 1 < nblk) load_pre(n + 1, pre);
-      __syncthreads();
+      } produce(pre, n, slabs);
+      if (n + 1 < nblk) load_pre(n + 1, pre))
+      SPROF(3, __syncthreads())
     }
-#pragma unroll 2
-    for (int i = 0; i < BR / 4; ++i) kstep(cur, i);
+    SPROF(0, _Pragma("unroll 2") for (int i = 0; i < BR / 4; ++i) kstep(cur, i))
     if (pl.once) {
-      if (n + 1 == nblk) flush(0);
+      SPROF(2, if (n + 1 == nblk) flush(0))
     } else {
-      for (int k = k0; k < k1; ++k)
-        if (g0 + n + 1 == sb(k + 1)) flush(k);
+      SPROF(2, for (int k = k0; k < k1; ++k) if (g0 + n + 1 == sb(k + 1)) flush(k))
     }
-    __syncthreads();
+    SPROF(3, __syncthreads())
   }
+#ifdef FAGP_GRAM_PROFILE
+  if (lane == 0)
+    for (int i = 0; i < 4; ++i) atomicAdd(reinterpret_cast<unsigned long long*>(&g_gram_prof[i]), (unsigned long long)tp[i]);
+#endif
+#undef SPROF
   if (bad_x) raise_flag(flags, FAGP_FLAG_X_NONFINITE);
 }
 
