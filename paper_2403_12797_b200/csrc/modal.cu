@@ -451,7 +451,9 @@ __device__ __forceinline__ void smem_nt(double* out, int ldo, const double* A, i
   }
 }
 
-constexpr int kModeSplit = 4;  // CTAs per leading pair index
+constexpr int kModeSplit = 4;  // expand3: CTAs per leading pair index
+constexpr int kCtcSplit = 2;   // ctc3: CTAs per leading pair index (P x 2 = 110 at C3: one wave)
+constexpr int kCtcNT = 512;
 
 // expand3: CTA (pi0, s) computes H[pi0][pi1][.] for its quarter of pi1 from K, with the stage
 // order and per-output fma order of the three mode_kernel launches of expand() (bitwise the same H):
@@ -494,7 +496,7 @@ __global__ void __launch_bounds__(256) expand3_kernel(const double* __restrict__
 //   Ct[pi0][pi1][pi2] = (1 + [a0 != b0]) sum over the orderings of pi1, pi2 of B
 // and contracts the last two pair indices for its quarter of k2:
 //   W1[pi1][k2] = sum_pi2 Ct[pi0][pi1][pi2] V[pi2][k2];  Z[pi0][k1][k2] = sum_pi1 V[pi1][k1] W1[pi1][k2]
-__global__ void __launch_bounds__(256) ctc3_kernel(const double* __restrict__ D, int64_t ldd,
+__global__ void __launch_bounds__(kCtcNT) ctc3_kernel(const double* __restrict__ D, int64_t ldd,
                                                    const double* __restrict__ s, BasisView b, int P,
                                                    double* __restrict__ Z) {
   extern __shared__ double sm[];
@@ -504,7 +506,7 @@ __global__ void __launch_bounds__(256) ctc3_kernel(const double* __restrict__ D,
   double* W1 = Ct + P * P;  // [P][L] (columns of this CTA, ld L)
   double* B = W1 + P * L;   // [M2][M2]
   const int pi0 = int(blockIdx.x), tid = int(threadIdx.x), nt = int(blockDim.x);
-  const int k0 = int(blockIdx.y) * L / kModeSplit, k1 = (int(blockIdx.y) + 1) * L / kModeSplit;
+  const int k0 = int(blockIdx.y) * L / kCtcSplit, k1 = (int(blockIdx.y) + 1) * L / kCtcSplit;
   int a0, b0;
   pair_decode(pi0, M, a0, b0);
   const double* Vg = b.modal();
@@ -549,17 +551,27 @@ __global__ void __launch_bounds__(256) ctc3_kernel(const double* __restrict__ D,
 
 // ctc3 stage 2: C''[k0][k1 k2] = sum_pi0 V[pi0][k0] Z[pi0][k1 k2], written straight into the
 // padded predict-operand layout op[kap][nu] (canonical index nu KR + kap), zeros in the padding
-__global__ void ctc3_op_kernel(const double* __restrict__ Z, const double* __restrict__ Vg, int P, int L, Plan pl,
-                               double* __restrict__ op) {
+constexpr int kOpE = 32, kOpG = 4;  // ctc3_op: entries per CTA x pi0 groups
+__global__ void __launch_bounds__(kOpE * kOpG) ctc3_op_kernel(const double* __restrict__ Z,
+                                                              const double* __restrict__ Vg, int P, int L, Plan pl,
+                                                              double* __restrict__ op) {
+  // group g sums pi0 in [g P / 4, (g + 1) P / 4) with every load in flight, then the 4 group
+  // sums are added in group order (fixed order: deterministic)
+  __shared__ double red[kOpG][kOpE];
+  const int grp = int(threadIdx.x) / kOpE, el = int(threadIdx.x) % kOpE;
   const int64_t total = pl.KP * pl.NP;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+  const int64_t e = int64_t(blockIdx.x) * kOpE + el;
+  double acc = 0.0;
+  bool valid = false;
+  if (e < total) {
     const int64_t kap = e / pl.NP, nu = e - (e / pl.NP) * pl.NP;
-    double acc = 0.0;
-    if (kap < pl.KR && nu < pl.NR) {
+    valid = kap < pl.KR && nu < pl.NR;
+    if (valid) {
       const int64_t c = nu * pl.KR + kap;
       const int k0 = int(c / (L * L)), k12 = int(c - int64_t(k0) * L * L);
-      int i = 0;
-      for (; i + 16 <= P; i += 16) {
+      const int i0 = grp * P / kOpG, i1 = (grp + 1) * P / kOpG;
+      int i = i0;
+      for (; i + 16 <= i1; i += 16) {
         double z[16], v[16];
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
@@ -569,9 +581,27 @@ __global__ void ctc3_op_kernel(const double* __restrict__ Z, const double* __res
 #pragma unroll
         for (int u = 0; u < 16; ++u) acc = fma(v[u], z[u], acc);
       }
-      for (; i < P; ++i) acc = fma(Vg[i * L + k0], Z[int64_t(i) * L * L + k12], acc);
+      {
+        double z[16], v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const bool ok = i + u < i1;
+          z[u] = ok ? Z[int64_t(i + u) * L * L + k12] : 0.0;
+          v[u] = ok ? Vg[(i + u) * L + k0] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (i + u < i1) acc = fma(v[u], z[u], acc);
+      }
     }
-    op[e] = acc;
+  }
+  red[grp][el] = acc;
+  __syncthreads();
+  if (grp == 0 && e < total) {
+    double t = red[0][el];
+#pragma unroll
+    for (int g = 1; g < kOpG; ++g) t += red[g][el];
+    op[e] = valid ? t : 0.0;
   }
 }
 
@@ -1024,10 +1054,10 @@ int build_predict_op(const double* D, const double* sqrt_lam, const double* w, c
     // Z = S0 [P][L^2]
     const size_t smem = ctc3_smem(pl.P, pl.L, b->M);
     FAGP_CUDA_TRY(cudaFuncSetAttribute(ctc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    ctc3_kernel<<<dim3(unsigned(pl.P), kModeSplit), 256, smem, s>>>(D, b->m, sqrt_lam, view(b), pl.P, S0);
+    ctc3_kernel<<<dim3(unsigned(pl.P), kCtcSplit), kCtcNT, smem, s>>>(D, b->m, sqrt_lam, view(b), pl.P, S0);
     FAGP_LAUNCH_CHECK();
-    const int grid = int(tmax<int64_t>(1, ceil_div(pl.KP * pl.NP, 128)));
-    ctc3_op_kernel<<<grid, 128, 0, s>>>(S0, V, pl.P, pl.L, pl, op);
+    ctc3_op_kernel<<<unsigned(tmax<int64_t>(1, ceil_div(pl.KP * pl.NP, kOpE))), kOpE * kOpG, 0, s>>>(S0, V, pl.P,
+                                                                                                      pl.L, pl, op);
     FAGP_LAUNCH_CHECK();
     return set_weights(op, w, b, s);
   }
