@@ -48,5 +48,13 @@ int main(int argc, char** argv) {
   printf("CTA 0 factor_block total %.1f us (%.2f per step)\n", fb, fb / (steps - 1));
   printf("sum: phaseA %.1f sync1 %.1f phaseB %.1f sync2 %.1f us; phase C %.1f us\n", tot[0], tot[1], tot[2], tot[3],
          (prof[63][0][5] - prof[steps - 1][0][4]) * 1e-3);
+  unsigned long long bmax[64];
+  int bcta[64];
+  cudaMemcpyFromSymbol(bmax, fagp::la::g_chol_bmax, sizeof(bmax));
+  cudaMemcpyFromSymbol(bcta, fagp::la::g_chol_bmax_cta, sizeof(bcta));
+  printf("step: CTA0 B-end | latest B-end (cta) | step length   (us from CTA 0's step start)\n");
+  for (int k = 0; k < steps && k < 63; k += 2)
+    printf("%3d  %6.2f | %6.2f (%3d) | %6.2f\n", k, (prof[k][0][3] - prof[k][0][0]) * 1e-3,
+           (long long)(bmax[k] - prof[k][0][0]) * 1e-3, bcta[k], (prof[k][0][4] - prof[k][0][0]) * 1e-3);
   return 0;
 }
