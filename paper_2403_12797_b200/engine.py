@@ -255,6 +255,7 @@ class PosteriorEngine:
                 gev.append((name, e))
 
         mark("start", cs)
+        self._host_flags = None
         X, y, Xs = self._host_buffers()
         p = b.p
         Xh = self._pinned(Xh, "X", (self.N, p))
@@ -330,13 +331,22 @@ class PosteriorEngine:
             mark(f"d2h{ci}", self.s_out)
         if trace is not None:
             trace.append(time.perf_counter())
+        # the flag words ride home with the results (no separate D2H + sync in check())
+        fh = self.__dict__.get("_flags_pinned")
+        if fh is None:
+            fh = self._flags_pinned = torch.empty((2,), dtype=torch.int32, pin_memory=True)
+        self.s_out.wait_stream(cs)
+        with torch.cuda.stream(self.s_out):
+            fh.copy_(self.flags, non_blocking=True)
         self.s_out.synchronize()
+        self._host_flags = (int(fh[0]), int(fh[1]))
         if gev is not None:
             _GPU_TRACE.append([(n, gev[0][1].elapsed_time(e)) for n, e in gev])
         if trace is not None:
             trace.append(time.perf_counter())
             _TRACE.append([1e3 * (b - a) for a, b in zip(trace, trace[1:])])
         if asynchronous and self.factor_needs_retry():
+            self._host_flags = None
             self._retry_factor(X, Xs, y, fault_flip)
             self.stage_predict(Xs)
             torch.cuda.current_stream(self.device).synchronize()
@@ -385,7 +395,8 @@ class PosteriorEngine:
     def raise_errors(self, X=None, Xs=None, y=None, factor_failed=False, after_predict=False):
         """Raise the reference's exception for whatever went wrong (validation order of
         fagp_posterior: train X, train Phi, test X, test Phi, then the factorisation)."""
-        fl = [int(v) for v in dev.to_host(self.flags)]
+        hf, self._host_flags = self.__dict__.get("_host_flags"), None
+        fl = list(hf) if hf is not None else [int(v) for v in dev.to_host(self.flags)]
         b = self.basis
         if fl[0] & _lib.FLAG_STALLED:
             raise RuntimeError("pipelined Gram: an input chunk was never signalled (FAGP_FLAG_STALLED)")
