@@ -356,13 +356,24 @@ class PosteriorEngine:
         return o[0], (o[1] if self.want_var else None)
 
     def _predict_chunks(self):
-        """Row ranges of the chunked predict: cut at whole waves of the fused predict (every
-        chunk but the last fills all SMs to the end), else at multiples of 64 rows."""
-        Ns, pc = self.Ns, self.PREDICT_CHUNKS
+        """Row ranges of the chunked predict, cut at whole waves of the fused predict (every chunk
+        but the last fills all SMs to the end; else multiples of 64 rows).  Each chunk's D2H
+        overlaps the next chunk's compute, so only the last chunk's D2H is exposed: the chunks
+        shrink geometrically towards the end (..., 8, 4, 2, 1 waves), the rest split evenly."""
+        Ns, pc = self.Ns, max(1, self.PREDICT_CHUNKS)
         wave = int(_lib.lib().fagp_predict_x_wave_rows(self.basis.ref)) or 64
         nw = -(-max(Ns, 1) // wave)
-        cuts = sorted({min(Ns, (i * nw // pc) * wave) for i in range(pc + 1)} | {Ns})
-        return [(a, e) for a, e in zip(cuts, cuts[1:]) if e > a]
+        tail = []
+        while len(tail) < pc - 2 and sum(tail) + 2 ** len(tail) <= nw // 2:
+            tail.append(2 ** len(tail))
+        head = nw - sum(tail)
+        nh = max(1, pc - len(tail))
+        sizes = [head * (i + 1) // nh - head * i // nh for i in range(nh)] + tail[::-1]
+        cuts, a = [0], 0
+        for w in sizes:
+            a += w
+            cuts.append(min(Ns, a * wave))
+        return [(x, y) for x, y in zip(cuts, cuts[1:]) if y > x]
 
     def _ready_words(self, n):
         """Zeroed device words for fagp_gram_x_pipelined (re-armed by the launch itself)."""
