@@ -314,22 +314,24 @@ __device__ __forceinline__ int64_t h_index(int64_t i, int64_t j, int p, int M, i
   return key;
 }
 
-// one CTA per row i (grid-stride), threads over j; the per-dimension pair keys come from a shared
-// M x M table (M <= 64; computed inline beyond) and 32-bit digit arithmetic
+// One CTA per row i (grid-stride), threads over j.  The pair key separates over dimensions,
+// key(i, j) = sum_d P^(p-1-d) pk(a_d, b_d), so each row builds two small shared tables --
+// KH[j / M] (dims < p-1) and KL[j % M] (the last dim) -- and a column costs two table reads and
+// one gather; (j / M, j % M) advance incrementally.  Shapes whose tables do not fit take the
+// digit-by-digit key.
+constexpr int kPairKH = 4096, kPairKL = 64;
 __global__ void pair_system_kernel(const double* __restrict__ H, const double* __restrict__ s, double sigma2,
                                    double jit, BasisView b, int P, double* __restrict__ A, double* __restrict__ G) {
-  constexpr int kTab = 64;
-  __shared__ int pk[kTab * kTab];
+  __shared__ int KH[kPairKH], KL[kPairKL];
   const int M = b.M, p = b.p;
-  const int64_t m = b.m;
-  const bool tab = M <= kTab;
+  const int64_t m = b.m, MH = m / M;
+  const int nt = int(blockDim.x);
+  const bool tab = M <= kPairKL && MH <= kPairKH;
   auto pkey = [&](int a, int c) {
     const int lo = a < c ? a : c, hi = a < c ? c : a;
     return lo * M - lo * (lo - 1) / 2 + (hi - lo);
   };
-  if (tab)
-    for (int e = threadIdx.x; e < M * M; e += blockDim.x) pk[e] = pkey(e / M, e % M);
-  __syncthreads();
+  const int stq = nt / M, str = nt - (nt / M) * M;  // nt = stq M + str
   for (int64_t i = blockIdx.x; i < m; i += gridDim.x) {
     int di[FAGP_MAX_P];
     {
@@ -339,33 +341,61 @@ __global__ void pair_system_kernel(const double* __restrict__ H, const double* _
         q /= M;
       }
     }
+    if (tab) {
+      __syncthreads();  // the previous row's readers are done
+      for (int e = threadIdx.x; e < MH; e += nt) {
+        int q = e, key = 0, pw = P;
+        for (int d = p - 2; d >= 0; --d) {
+          key += pw * pkey(di[d], q % M);
+          q /= M;
+          pw *= P;
+        }
+        KH[e] = key;
+      }
+      for (int e = threadIdx.x; e < M; e += nt) KL[e] = pkey(di[p - 1], e);
+      __syncthreads();
+    }
     const double si = s ? s[i] : 1.0;
+    int jh = int(threadIdx.x) / M, jl = int(threadIdx.x) - (int(threadIdx.x) / M) * M;
+    auto advance = [&]() {
+      jh += stq;
+      jl += str;
+      if (jl >= M) {
+        jl -= M;
+        ++jh;
+      }
+    };
     // 4 columns per thread per pass: keys first, then the 4 gathers in flight together
-    for (int64_t jb = threadIdx.x; jb < m; jb += 4 * int64_t(blockDim.x)) {
+    for (int64_t jb = threadIdx.x; jb < m; jb += 4 * int64_t(nt)) {
       int64_t key[4];
       double g[4], sj[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int64_t j = jb + u * int64_t(blockDim.x);
-        unsigned q = unsigned(j < m ? j : 0);
-        int64_t k = 0, pw = 1;
-        for (int d = p - 1; d >= 0; --d) {
-          const unsigned c = q % unsigned(M);
-          q /= unsigned(M);
-          k += pw * (tab ? pk[di[d] * M + int(c)] : pkey(di[d], int(c)));
-          pw *= P;
+        const int64_t j = jb + u * int64_t(nt);
+        if (tab) {
+          key[u] = j < m ? int64_t(KH[jh] + KL[jl]) : 0;
+          advance();
+        } else {
+          unsigned q = unsigned(j < m ? j : 0);
+          int64_t k = 0, pw = 1;
+          for (int d = p - 1; d >= 0; --d) {
+            const unsigned c = q % unsigned(M);
+            q /= unsigned(M);
+            k += pw * pkey(di[d], int(c));
+            pw *= P;
+          }
+          key[u] = k;
         }
-        key[u] = k;
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int64_t j = jb + u * int64_t(blockDim.x);
+        const int64_t j = jb + u * int64_t(nt);
         g[u] = H[key[u]];
         sj[u] = (A && j < m) ? s[j] : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int64_t j = jb + u * int64_t(blockDim.x);
+        const int64_t j = jb + u * int64_t(nt);
         if (j >= m) continue;
         if (G) G[i * m + j] = g[u];
         if (A) {
