@@ -56,5 +56,12 @@ int main(int argc, char** argv) {
   for (int k = 0; k < steps && k < 63; k += 2)
     printf("%3d  %6.2f | %6.2f (%3d) | %6.2f\n", k, (prof[k][0][3] - prof[k][0][0]) * 1e-3,
            (long long)(bmax[k] - prof[k][0][0]) * 1e-3, bcta[k], (prof[k][0][4] - prof[k][0][0]) * 1e-3);
+  unsigned long long b8[2][256];
+  cudaMemcpyFromSymbol(b8, fagp::la::g_chol_b8, sizeof(b8));
+  printf("step 8 phase B per CTA (us): start rel. CTA0 step start / duration\n");
+  for (int c = 0; c < 148; ++c)
+    printf("%3d:%5.2f/%5.2f%s", c, (long long)(b8[0][c] - prof[8][0][0]) * 1e-3, (long long)(b8[1][c] - b8[0][c]) * 1e-3,
+           c % 6 == 5 ? "\n" : "  ");
+  printf("\n");
   return 0;
 }
