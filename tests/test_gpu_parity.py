@@ -468,3 +468,30 @@ def test_pipelined_gram_without_signal_reports_stall():
                                        _lib.ptr(ws), wsz, _lib.ptr(flags), None), "pipelined")
     torch.cuda.synchronize()
     assert int(dev.to_host(flags)[0]) & _lib.FLAG_STALLED
+
+
+@pytest.mark.parametrize("M", [4, 10])
+def test_fused_mode_products_match_the_generic_kernels(M, monkeypatch):
+    """p = 3 fused mode products against the generic per-mode kernels (FAGP_MODE_UNFUSED=1):
+    expand3 (K -> pair Gram) keeps their stage and fma order -- bitwise the same G; ctc3 (the C''
+    predict operand, folded and contracted in another order) agrees to rounding."""
+    from paper_2403_12797_b200.posterior import gram_x_packed
+
+    rng = np.random.default_rng(40 + M)
+    N = 20_000
+    X = rng.uniform(-1, 1, (N, 3))
+    y = np.cos(X).sum(1) + 0.05 * rng.standard_normal(N)
+    basis = F.Basis(F.ArdKernelParams.isotropic(3, 1.0, 1.0), M)
+    packed = gram_x_packed(basis, dev.to_device(X), dev.to_device(y), 0.1)
+
+    def run():
+        G, t = gram_unpack(basis, packed)
+        f, st, _ = factor_packed(basis, packed, 0.01, 0.1, N)
+        assert st == 0
+        return dev.to_host(G), dev.to_host(f.predict_op)
+
+    G1, op1 = run()
+    monkeypatch.setenv("FAGP_MODE_UNFUSED", "1")
+    G0, op0 = run()
+    assert np.array_equal(G1, G0)
+    assert np.abs(op1 - op0).max() <= 1e-12 * np.abs(op0).max()
