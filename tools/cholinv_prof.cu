@@ -63,5 +63,12 @@ int main(int argc, char** argv) {
     printf("%3d:%5.2f/%5.2f%s", c, (long long)(b8[0][c] - prof[8][0][0]) * 1e-3, (long long)(b8[1][c] - b8[0][c]) * 1e-3,
            c % 6 == 5 ? "\n" : "  ");
   printf("\n");
+  unsigned long long jb[16];
+  cudaMemcpyFromSymbol(jb, fagp::la::g_chol_job, sizeof(jb));
+  printf("step 8, CTA 5 phase B (us from its phase-B start): issued %.2f", (long long)(jb[0] - b8[0][5]) * 1e-3);
+  for (int q = 0; q < 6; ++q)
+    if (jb[1 + 2 * q]) printf(" | job %d ready %.2f done %.2f", q, (long long)(jb[1 + 2 * q] - b8[0][5]) * 1e-3,
+                              (long long)(jb[2 + 2 * q] - b8[0][5]) * 1e-3);
+  printf(" | end %.2f\n", (long long)(b8[1][5] - b8[0][5]) * 1e-3);
   return 0;
 }
