@@ -47,7 +47,7 @@ CONFIGS = {
 METRIC = "posterior mean+var samples/s (N=1e6, p=3, M=10); % FP64 tensor peak"
 NOISE_VAR = 0.0025
 FP64_PEAK_FILE = ROOT / "profiles" / "fp64_peak_r01.json"
-NCU_SUMMARY_FILE = ROOT / "profiles" / "ncu_summary_r02c.json"
+NCU_SUMMARY_FILE = ROOT / "profiles" / "ncu_summary_r02d.json"
 
 
 def log(*a):
