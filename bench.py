@@ -42,6 +42,7 @@ CONFIGS = {
     "c1": (1, 10, 1_000, 1_000),
     "c2": (2, 10, 100_000, 100_000),
     "c3": (3, 10, 1_000_000, 1_000_000),
+    "c4": (4, 8, 4_000_000, 1_000_000),  # BASELINE configs[3] (test count not given: 1e6)
     "c5": (5, 6, 8_000_000, 2_000_000),
 }
 METRIC = "posterior mean+var samples/s (N=1e6, p=3, M=10); % FP64 tensor peak"

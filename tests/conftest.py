@@ -74,7 +74,7 @@ class Case:
         return Dataset(X=self.X, y=self.y, noise_std=0.05, seed=self.seed, domain=((-1.0, 1.0),) * self.p)
 
 
-CASE_NAMES = ["c1", "c2s", "c3s", "ard4", "lin2", "p1m40", "c5s"]
+CASE_NAMES = ["c1", "c2s", "c3s", "ard4", "lin2", "p1m40", "c5s", "c4s"]
 
 
 @pytest.fixture(scope="session")

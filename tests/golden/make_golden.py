@@ -35,6 +35,7 @@ CASES = {
     "lin2": (2, 7, 900, 200, (0.8, 1.3), (0.6, 1.7), 0.05, -0.5, "rho_linear", True),
     "p1m40": (1, 40, 3000, 400, (1.5,), (1.2,), 0.001, 1.0, "rho_squared", True),
     "c5s": (5, 6, 600, 80, None, None, 0.0025, 0.0, "rho_squared", False),
+    "c4s": (4, 8, 3000, 300, None, None, 0.0025, 0.0, "rho_squared", False),
 }
 
 LITERAL_CASES = ("c1", "lin2", "ard4", "p1m40", "c5s")
