@@ -14,7 +14,12 @@ __host__ __device__ inline int64_t chol_scratch_len(int64_t m) { return m + 32 *
 int potrf_persistent(double* A, int64_t m, int64_t lda, int* info, double* scratch, cudaStream_t s);
 
 // scratch doubles: L_kk^{-1} x 2 | panels (T blocks) | flag
-__host__ __device__ inline int64_t cholinv_scratch_len(int64_t m) { return int64_t(2 + (m + 31) / 32) * 32 * 32 + 2; }
+// [2 L^{-1} blocks | T panels | flag + 2 barrier counters (2 doubles, zeroed per launch) |
+//  SM id per CTA (kCholInvSmTab ints)]
+constexpr int64_t kCholInvSmTab = 1024;
+__host__ __device__ inline int64_t cholinv_scratch_len(int64_t m) {
+  return int64_t(2 + (m + 31) / 32) * 32 * 32 + 2 + kCholInvSmTab / 2;
+}
 
 // Dout (ld ldd, full symmetric) = A^{-1} of the SPD m x m matrix A (overwritten) by one
 // persistent kernel (Cholesky, triangular inverse into X (m x m scratch), X^T X); *info
