@@ -48,7 +48,7 @@ CONFIGS = {
 METRIC = "posterior mean+var samples/s (N=1e6, p=3, M=10); % FP64 tensor peak"
 NOISE_VAR = 0.0025
 FP64_PEAK_FILE = ROOT / "profiles" / "fp64_peak_r01.json"
-NCU_SUMMARY_FILE = ROOT / "profiles" / "ncu_summary_r02e.json"
+NCU_SUMMARY_FILE = ROOT / "profiles" / "ncu_summary_r02f.json"
 
 
 def log(*a):
