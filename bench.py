@@ -66,12 +66,12 @@ def launches_per_step(m, pair, p=1, fused=False, inverse=False):
     the same step shows (profiles/ncu_summary_*.json)."""
     if pair and fused and inverse:
         # fagp_gram_x: fused Gram + partial sum; fagp_predict_x: one fused kernel;
-        # fagp_factor_inv_async at p = 3: expand3 (K -> H), pair_system + t copy, fused Cholesky
-        # inverse, w GEMV, ctc3 + ctc3_op (-> C''), w copy; other p: p mode products, pair_system
-        # + t copy, inverse, GEMV, ctilde, p mode products, scatter, w copy
+        # fagp_factor_inv_async at p = 3: expand3 (K -> H), pair_system (+ the t copy), fused
+        # Cholesky inverse, w GEMV, ctc3 + ctc3_op (-> C'', + the w copy); other p: p mode
+        # products, pair_system, inverse, GEMV, ctilde, p mode products, scatter, w copy
         if p == 3:
-            return 2 + (1 + 2 + 1 + 1 + 2 + 1) + 1
-        return 2 + (p + 2 + 1 + 1 + 1 + p + 1 + 1) + 1
+            return 2 + (1 + 1 + 1 + 1 + 2) + 1
+        return 2 + (p + 1 + 1 + 1 + 1 + p + 1 + 1) + 1
     nblk = -(-m // 32)
     potrf = nblk + (nblk - 1)  # fused diag+panel kernel per step, trailing GEMM between steps
     mp = 32

@@ -321,7 +321,8 @@ __device__ __forceinline__ int64_t h_index(int64_t i, int64_t j, int p, int M, i
 // digit-by-digit key.
 constexpr int kPairKH = 4096, kPairKL = 64;
 __global__ void pair_system_kernel(const double* __restrict__ H, const double* __restrict__ s, double sigma2,
-                                   double jit, BasisView b, int P, double* __restrict__ A, double* __restrict__ G) {
+                                   double jit, BasisView b, int P, double* __restrict__ A, double* __restrict__ G,
+                                   const double* __restrict__ tsrc, double* __restrict__ t) {
   __shared__ int KH[kPairKH], KL[kPairKL];
   const int M = b.M, p = b.p;
   const int64_t m = b.m, MH = m / M;
@@ -356,6 +357,7 @@ __global__ void pair_system_kernel(const double* __restrict__ H, const double* _
       __syncthreads();
     }
     const double si = s ? s[i] : 1.0;
+    if (t && threadIdx.x == 0) t[i] = tsrc[i];  // t = the gram buffer's tail (one copy launch fewer)
     int jh = int(threadIdx.x) / M, jl = int(threadIdx.x) - (int(threadIdx.x) / M) * M;
     auto advance = [&]() {
       jh += stq;
@@ -584,12 +586,16 @@ __global__ void __launch_bounds__(kCtcNT) ctc3_kernel(const double* __restrict__
 constexpr int kOpE = 32, kOpG = 4;  // ctc3_op: entries per CTA x pi0 groups
 __global__ void __launch_bounds__(kOpE * kOpG) ctc3_op_kernel(const double* __restrict__ Z,
                                                               const double* __restrict__ Vg, int P, int L, Plan pl,
-                                                              double* __restrict__ op) {
+                                                              double* __restrict__ op, const double* __restrict__ w,
+                                                              int64_t m) {
   // group g sums pi0 in [g P / 4, (g + 1) P / 4) with every load in flight, then the 4 group
   // sums are added in group order (fixed order: deterministic)
   __shared__ double red[kOpG][kOpE];
   const int grp = int(threadIdx.x) / kOpE, el = int(threadIdx.x) % kOpE;
   const int64_t total = pl.KP * pl.NP;
+  // the mean weights w ride along into the operand's tail (one copy launch fewer)
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < m; q += int64_t(gridDim.x) * blockDim.x)
+    op[total + q] = w[q];
   const int64_t e = int64_t(blockIdx.x) * kOpE + el;
   double acc = 0.0;
   bool valid = false;
@@ -1060,8 +1066,9 @@ int system(const double* H, const double* g, const double* sqrt_lam, double sigm
   const int64_t m = b->m;
   if (A || G) {
     const int grid = int(tmin<int64_t>(m, 8 * num_sms()));
-    pair_system_kernel<<<grid, 256, 0, s>>>(H, sqrt_lam, sigma2, jit, view(b), pl.P, A, G);
+    pair_system_kernel<<<grid, 256, 0, s>>>(H, sqrt_lam, sigma2, jit, view(b), pl.P, A, G, g + pl.Klen, t);
     FAGP_LAUNCH_CHECK();
+    return FAGP_OK;
   }
   if (t) {
     copy_kernel<<<unsigned(ceil_div(m, 256)), 256, 0, s>>>(g + pl.Klen, t, m);
@@ -1086,10 +1093,10 @@ int build_predict_op(const double* D, const double* sqrt_lam, const double* w, c
     FAGP_CUDA_TRY(cudaFuncSetAttribute(ctc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     ctc3_kernel<<<dim3(unsigned(pl.P), kCtcSplit), kCtcNT, smem, s>>>(D, b->m, sqrt_lam, view(b), pl.P, S0);
     FAGP_LAUNCH_CHECK();
-    ctc3_op_kernel<<<unsigned(tmax<int64_t>(1, ceil_div(pl.KP * pl.NP, kOpE))), kOpE * kOpG, 0, s>>>(S0, V, pl.P,
-                                                                                                      pl.L, pl, op);
+    ctc3_op_kernel<<<unsigned(tmax<int64_t>(1, ceil_div(pl.KP * pl.NP, kOpE))), kOpE * kOpG, 0, s>>>(
+        S0, V, pl.P, pl.L, pl, op, w, b->m);
     FAGP_LAUNCH_CHECK();
-    return set_weights(op, w, b, s);
+    return FAGP_OK;
   }
   {
     const int grid = int(tmax<int64_t>(1, tmin<int64_t>(ceil_div(pl.Hlen, 256), 16 * num_sms())));
