@@ -912,10 +912,11 @@ int gram(const double* X, const double* y, double c, int64_t N, const fagp_basis
          void* ws, size_t ws_bytes, uint32_t* flags, cudaStream_t s, const unsigned* ready) {
   GPlan pl;
   if (!make_gplan(N, b->p, b->M, pl)) return FAGP_EUNSUPPORTED;
-  if (ws == nullptr || ws_bytes < size_t(pl.nparts) * size_t(pl.plen) * sizeof(double)) return FAGP_EWORKSPACE;
   if (k0 < 0 || k1 > pl.S || k0 >= k1) return FAGP_EINVAL;
   // one launch over every sub-range: one partial per CTA (and row group)
   pl.once = (k0 == 0 && k1 == pl.S) ? 1 : 0;
+  const size_t parts = pl.once ? size_t(pl.grid) * pl.G : size_t(pl.nparts);
+  if (ws == nullptr || ws_bytes < parts * size_t(pl.plen) * sizeof(double)) return FAGP_EWORKSPACE;
   pl.ready = pl.once ? ready : nullptr;
   if (pl.ready) {
     // load partial_sum_kernel now: with lazy module loading its first launch (queued behind a

@@ -495,3 +495,32 @@ def test_fused_mode_products_match_the_generic_kernels(M, monkeypatch):
     G0, op0 = run()
     assert np.array_equal(G1, G0)
     assert np.abs(op1 - op0).max() <= 1e-12 * np.abs(op0).max()
+
+
+@pytest.mark.parametrize("subranges,chunks", [("1", 1), ("3", 7), ("27", 2)])
+def test_host_pipeline_chunking_is_bitwise_invariant(subranges, chunks, monkeypatch):
+    """The host path's upload chunking (Gram sub-ranges) and predict chunking change nothing:
+    every split gives the device-resident path's bits."""
+    from paper_2403_12797_b200.engine import PosteriorEngine
+
+    rng = np.random.default_rng(5)
+    N, Ns = 150_001, 90_017
+    X = rng.uniform(-1, 1, (N, 3))
+    y = np.cos(X).sum(1) + 0.05 * rng.standard_normal(N)
+    Xs = rng.uniform(-1, 1, (Ns, 3))
+    model = F.GpModel(F.ArdKernelParams.isotropic(3, 1.0, 1.0), 0.0025, n_eigen=10)
+
+    class Dev:
+        pass
+
+    Dev.X, Dev.y = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    ref = F.fagp_posterior(Dev, torch.from_numpy(Xs).cuda(), model, memory_cap=None)
+    monkeypatch.setenv("FAGP_GRAM_SUBRANGES", subranges)
+    monkeypatch.setattr(PosteriorEngine, "PREDICT_CHUNKS", chunks)
+
+    class Host:
+        pass
+
+    Host.X, Host.y = torch.from_numpy(X).pin_memory(), y
+    got = F.fagp_posterior(Host, Xs, model, memory_cap=None)
+    assert np.array_equal(got.mean, ref.mean) and np.array_equal(got.var, ref.var)
