@@ -470,7 +470,7 @@ def test_pipelined_gram_without_signal_reports_stall():
     assert int(dev.to_host(flags)[0]) & _lib.FLAG_STALLED
 
 
-@pytest.mark.parametrize("M", [4, 10])
+@pytest.mark.parametrize("M", [4, 10, 11, 12])
 def test_fused_mode_products_match_the_generic_kernels(M, monkeypatch):
     """p = 3 fused mode products against the generic per-mode kernels (FAGP_MODE_UNFUSED=1):
     expand3 (K -> pair Gram) keeps their stage and fma order -- bitwise the same G; ctc3 (the C''
