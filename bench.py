@@ -55,12 +55,6 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-def useful_flops(N, Ns, m):
-    """SURVEY.md §8d algorithmic count: Gram N m(m+1) + t 2Nm + chol m^3/3 + trtri m^3/3
-    + mean 2N*m + var N* m(m+1) + 2N*m."""
-    return N * m * (m + 1) + 2 * N * m + 2 * m**3 / 3 + 2 * Ns * m + Ns * m * (m + 1) + 2 * Ns * m
-
-
 def launches_per_step(m, pair, p=1, fused=False, inverse=False):
     """Kernels of ours launched by one timed step (no jitter retry), as the ncu launch list of
     the same step shows (profiles/ncu_summary_*.json)."""
@@ -193,55 +187,108 @@ def make_inputs(cfg, rank, world):
     return ds.X[a:b], ds.y[a:b], Xs[c:d]
 
 
-def cpu_baseline(cfg, sample_n):
-    """The oracle port (the reference algorithm on numpy/OpenBLAS) on a bounded sample."""
+def cpu_info():
+    """Host description for the CPU legs: logical cores, model name, BLAS library + threads."""
+    from threadpoolctl import threadpool_info
+
+    model = "unknown"
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    blas = [i for i in threadpool_info() if i.get("user_api") == "blas"]
+    return {"cpu_count": os.cpu_count(), "model": model,
+            "blas": [f"{i.get('internal_api')} {i.get('version')} x{i.get('num_threads')}" for i in blas]}
+
+
+def cpu_posterior(cfg, mode, workers, max_rows=None):
+    """One posterior of config `cfg` through the oracle port of the reference path (its own
+    evaluation order and Backend mode: materialised Phi, OpenBLAS GEMMs, LAPACK potrf; the
+    variance is the diagonal of its covariance restated blockwise), phases timed.  The full
+    config when it fits in host memory (C1-C3); else the largest row subsample that does, with
+    the phases extrapolated linearly as BASELINE.md §4 prescribes (train-row phases x N/n,
+    test-row phases x N*/n*, the factor constant)."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import fagp_oracle as O
-    from threadpoolctl import threadpool_info
 
     from paper_2403_12797_b200.datagen import generate, test_inputs, train_seed
 
     p, M, N, Ns = CONFIGS[cfg]
-    n = min(sample_n, N)
-    ns = max(1, int(round(n * Ns / N)))
+    m = M**p
+    n, ns = N, Ns
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:  # noqa: BLE001
+        avail = 64 << 30
+    need = lambda a, b: 8 * (a + b) * m * 1.15 + 6 * 8 * m * m  # noqa: E731 - Phi, Phi*, G/A/L/U
+    while need(n, ns) > 0.7 * avail or (max_rows is not None and n > max_rows):
+        n, ns = max(1, n // 2), max(1, ns // 2)
     ds = generate(n, p, train_seed(p), 0.05)
     Xs = test_inputs(ns, p)
     t0 = time.perf_counter()
-    O.posterior(ds.X, ds.y, Xs, [1.0] * p, [1.0] * p, M, NOISE_VAR, block=None, predict_block=32768)
-    dt = time.perf_counter() - t0
-    threads = max([i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"] or [1])
-    return {"value": ns / dt, "unit": "samples/s", "cores": int(threads), "kind": "port",
-            "sample": f"N={n} train / N*={ns} test rows of config {cfg} (p={p}, M={M}), one full posterior "
-                      f"(materialised Phi, OpenBLAS SYRK/GEMV, LAPACK potrf), {dt:.2f} s; samples/s scales "
-                      f"linearly in N=N* (m^3 terms negligible)"}
+    _, _, ph = O.posterior_timed(ds.X, ds.y, Xs, [1.0] * p, [1.0] * p, M, NOISE_VAR, mode=mode, workers=workers)
+    wall = time.perf_counter() - t0
+    extrap = (n, ns) != (N, Ns)
+    if extrap:
+        fN, fNs = N / n, Ns / ns
+        ph = {k: v * (fN if k in ("eigensystem_train", "gram", "phi_t_r") else
+                      fNs if k in ("eigensystem_test", "mean", "var") else 1.0) for k, v in ph.items()}
+    total = sum(ph.values())
+    return {"seconds": total, "wall_s": wall, "phases_s": {k: round(v, 4) for k, v in ph.items()}, "n": n, "ns": ns,
+            "extrapolated": extrap, "mode": mode, "workers": workers}
+
+
+def _cpu_line(r, cfg):
+    p, M, N, Ns = CONFIGS[cfg]
+    what = (f"full config {cfg}: N={N} train / N*={Ns} test" if not r["extrapolated"] else
+            f"config {cfg} extrapolated linearly from N={r['n']} / N*={r['ns']} rows (host memory)")
+    return (f"{what}, one posterior through the oracle port of the reference path, Backend "
+            f"{r['mode']}(workers={r['workers']}): materialised Phi, OpenBLAS GEMM, LAPACK potrf, "
+            f"variance = diag of the reference covariance restated in 32768-row blocks")
+
+
+def cpu_baseline(cfg):
+    """The reference path on this host's cores (rank 0, N=1 only): one posterior of the config."""
+    workers = os.cpu_count() or 1
+    r = cpu_posterior(cfg, "parallel", workers)
+    p, M, N, Ns = CONFIGS[cfg]
+    return {"value": Ns / r["seconds"], "unit": "samples/s", "cores": workers, "kind": "port",
+            "sample": _cpu_line(r, cfg), "phases_s": r["phases_s"], "host": cpu_info()}
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU implementation of the path (oracle port, all host
+    threads: Backend parallel(workers=os.cpu_count())) timed on rank 0.  Warm-up steps run a
+    small sample (thread pools, page-in); each of the K timed steps is ONE FULL posterior of the
+    config (C3: N = N* = 1e6), phases recorded.  After the timed steps one Backend("serial")
+    posterior is recorded for the mode comparison of BASELINE.md §4."""
     if rank != 0:
         return
     p, M, N, Ns = CONFIGS[args.config]
-    sample = args.cpu_sample
-    vals = []
-    for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(args.config, sample)
-        if i >= args.warmup:
-            vals.append(cb)
-    v = statistics.median([c["value"] for c in vals])
-    cb = dict(vals[-1])
-    cb["value"] = v
+    workers = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_posterior(args.config, "parallel", workers, max_rows=20_000)
+    runs = [cpu_posterior(args.config, "parallel", workers) for _ in range(args.steps)]
+    secs = [r["seconds"] for r in runs]
+    t = statistics.mean(secs)
+    v = Ns / t
+    phases = {k: round(statistics.median([r["phases_s"][k] for r in runs]), 4) for k in runs[0]["phases_s"]}
+    serial = cpu_posterior(args.config, "serial", 1) if not args.no_serial else None
+    cb = {"value": v, "unit": "samples/s", "cores": workers, "kind": "port", "sample": _cpu_line(runs[0], args.config),
+          "phases_s": phases, "host": cpu_info(), "step_s": [round(x, 3) for x in secs],
+          "serial": None if serial is None else {"value": Ns / serial["seconds"], "seconds": round(serial["seconds"], 3),
+                                                 "phases_s": serial["phases_s"]}}
     out = {"metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": 1e3 * (cb_n(args) / v), "higher_is_better": True,
+           "warmup": args.warmup, "ms_per_step": round(1e3 * t, 1), "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator)",
-           "impl": "reference", "config": config_dict(args, world=1),
-           "cpu_baseline": cb, "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
-                                       "d2h_bytes_per_step": 0}}
+           "impl": "reference", "config": config_dict(args, world=1), "cpu_baseline": cb,
+           "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
-
-
-def cb_n(args):
-    p, M, N, Ns = CONFIGS[args.config]
-    n = min(args.cpu_sample, N)
-    return max(1, int(round(n * Ns / N)))
 
 
 def config_dict(args, world):
@@ -259,7 +306,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
-    ap.add_argument("--cpu-sample", type=int, default=100_000)
+    ap.add_argument("--no-serial", action="store_true", help="reference arm: skip the Backend('serial') record")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -351,24 +398,20 @@ def main():
     else:
         gram_flops = n_loc * m * (m + 1) + 2 * n_loc * m
         pred_flops = ns_loc * m * (m + 1) + 4 * ns_loc * m
-    ref_gram = n_loc * m * (m + 1) + 2 * n_loc * m  # SURVEY.md §8d counts (reference algorithm)
-    ref_pred = ns_loc * m * (m + 1) + 4 * ns_loc * m
     g_ms, p_ms = statistics.mean(gram_ms), statistics.mean(pred_ms)
     peak, peak_src = fp64_peak()
     if g_ms >= p_ms:
-        dom, dflops, rflops, dms = "fagp_gram_x (eigenfunctions on chip + modal DMMA Gram + t, partial sum)" if pair else \
-            "fagp_gram (fused SYRK + reduce)", gram_flops, ref_gram, g_ms
+        dom, dflops, dms = "fagp_gram_x (eigenfunctions on chip + modal DMMA Gram + t, partial sum)" if pair else \
+            "fagp_gram (fused SYRK + reduce)", gram_flops, g_ms
         traffic = ncu_traffic("fused_gram_split_kernel" if pair and p == 3 and M == 10 else "fused_gram_kernel" if pair else "gram_kernel_fast")
     else:
-        dom, dflops, rflops, dms = "fagp_predict_x (eigenfunctions on chip + modal DMMA variance + mean)" if pair else \
-            "fagp_predict (fused triangular GEMM)", pred_flops, ref_pred, p_ms
+        dom, dflops, dms = "fagp_predict_x (eigenfunctions on chip + modal DMMA variance + mean)" if pair else \
+            "fagp_predict (fused triangular GEMM)", pred_flops, p_ms
         traffic = ncu_traffic(("fused_predict_split_kernel" if p == 3 and 9 <= M <= 12 else "fused_predict_kernel") if pair else "predict_kernel_fast")
     achieved = dflops / (dms / 1e3) / 1e12
     roofline = {"bound": "tensor", "kernel": dom, "achieved": round(achieved, 3), "peak": peak, "unit": "TFLOP/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                "flops_per_launch": dflops, "algorithm": "modal form (L^p = (2M-1)^p entries)" if pair else "direct",
-                "reference_equivalent_tflops": round(rflops / (dms / 1e3) / 1e12, 3)}
-    step_tf = useful_flops(N, Ns, m) / world / (ms / 1e3) / 1e12
+                "flops_per_launch": dflops, "algorithm": "modal form (L^p = (2M-1)^p entries)" if pair else "direct"}
 
     # ---- end to end through the public API (pinned host in, host numpy out) ----
     e2e = None
@@ -412,7 +455,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.config, args.cpu_sample)
+        cpu = cpu_baseline(args.config)
 
     if rank == 0:
         out = {"metric": METRIC, "value": round(value, 1), "unit": "samples/s", "n_gpus": world,
@@ -423,7 +466,6 @@ def main():
                                                 inverse=eng.inverse_route) * args.steps,
                "phases_ms": {"gram": round(g_ms, 3),
                              "allreduce+factor": round(statistics.mean(factor_ms), 3), "predict": round(p_ms, 3)},
-               "step_reference_equivalent_tflops": round(step_tf, 3),
                "jitter": eng.jitter.value, "lib": str(_lib.LIB_PATH.name)}
         print(json.dumps(out), flush=True)
     if world > 1:

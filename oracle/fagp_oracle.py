@@ -214,6 +214,127 @@ def posterior_literal(X, y, Xs, eps, rho, n, noise_var, mean_const=0.0, variant=
     return {"mean": mean, "var": var, "w": w, "inner": inner, "lambda_bar": lb, "jitter": jit}
 
 
+# ---- the reference's execution modes, timed per phase (bench.py's CPU arm) -------------------
+def _blas_single_thread():
+    """backend.py:63-70: BLAS pinned to one thread for the duration of a call."""
+    from threadpoolctl import threadpool_limits
+
+    return threadpool_limits(limits=1, user_api="blas")
+
+
+_POOLS = {}
+
+
+def _pool(workers):
+    """backend.py:49-60 (one long-lived pool per worker count)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    if workers not in _POOLS:
+        _POOLS[workers] = ThreadPoolExecutor(max_workers=workers)
+    return _POOLS[workers]
+
+
+def gemm(a, b, mode="serial", workers=1, transpose_a=False, transpose_b=False):
+    """backend.py:90-130 Backend.gemm: ``serial`` is one BLAS call (OpenBLAS threads inside);
+    ``parallel`` partitions the output rows into max(32, ceil(rows / workers)) blocks computed
+    by a thread pool with BLAS pinned to one thread."""
+    opa = a.T if transpose_a else a
+    opb = b.T if transpose_b else b
+    rows = opa.shape[0]
+    if not (mode == "parallel" and workers > 1):
+        return opa @ opb
+    block = max(32, -(-rows // workers))
+    out = np.empty((rows,) if opb.ndim == 1 else (rows, opb.shape[1]))
+    starts = list(range(0, rows, block))
+
+    def fill(start):
+        out[start:start + block] = opa[start:start + block] @ opb
+
+    with _blas_single_thread():
+        if len(starts) > 1:
+            list(_pool(workers).map(fill, starts))
+        else:
+            fill(0)
+    return out
+
+
+def eigensystem_phi(X, eps, rho, n, variant=DELTA2_RHO_SQUARED, mode="serial", workers=1):
+    """mercer.py:356-368: Phi assembled in one piece (serial) or in max(32, ceil(N / workers))
+    row blocks on worker threads (parallel), then the finiteness scan (mercer.py:370)."""
+    N = X.shape[0]
+    if mode == "parallel" and workers > 1 and N > 1:
+        from concurrent.futures import ThreadPoolExecutor
+
+        phi = np.empty((N, n ** X.shape[1]))
+        block = max(32, -(-N // workers))
+
+        def fill(start):
+            phi[start:start + block] = assemble_phi(X[start:start + block], eps, rho, n, variant)
+
+        with ThreadPoolExecutor(max_workers=workers) as pool:
+            list(pool.map(fill, range(0, N, block)))
+    else:
+        phi = assemble_phi(X, eps, rho, n, variant)
+    if not np.all(np.isfinite(phi)):
+        raise ArithmeticError("non-finite feature value")
+    return phi
+
+
+PHASES7 = ("eigensystem_train", "eigensystem_test", "gram", "phi_t_r", "factor_solve_trtri", "mean", "var")
+
+
+def posterior_timed(X, y, Xs, eps, rho, n, noise_var, mean_const=0.0, variant=DELTA2_RHO_SQUARED,
+                    mode="serial", workers=1, var_block=32768):
+    """The reference path in its own evaluation order and Backend mode, with the seven phases of
+    BASELINE.md §4 / SURVEY.md §8d timed separately (seconds):
+      (i) eigensystem(X), (ii) eigensystem(X*)                      mercer.py:295-384
+      (iii) G = gemm(Phi, Phi, transpose_a)                          posterior.py:168
+      (iv) t = gemm(Phi, y - c, transpose_a)                         posterior.py:229-233
+      (v) A-build + SpdFactor (jitter) + w + U = L^{-1} diag(s)       posterior.py:169-175, 234-235
+      (vi) mean = c + gemm(Phi*, w)                                   posterior.py:247
+      (vii) var = sigma2 rowsum((Phi*_b U^T)^2) over var_block rows   posterior.py:249-263 (diagonal)
+    Returns (mean, var, {phase: seconds})."""
+    import time
+
+    eps, rho = list(eps), list(rho)
+    ph = {}
+    clock = time.perf_counter
+    t0 = clock()
+    phi = eigensystem_phi(X, eps, rho, n, variant, mode, workers)
+    ph["eigensystem_train"] = clock() - t0
+    t0 = clock()
+    phis = eigensystem_phi(Xs, eps, rho, n, variant, mode, workers)
+    ph["eigensystem_test"] = clock() - t0
+    t0 = clock()
+    G = gemm(phi, phi, mode, workers, transpose_a=True)
+    ph["gram"] = clock() - t0
+    t0 = clock()
+    r = np.asarray(y, dtype=float) - mean_const
+    t = gemm(phi, r, mode, workers, transpose_a=True)
+    ph["phi_t_r"] = clock() - t0
+    del phi
+    t0 = clock()
+    lam = eigenvalues(eps, rho, n, variant)
+    s = np.sqrt(lam_floored(lam))
+    A = s[:, None] * G
+    A *= s
+    A.flat[:: A.shape[0] + 1] += noise_var
+    L, _ = spd_factor(A)
+    w = s * sla.cho_solve((L, True), s * t, check_finite=False)
+    U = sla.solve_triangular(L, np.diag(s), lower=True, check_finite=False)
+    ph["factor_solve_trtri"] = clock() - t0
+    t0 = clock()
+    mean = mean_const + gemm(phis, w, mode, workers)
+    ph["mean"] = clock() - t0
+    t0 = clock()
+    var = np.empty(Xs.shape[0])
+    for a in range(0, Xs.shape[0], var_block):
+        Z = gemm(phis[a:a + var_block], U, mode, workers, transpose_b=True)
+        var[a:a + var_block] = noise_var * np.einsum("ij,ij->i", Z, Z)
+    ph["var"] = clock() - t0
+    return mean, var, ph
+
+
 def useful_flops(N, Ns, m):
     """Algorithmic flop count of the path."""
     return N * m * (m + 1) + 2 * N * m + m**3 / 3 + m**3 / 3 + 2 * Ns * m + Ns * m * (m + 1) + 2 * Ns * m

@@ -36,17 +36,16 @@ __host__ inline int cuda_fail(cudaError_t e, const char* file, int line) {
 
 constexpr int kNumSMs = 148;  // B200; only used as a grid-sizing hint (queried at run time)
 
+constexpr int kMaxDevices = 64;  // per-device caches of device properties / occupancies
+
 __host__ inline int num_sms() {
-  static int cached = 0;  // read-only after first call; value is a device property
-  if (cached == 0) {
-    int dev = 0, n = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess &&
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
-      cached = n;
-    else
-      cached = kNumSMs;
-  }
-  return cached;
+  static int cached[kMaxDevices];  // per device (a device property; 0 = not read yet)
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return kNumSMs;
+  if (dev < kMaxDevices && cached[dev] > 0) return cached[dev];
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = kNumSMs;
+  if (dev < kMaxDevices) cached[dev] = n;
+  return n;
 }
 
 // D += A(8x4) * B(4x8) on the FP64 tensor pipe.  Fragment layout (lane = 0..31):

@@ -800,6 +800,7 @@ static bool make_gplan(int64_t N, int p, int M, GPlan& pl) {
   const int64_t bpc = ceil_div(blocks, pl.grid);  // blocks per CTA
   pl.S = bpc >= 16 ? 8 : bpc >= 8 ? 4 : 1;
   if (const char* e = getenv("FAGP_GRAM_SUBRANGES")) pl.S = tmax(1, tmin<int>(int(bpc), atoi(e)));  // tuning knob
+  pl.S = tmin(pl.S, 64);  // ready words re-armed by one partial_sum block (and a sane chunk count)
   pl.rows_per_cta = bpc * pl.br;
   pl.grid = int(tmax<int64_t>(1, ceil_div(tmax<int64_t>(N, 1), pl.rows_per_cta)));
   pl.nparts = pl.grid * pl.S * pl.G;

@@ -1,11 +1,14 @@
 """Data-parallel sharding across GPUs.
 
 Training rows are split into contiguous shards, one per rank; each rank contracts its
-shard into a partial packed Gram ``[Phi_g | r_g]^T [Phi_g | r_g]`` and a single
-``all_reduce(SUM)`` of that (m+1)(m+2)/2-double buffer (4.0 MB at p=3, M=10) over NCCL
-joins them.  Every rank then factorises the m x m system redundantly (no broadcast) and
-predicts its own contiguous shard of the test rows.  Deterministic for a fixed world
-size: fixed split-K tree per rank and NCCL's fixed reduction order.
+shard into a partial Gram buffer and a single ``all_reduce(SUM)`` over NCCL joins them.
+On the modal shapes (p >= 2) that buffer is ``[K | t]``: the L^p modal moments
+K[kappa] = sum_r prod_d g_{d,kappa_d}(x_rd) (L = 2M-1) and t = Phi^T (y - c) -- L^p + m
+doubles, 63 KB at p=3, M=10 (7,859 doubles; 1.3 MB at C5) instead of the reference-shaped
+packed SYRK (4.0 MB at C3).  p = 1 keeps the packed (m+1)(m+2)/2 buffer.  Every rank then
+factorises redundantly (no broadcast) and predicts its own contiguous shard of the test
+rows.  Deterministic for a fixed world size: fixed per-CTA partial order on every rank and
+the collective's fixed reduction order.
 """
 
 from __future__ import annotations
@@ -35,6 +38,9 @@ def all_gather_rows(t, group=None):
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
+    if t.is_cuda and dist.get_backend(group) == "gloo":
+        # gloo's all_gather is CPU-only: stage through host memory (NCCL gathers in place)
+        return all_gather_rows(t.cpu(), group).to(t.device)
     n_local = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
     sizes = [torch.zeros_like(n_local) for _ in range(world)]
     dist.all_gather(sizes, n_local, group=group)

@@ -31,6 +31,25 @@ _GPU_TRACE = None  # diagnostics: a list collects [(mark, ms since entry)] per r
 _TRACE = None  # diagnostics: set to a list to collect run_host phase times in ms (tools/e2e_probe.py)
 
 
+def _free_refcount():
+    """sys.getrefcount of a pool entry's ndarray that nobody else holds, measured on the same
+    code path as _out_buffer's check (pool tuple + loop name + call argument): the interpreter's
+    own count, not a hard-coded literal (CPython 3.14 borrows stack references)."""
+    global _FREE_RC
+    if _FREE_RC is None:
+        import sys
+
+        import numpy as np
+
+        pool = [(None, np.empty(1))]
+        for _t, arr in pool:
+            _FREE_RC = sys.getrefcount(arr)
+    return _FREE_RC
+
+
+_FREE_RC = None
+
+
 class PosteriorEngine:
     def __init__(self, kernel, n_eigen, N, Ns, noise_var, mean_const=0.0, delta2_variant="rho_squared",
                  device=None, group=None, want_var=True, keep_gram=False):
@@ -263,7 +282,12 @@ class PosteriorEngine:
         Xsh = self._pinned(Xsh, "Xs", (self.Ns, p))
         self.flags.zero_()
         nch = int(L.fagp_gram_x_chunks(self.N, b.ref))
-        ready = self._ready_words(nch)  # (first call: zeroed on cs before s_in is ordered behind it)
+        ready = self._ready_words(nch)
+        # re-arm the ready words on the compute stream behind everything the copy stream has
+        # queued so far: a late signal of an earlier call (one that timed out with STALLED)
+        # lands before the zeroing, never after it
+        cs.wait_stream(self.s_in)
+        ready.zero_()
         self.s_in.wait_stream(cs)
         sin = _lib.stream_handle(self.s_in)
         if self.pipelined_gram:
@@ -391,8 +415,9 @@ class PosteriorEngine:
         import torch
 
         pool = self.__dict__.setdefault("_out_pool", [])
+        free = _free_refcount()
         for t, arr in pool:
-            if arr.shape == (rows, self.Ns) and sys.getrefcount(arr) <= 3:  # pool tuple + loop name + argument
+            if arr.shape == (rows, self.Ns) and sys.getrefcount(arr) <= free:
                 return t, arr
         # two at a time: the common `r = fagp_posterior(...)` loop holds one result while the
         # next call fills the other
