@@ -340,6 +340,15 @@ int fagp_inner_operand(const double* inner, const double* w, const fagp_basis* b
  * B = Phi* inner (posterior.py:262, cli.py:222). */
 int fagp_rowdot(const double* A, const double* B, int64_t n, int64_t k, double* out, void* stream);
 
+/* ---- the exact dense GP (validation route) ------------------------
+ * K[i, j] = exp(-sum_d (eps_d (A[i, d] - B[j, d]))^2) (+ diag_add on i == j): the reference's
+ * gram_matrix (kernels.py:119-145) with its accumulation order, and with diag_add = sigma2 the
+ * C = K + sigma2 I of exact_posterior (posterior.py:131-132).  A (na x p), B (nb x p) row-major
+ * device points; eps_host: p host doubles (p <= 64); K row-major with leading dimension ldk.
+ * exact_posterior then runs on fagp_potrf (jitter on the host), fagp_potrs and fagp_dgemm. */
+int fagp_se_gram(const double* A, int64_t na, const double* B, int64_t nb, int32_t p, const double* eps_host,
+                 double diag_add, double* K, int64_t ldk, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -186,6 +186,47 @@ def posterior(X, y, Xs, eps, rho, n, noise_var, mean_const=0.0, variant=DELTA2_R
     return {"G": G, "t": t, "lam": lam, "mean": mean, "var": var, **fitd}
 
 
+def covariance(Xs, fitd, eps, rho, n, noise_var, variant=DELTA2_RHO_SQUARED):
+    """The reference's full predictive covariance, scaled form (posterior.py:249-263):
+    inner = sigma2 (s_i (A^{-1})_ij s_j) symmetrised; cov = (Phi* inner) Phi*^T symmetrised."""
+    m = fitd["L"].shape[0]
+    a_inv = sla.cho_solve((fitd["L"], True), np.eye(m), check_finite=False)
+    s = fitd["s"]
+    inner = noise_var * (s[:, None] * a_inv * s[None, :])
+    inner = 0.5 * (inner + inner.T)
+    phis = assemble_phi(Xs, list(eps), list(rho), n, variant)
+    cov = (phis @ inner) @ phis.T
+    return 0.5 * (cov + cov.T)
+
+
+def se_gram(A, B, eps):
+    """kernels.py:119-145 gram_matrix: acc += (eps_j (a_j - b_j))^2 over dims in order; exp(-acc)."""
+    acc = np.zeros((A.shape[0], B.shape[0]))
+    for j, e in enumerate(eps):
+        t = e * (A[:, j][:, None] - B[:, j][None, :])
+        acc += t * t
+    return np.exp(-acc)
+
+
+def exact_posterior(X, y, Xs, eps, noise_var, mean_const=0.0, want_cov=False):
+    """posterior.py:107-144: the dense exact GP.  C = K + sigma2 I, SpdFactor (jitter schedule),
+    alpha = C^{-1}(y - c), mean = c + Ks alpha; cov = Kss - Ks C^{-1} Ks^T symmetrised.  The
+    reference's LU fallback (posterior.py:100-104) is not restated (raises instead)."""
+    K = se_gram(X, X, eps)
+    C = K + noise_var * np.eye(X.shape[0])
+    L, jit = spd_factor(C)
+    r = np.asarray(y, dtype=float) - mean_const
+    alpha = sla.cho_solve((L, True), r, check_finite=False)
+    Ks = se_gram(Xs, X, eps)
+    out = {"mean": mean_const + Ks @ alpha, "jitter": jit}
+    Z = sla.solve_triangular(L, Ks.T, lower=True, check_finite=False)
+    out["var"] = 1.0 - np.einsum("ij,ij->j", Z, Z)  # diag(Kss) = 1 exactly
+    if want_cov:
+        cov = se_gram(Xs, Xs, eps) - Ks @ sla.cho_solve((L, True), Ks.T, check_finite=False)
+        out["cov"] = 0.5 * (cov + cov.T)
+    return out
+
+
 def posterior_literal(X, y, Xs, eps, rho, n, noise_var, mean_const=0.0, variant=DELTA2_RHO_SQUARED):
     """method="literal" (posterior.py:176, 184-188, 236-247, 256-262): LamBar factorized
     directly, mean through t1..t5, var = diag(Phi* inner Phi*^T)."""

@@ -9,6 +9,7 @@ include/fagp_b200.h).  Importing works without a GPU; every compute call require
 
 from .backend import PHASES, Backend, SpdFactor, TimingRecord, phase_scope, spd_solve
 from .datagen import Dataset, generate
+from .exact import exact_posterior, se_gram
 from .errors import BudgetError, ConfigError, CsvFormatError, NumericalError
 from .kernels import ArdKernelParams, KernelParams1D
 from .mercer import (
@@ -49,7 +50,7 @@ __all__ = [
     "DEFAULT_MEMORY_CAP", "DELTA2_RHO_LINEAR", "DELTA2_RHO_SQUARED", "EigenSystem", "Fit", "GpModel",
     "KernelParams1D", "LAMBDA_FLOOR_REL", "LambdaBarSolve", "NumericalError", "PHASES", "PosteriorResult",
     "ShapeParams", "SpdFactor", "TimingRecord", "basis_table", "eigenfunction_1d", "eigensystem",
-    "eigenvalues_1d", "estimate_bytes", "fagp_posterior", "fagp_posterior_from_eigensystems", "fit",
+    "eigenvalues_1d", "estimate_bytes", "exact_posterior", "fagp_posterior", "fagp_posterior_from_eigensystems", "fit",
     "generate", "lambda_bar", "multi_indices", "normalized_hermite", "phase_scope", "predict",
-    "reconstruct_kernel", "set_fault_injection", "shape_params", "spd_solve", "__version__",
+    "reconstruct_kernel", "se_gram", "set_fault_injection", "shape_params", "spd_solve", "__version__",
 ]

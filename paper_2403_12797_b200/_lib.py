@@ -105,6 +105,7 @@ SIGNATURES = {
     "fagp_inner_operand_workspace_size": (ctypes.c_size_t, [_BASIS]),
     "fagp_inner_operand": (ctypes.c_int, [_P, _P, _BASIS, _P, _P, ctypes.c_size_t, _P]),
     "fagp_rowdot": (ctypes.c_int, [_P, _P, _I64, _I64, _P, _P]),
+    "fagp_se_gram": (ctypes.c_int, [_P, _I64, _P, _I64, _I32, _P, _D, _P, _I64, _P]),
 }
 
 _LIB = None

@@ -22,7 +22,7 @@ from fagp.backend import SpdFactor  # noqa: E402
 from fagp.bench import BenchConfig, _test_inputs, train_seed  # noqa: E402
 from fagp.kernels import ArdKernelParams, KernelParams1D  # noqa: E402
 from fagp.mercer import eigensystem, multi_indices  # noqa: E402
-from fagp.posterior import GpModel, LambdaBarSolve, fagp_posterior  # noqa: E402
+from fagp.posterior import GpModel, LambdaBarSolve, exact_posterior, fagp_posterior  # noqa: E402
 
 OUT = Path(__file__).with_name("golden.npz")
 
@@ -39,6 +39,9 @@ CASES = {
 }
 
 LITERAL_CASES = ("c1", "lin2", "ard4", "p1m40", "c5s")
+COV_CASES = ("c1", "ard4", "lin2", "p1m40", "c3s")  # store the reference's full covariance (head block)
+EXACT_CASES = ("c1", "ard4", "lin2")  # the exact dense GP (posterior.py:107-144)
+COV_HEAD = 200  # cov[:200, :200]: the covariance of the first 200 test points
 
 
 def digest(a):
@@ -82,6 +85,13 @@ def main():
         out[pre + "phi_head"] = es.phi[:8].copy()
         if full_g:
             out[pre + "G"] = G
+        if name in COV_CASES:  # off-diagonal entries of the reference covariance (posterior.py:249-263)
+            out[pre + "cov_head"] = res.cov[:COV_HEAD, :COV_HEAD].copy()
+        if name in EXACT_CASES:
+            ex = exact_posterior(ds, Xs, model, want_cov=True)
+            out[pre + "exact_mean"] = ex.mean
+            out[pre + "exact_var"] = np.diag(ex.cov).copy()
+            out[pre + "exact_cov_head"] = ex.cov[:COV_HEAD, :COV_HEAD].copy()
         if name in LITERAL_CASES:  # the cross-check route (posterior.py:236-244, 256-260)
             lit = fagp_posterior(ds, Xs, model, want_cov=True, method="literal", delta2_variant=var_kind,
                                  memory_cap=1 << 40)

@@ -8,8 +8,10 @@ is the product's real all-reduce payload, the packed modal [K | t] buffer (L^p +
 
   * fagp_posterior(group=) from host arrays (PosteriorEngine.run_host -> stage_reduce), from
     device tensors (PosteriorEngine.run), fit(group=) + predict, and
-    fagp_posterior_sharded(gather=True): mean and var equal the one-rank result to 1e-13
-    (elementwise relative; the cross-rank sum adds in another order);
+    fagp_posterior_sharded(gather=True): mean and var match the CPU oracle to 1e-9 (the parity
+    bar) and the one-rank result to 1e-10 -- the cross-rank sum adds the Gram in another order,
+    and this system (cond(A) ~ 1e8) turns that last-bit difference of G into ~1e-11 of the mean
+    (measured on the B200: 1.2e-11; two blockings of the CPU oracle's Gram differ alike);
   * run-to-run bitwise at a fixed world size.
 Reference: /root/reference/pkg/src/fagp/backend.py:109-130 (the row partition of the Gram).
 """
@@ -96,6 +98,9 @@ def _worker(rank, world, port, outdir):
     dist.destroy_process_group()
 
 
+RANK_TOL = 1e-10  # summation-order sensitivity of the posterior (see the docstring)
+
+
 def _rel(a, b):
     return float(np.max(np.abs(a - b) / np.abs(b)))
 
@@ -104,6 +109,8 @@ def test_two_ranks_match_one_rank():
     import paper_2403_12797_b200 as F
     from paper_2403_12797_b200.distributed import shard_range
 
+    import fagp_oracle as O
+
     X, y, Xs = _inputs()
 
     class Full:
@@ -111,6 +118,8 @@ def test_two_ranks_match_one_rank():
 
     Full.X, Full.y = X, y
     ref = F.fagp_posterior(Full, Xs, _model(), memory_cap=None)
+    orc = O.posterior(X, y, Xs, [1.0] * P, [1.0] * P, M, NOISE, 0.1)
+    assert _rel(ref.mean, orc["mean"]) <= 1e-9 and _rel(ref.var, orc["var"]) <= 1e-9
     world = 2
     with tempfile.TemporaryDirectory() as td:
         mp.start_processes(_worker, args=(world, _free_port(), td), nprocs=world, join=True, start_method="spawn")
@@ -120,11 +129,12 @@ def test_two_ranks_match_one_rank():
         # bitwise run to run at a fixed world size
         assert np.array_equal(o["host0_mean"], o["host1_mean"]) and np.array_equal(o["host0_var"], o["host1_var"])
         for key in ("host0", "dev", "fit"):
-            assert _rel(o[key + "_mean"], ref.mean[c:d]) <= 1e-13, (r, key)
-            assert _rel(o[key + "_var"], ref.var[c:d]) <= 1e-13, (r, key)
+            assert _rel(o[key + "_mean"], ref.mean[c:d]) <= RANK_TOL, (r, key, _rel(o[key + "_mean"], ref.mean[c:d]))
+            assert _rel(o[key + "_var"], ref.var[c:d]) <= RANK_TOL, (r, key, _rel(o[key + "_var"], ref.var[c:d]))
+            assert _rel(o[key + "_mean"], orc["mean"][c:d]) <= 1e-9 and _rel(o[key + "_var"], orc["var"][c:d]) <= 1e-9
         # the device-resident, host-pipelined and fit/predict routes reduce the same buffer
         assert np.array_equal(o["dev_mean"], o["host0_mean"]) and np.array_equal(o["fit_var"], o["host0_var"])
         # gathered: every rank holds the full vectors, in rank order
         assert o["sharded_mean"].shape == (NS,)
-        assert _rel(o["sharded_mean"], ref.mean) <= 1e-13 and _rel(o["sharded_var"], ref.var) <= 1e-13
+        assert _rel(o["sharded_mean"], ref.mean) <= RANK_TOL and _rel(o["sharded_var"], ref.var) <= RANK_TOL
     assert np.array_equal(outs[0]["sharded_mean"], outs[1]["sharded_mean"])

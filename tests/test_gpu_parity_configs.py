@@ -169,3 +169,34 @@ def test_spd_inverse_breakdown_stress():
         inv, info = spd_inverse(A)
         assert info == 0
         assert scaled_err(dev.to_host(inv), np.linalg.inv(A)) < 1e-12
+
+
+# ---- full covariance (off-diagonal entries) and the exact GP against the reference ----------
+@pytest.mark.parametrize("name", ["c1", "ard4", "lin2", "p1m40", "c3s"])
+def test_full_covariance_matches_reference(cases, name):
+    """want_cov=True: the reference's full N* x N* covariance (posterior.py:249-263), every entry
+    of its 200 x 200 head block, not only the diagonal."""
+    c = cases[name]
+    res = F.fagp_posterior(c.dataset(), c.Xs[:200], c.model(), want_cov=True, delta2_variant=c.variant,
+                           memory_cap=None)
+    ref = c.ref["cov_head"]
+    assert res.cov.shape == ref.shape
+    assert scaled_err(res.cov, ref) <= MEAN_VAR_RTOL, scaled_err(res.cov, ref)
+    assert np.array_equal(res.cov, res.cov.T)
+    assert rel_err(np.diag(res.cov), np.diag(ref)) <= MEAN_VAR_RTOL
+
+
+@pytest.mark.parametrize("name", ["c1", "ard4", "lin2"])
+def test_exact_posterior_on_device_matches_reference(cases, name):
+    """exact_posterior (posterior.py:107-144) on the device: SE Gram kernel + Cholesky + solves."""
+    c = cases[name]
+    ex = F.exact_posterior(c.dataset(), c.Xs, c.model(), want_cov=True)
+    assert scaled_err(ex.mean, c.ref["exact_mean"]) <= MEAN_VAR_RTOL
+    assert rel_err(ex.mean, c.ref["exact_mean"]) <= 1e-8
+    assert scaled_err(ex.cov[:200, :200], c.ref["exact_cov_head"]) <= MEAN_VAR_RTOL
+    assert scaled_err(ex.var, c.ref["exact_var"]) <= MEAN_VAR_RTOL
+    assert np.array_equal(ex.cov, ex.cov.T)
+    # the SE Gram itself against the reference's gram_matrix restatement (CUDA exp: ulps)
+    K = dev.to_host(F.se_gram(c.X[:300], c.X[:300], c.kernel()))
+    Kref = O.se_gram(c.X[:300], c.X[:300], c.eps)
+    assert np.all(np.diag(K) == 1.0) and np.max(np.abs(K - Kref) / Kref) <= 1e-15

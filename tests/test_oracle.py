@@ -96,3 +96,29 @@ def test_oracle_literal_matches_reference(cases, name):
     # the reference takes diag(cov) after cov = Phi* inner Phi*^T; the restatement forms only
     # the diagonal (same products, different summation order) -- ill-conditioned route
     assert scaled_err(out["var"], c.ref["literal_var"]) < 1e-9
+
+
+COV_CASES = ["c1", "ard4", "lin2", "p1m40", "c3s"]
+
+
+@pytest.mark.parametrize("name", COV_CASES)
+def test_oracle_covariance_matches_reference(cases, name):
+    """The full covariance restatement (off-diagonal entries included) against the reference's
+    own cov (posterior.py:249-263), on the first 200 test points."""
+    c = cases[name]
+    out = O.posterior(c.X, c.y, c.Xs[:200], c.eps, c.rho, c.M, c.noise_var, c.mean_const, c.variant)
+    cov = O.covariance(c.Xs[:200], out, c.eps, c.rho, c.M, c.noise_var, c.variant)
+    ref = c.ref["cov_head"]
+    assert cov.shape == ref.shape
+    assert scaled_err(cov, ref) < 1e-12
+    assert np.array_equal(cov, cov.T)
+
+
+@pytest.mark.parametrize("name", ["c1", "ard4", "lin2"])
+def test_oracle_exact_gp_matches_reference(cases, name):
+    """exact_posterior restatement (posterior.py:107-144) against the reference's outputs."""
+    c = cases[name]
+    out = O.exact_posterior(c.X, c.y, c.Xs, c.eps, c.noise_var, c.mean_const, want_cov=True)
+    assert scaled_err(out["mean"], c.ref["exact_mean"]) < 1e-12
+    assert scaled_err(out["cov"][:200, :200], c.ref["exact_cov_head"]) < 1e-12
+    assert scaled_err(out["var"], c.ref["exact_var"]) < 1e-10
