@@ -117,7 +117,8 @@ struct GPlan {
   int64_t Klen, len;   // output layout [K (KA*KB) | t (TA*TB = m)]
   int64_t plen;        // one partial: (kmf NFK + tmf NFT) fragments of 64 doubles
   int br;                // rows per block (kGR, or kSR for the split kernel)
-  int64_t rows_per_cta;  // multiple of br
+  int64_t rows_per_cta;  // rows of one CTA (a multiple of 4; the last block of a CTA may be partial)
+  int bpc;               // blocks per CTA = ceil(rows_per_cta / br)
   int S;                 // sub-ranges per CTA = chunks a host pipeline may launch separately
   int grid, nparts;      // nparts = grid * S * G partials
   HermCoef hc;           // recurrence coefficients (constant-bank operands)
@@ -175,12 +176,13 @@ fused_gram_kernel(const double* __restrict__ X, const double* __restrict__ y, do
   // (sub-range k = blocks [k bpc / S, (k + 1) bpc / S)); this launch covers sub-ranges [k0, k1)
   // and writes one partial per (CTA, sub-range, row group)
   const int cta = int(blockIdx.x);
-  const int bpc = int(pl.rows_per_cta / kGR);
+  const int bpc = pl.bpc;
   auto sb = [&](int k) { return int(int64_t(k) * bpc / pl.S); };
   const int g0 = sb(k0);
   const int nblk = sb(k1) - g0;
+  const int64_t cta_end = tmin<int64_t>(N, int64_t(cta + 1) * pl.rows_per_cta);
   auto blk_base = [&](int j) -> int64_t { return int64_t(cta) * pl.rows_per_cta + int64_t(g0 + j) * kGR; };
-  auto blk_end = [&](int j) -> int64_t { return tmin<int64_t>(N, blk_base(j) + kGR); };
+  auto blk_end = [&](int j) -> int64_t { return tmin<int64_t>(cta_end, blk_base(j) + kGR); };
   bool bad_x = false;
 
   // production: thread t < kGR p evaluates phi and g (one shared exponential, two independent
@@ -412,12 +414,13 @@ fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int M = pl.M, L = pl.L;
   const int cta = int(blockIdx.x);
-  const int bpc = int(pl.rows_per_cta / BR);
+  const int bpc = pl.bpc;
   auto sb = [&](int k) { return int(int64_t(k) * bpc / pl.S); };
   const int g0 = sb(k0);
   const int nblk = sb(k1) - g0;
+  const int64_t cta_end = tmin<int64_t>(N, int64_t(cta + 1) * pl.rows_per_cta);
   auto blk_base = [&](int j) -> int64_t { return int64_t(cta) * pl.rows_per_cta + int64_t(g0 + j) * BR; };
-  auto blk_end = [&](int j) -> int64_t { return tmin<int64_t>(N, blk_base(j) + BR); };
+  auto blk_end = [&](int j) -> int64_t { return tmin<int64_t>(cta_end, blk_base(j) + BR); };
   bool bad_x = false;
   const bool plane = tid < kGR * p;
   const int prow = tid / p, pdim = tid - (tid / p) * p;
@@ -646,7 +649,13 @@ fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__
       if (n + 1 < nblk) load_pre(n + 1, pre))
       SPROF(3, __syncthreads())
     }
-    SPROF(0, _Pragma("unroll 2") for (int i = 0; i < BR / 4; ++i) kstep(cur, i))
+    // k-steps holding a valid row (a CTA's last block may be partial; padding rows are zero)
+    const int nks = int(tmax<int64_t>(0, blk_end(n) - blk_base(n)) + 3) / 4;
+    if (nks == BR / 4) {
+      SPROF(0, _Pragma("unroll 2") for (int i = 0; i < BR / 4; ++i) kstep(cur, i))
+    } else {
+      SPROF(0, for (int i = 0; i < nks; ++i) kstep(cur, i))
+    }
     if (pl.once) {
       SPROF(2, if (n + 1 == nblk) flush(0))
     } else {
@@ -795,13 +804,17 @@ static bool make_gplan(int64_t N, int p, int M, GPlan& pl) {
   // sub-range holds at least 2 blocks), so a host pipeline can upload sub-range k + 1 of every
   // CTA while the Gram contracts sub-range k -- the first chunk, the only upload not hidden
   // behind the contraction, is 1/S of the rows
+  // The rows are cut evenly (in whole k-steps of 4) over the CTAs, so a CTA's last block may be
+  // partial (the split kernel skips its empty k-steps): the makespan is N / grid rows, not a
+  // whole number of blocks.
   const int64_t blocks = tmax<int64_t>(1, ceil_div(N, pl.br));
   pl.grid = int(tmin<int64_t>(num_sms(), blocks));
-  const int64_t bpc = ceil_div(blocks, pl.grid);  // blocks per CTA
+  pl.rows_per_cta = tmax<int64_t>(4, ceil_div(ceil_div(tmax<int64_t>(N, 1), pl.grid), 4) * 4);
+  const int64_t bpc = ceil_div(pl.rows_per_cta, pl.br);  // blocks per CTA
+  pl.bpc = int(bpc);
   pl.S = bpc >= 16 ? 8 : bpc >= 8 ? 4 : 1;
   if (const char* e = getenv("FAGP_GRAM_SUBRANGES")) pl.S = tmax(1, tmin<int>(int(bpc), atoi(e)));  // tuning knob
   pl.S = tmin(pl.S, 64);  // ready words re-armed by one partial_sum block (and a sane chunk count)
-  pl.rows_per_cta = bpc * pl.br;
   pl.grid = int(tmax<int64_t>(1, ceil_div(tmax<int64_t>(N, 1), pl.rows_per_cta)));
   pl.nparts = pl.grid * pl.S * pl.G;
   pl.hc = herm_coef_host();
@@ -884,9 +897,9 @@ int upload_chunk(const double* Xh, const double* yh, int64_t N, int p, int M, in
     return FAGP_OK;
   }
   if (k < 0 || k >= pl.S) return FAGP_EINVAL;
-  const int64_t bpc = pl.rows_per_cta / pl.br;
+  const int64_t bpc = pl.bpc;
   const int64_t off = (int64_t(k) * bpc / pl.S) * pl.br;
-  const int64_t sub_rows = ((int64_t(k + 1) * bpc / pl.S) * pl.br) - off;
+  const int64_t sub_rows = tmin<int64_t>((int64_t(k + 1) * bpc / pl.S) * pl.br, pl.rows_per_cta) - off;
   // CTAs c with c rpc + off + sub_rows <= N
   const int64_t head = N - off - sub_rows;
   const int64_t full = head < 0 ? 0 : tmin<int64_t>(pl.grid, head / pl.rows_per_cta + 1);
