@@ -143,17 +143,26 @@ inline int gemm(bool transB, const GemmArgs& g, int batch, cudaStream_t s, bool 
 // ---------------------------------------------------------------------------------------
 // One warp: lower-triangular inverse of the 32x32 block in S (identity-padded beyond nb),
 // lane c computes column c by forward substitution.  Result into Xs.
+// Xs = S^{-1} for the lower triangular 32 x 32 S (one warp; lane c = column c, held in
+// registers): column-oriented forward elimination X[j][c] = y_j / S[j][j], then
+// y_r -= S[r][j] X[j][c] for r > j -- 32 dependent steps of independent FMAs (the row-oriented
+// dot-product form is ~500 dependent shared-memory round trips).  Column j of S is read as
+// broadcasts.
 __device__ __forceinline__ void warp_trinv(const double (*S)[33], double (*Xs)[33], int lane) {
   const int c = lane;
-  for (int i = 0; i < 32; ++i) {
-    double v = 0.0;
-    if (i >= c) {
-      double sum = (i == c) ? 1.0 : 0.0;
-      for (int l = c; l < i; ++l) sum -= S[i][l] * Xs[l][c];
-      v = sum / S[i][i];
-    }
-    Xs[i][c] = v;
+  const double dinv = 1.0 / S[c][c];  // lane j: 1 / S[j][j]
+  double y[32];
+#pragma unroll
+  for (int r = 0; r < 32; ++r) y[r] = r == c ? 1.0 : 0.0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const double xj = y[j] * __shfl_sync(0xffffffffu, dinv, j);
+    y[j] = xj;
+#pragma unroll
+    for (int r = j + 1; r < 32; ++r) y[r] = fma(-S[r][j], xj, y[r]);
   }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) Xs[i][c] = i >= c ? y[i] : 0.0;
 }
 
 // One step of the blocked right-looking Cholesky (NB = 32), one warp per CTA.  Every CTA

@@ -673,7 +673,8 @@ fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__
 
 // out[e] = sum over the partials (fixed order: deterministic) of entry e of [K | t], read from
 // the fragment-major partial layout; non-finite -> PHI flag
-constexpr int kPSE = 32, kPSG = 16;  // partial_sum: entries per CTA x partial groups
+constexpr int kPSE = 8, kPSG = 64;  // partial_sum: entries per CTA x partial groups (many groups: C2-size
+                                     // plans have ~2400 partials per entry)
 __global__ void __launch_bounds__(kPSE * kPSG) partial_sum_kernel(const double* __restrict__ ws, const GPlan pl,
                                                                   double* __restrict__ out, uint32_t* flags) {
   __shared__ double red[kPSG][kPSE];

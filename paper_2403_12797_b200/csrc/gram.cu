@@ -312,8 +312,17 @@ __global__ void gram_reduce_kernel(const double* __restrict__ ws, int64_t m, Pla
     const size_t off = size_t(i % BT) * BT + size_t(j % BT);
     const size_t stride = size_t(pl.npairs) * BT * BT;
     const double* src = ws + size_t(pair) * BT * BT + off;
+    // loads issued 8 at a time (an L2 round trip each otherwise); the sum keeps chunk order
     double sum = 0.0;
-    for (int s = 0; s < pl.S; ++s) sum += src[s * stride];
+    int s = 0;
+    for (; s + 8 <= pl.S; s += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = src[(s + u) * stride];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) sum += v[u];
+    }
+    for (; s < pl.S; ++s) sum += src[s * stride];
     packed[i * (2 * me - i - 1) / 2 + j] = sum;
     if (i == j && i < m && not_finite(sum)) raise_flag(flags, FAGP_FLAG_PHI_NONFINITE);
   }

@@ -15,7 +15,7 @@ for r in rows:
     if d.get("Metric Name") != "gpu__time_duration.sum":
         continue
     v = float(d["Metric Value"].replace(",", ""))
-    v = v / 1000 if d["Metric Unit"] == "nsecond" else v * 1000 if d["Metric Unit"] == "msecond" else v
+    v = v / 1000 if d["Metric Unit"] in ("nsecond", "ns") else v * 1000 if d["Metric Unit"] == "msecond" else v
     agg.setdefault(d["Kernel Name"][:64], []).append(v)
 for k, v in agg.items():
     print(f"{k:64s} n={len(v):3d} avg={sum(v) / len(v):9.2f} us  last={v[-1]:9.2f}")
