@@ -1494,8 +1494,17 @@ int predict(const double* Xs, int64_t Ns, const fagp_basis* b, const double* op,
 }  // namespace fused
 }  // namespace fagp
 
+namespace fagp {
+namespace tiled {  // gram_tiled.cu: the output-tiled fused Gram (shapes beyond fused_gram's registers)
+bool eligible(int64_t N, int p, int M);
+size_t workspace(int64_t N, int p, int M);
+int gram(const double* X, const double* y, double c, int64_t N, const fagp_basis* b, double* out, void* ws,
+         size_t ws_bytes, uint32_t* flags, cudaStream_t s);
+}  // namespace tiled
+}  // namespace fagp
+
 // =======================================================================================
-// C ABI: the point-input entry points (tables only where the fused layouts do not apply)
+// C ABI: the point-input entry points (tables only where no fused layout applies)
 using namespace fagp;
 
 extern "C" {
@@ -1503,6 +1512,7 @@ extern "C" {
 size_t fagp_gram_x_workspace_size(int64_t N, const fagp_basis* basis) {
   if (check_basis(basis) || N < 0) return 0;
   if (fused::gram_eligible(N, basis->p, basis->M)) return fused::gram_workspace(N, basis->p, basis->M);
+  if (tiled::eligible(N, basis->p, basis->M)) return tiled::workspace(N, basis->p, basis->M);
   const size_t table = size_t(N) * table_width(basis->p, basis->M) * sizeof(double);
   return round_up(table, 256) + fagp_gram_workspace_size(N, basis);
 }
@@ -1530,6 +1540,8 @@ int fagp_gram_x_chunk(const double* X, int64_t N, const fagp_basis* basis, const
   if (fused::gram_eligible(N, basis->p, basis->M))
     return fused::gram(X, y, mean_const, N, basis, k, k + 1, gram, workspace, workspace_bytes, flags, s, nullptr);
   if (k != 0) return FAGP_EINVAL;
+  if (tiled::eligible(N, basis->p, basis->M))
+    return tiled::gram(X, y, mean_const, N, basis, gram, workspace, workspace_bytes, flags, s);
   const size_t table = round_up(size_t(N) * table_width(basis->p, basis->M) * sizeof(double), 256);
   if (workspace == nullptr || workspace_bytes < table + fagp_gram_workspace_size(N, basis)) return FAGP_EWORKSPACE;
   double* T = static_cast<double*>(workspace);

@@ -264,7 +264,9 @@ def test_potrf_matches_lapack(m, impl, monkeypatch):
 
 # ---- the point-input (fused) entry points against the table path ----------------------
 @pytest.mark.parametrize("p,M,N", [(2, 10, 1), (2, 10, 63), (2, 10, 5000), (3, 10, 1), (3, 10, 64), (3, 10, 4097),
-                                   (3, 6, 777), (4, 4, 3001), (3, 10, 200_003)])
+                                   (3, 6, 777), (4, 4, 3001), (3, 10, 200_003),
+                                   # output-tiled fused Gram (gram_tiled.cu): C4 / C5 shapes, ragged N
+                                   (4, 8, 1), (4, 8, 3001), (4, 8, 70_001), (5, 6, 5), (5, 6, 2001), (6, 3, 999)])
 def test_gram_x_matches_table_gram(p, M, N):
     from paper_2403_12797_b200.posterior import gram_x_packed
 
