@@ -59,7 +59,8 @@ struct TPlan {
   int64_t LA, LB, MA, MB;  // column counts: K sides L^q, L^(p-q); t sides M^q, M^(p-q)
   int goff, poff, rpoff, one, zero, bw;  // row slab layout (doubles), bw % 16 == 4
   int BR;                                // rows per block
-  int pad_all;                           // experiment: every warp runs all 16 DMMAs (invalid fragments are zero)
+  int masked;                            // 0: a warp with any valid fragment runs all 16 DMMAs (invalid
+                                         // fragments are zero -- measured faster than predicated DMMAs); 1: skip
   long long* prof;                       // diagnostics build (-DFAGP_TILED_PROF): per CTA [tile, total, produce, k-loop, barrier] cycles of warp 0
   int ntiles;                            // K tiles
   int fr[2], nt[2];                      // per side: K fragments, tiles (fragments split evenly)
@@ -99,8 +100,9 @@ static int tile_cost(int na, int nb) {
     int wa, wb;
     warp_tile(w, wa, wb);
     const int va = tmax(0, tmin(kWF, na - kWF * wa)), vb = tmax(0, tmin(kWF, nb - kWF * wb));
-    pipe[w % 4] += 16 * va * vb;
-    if (va * vb > 0) serial[w % 4] = tmax(serial[w % 4], 700 + 16 * va * vb);
+    const int d = va * vb > 0 ? kWF * kWF : 0;  // a warp with any valid fragment runs all 16 DMMAs
+    pipe[w % 4] += 16 * d;
+    if (d > 0) serial[w % 4] = tmax(serial[w % 4], 700 + 16 * d);
   }
   int c = 0;
   for (int s = 0; s < 4; ++s) c = tmax(c, tmax(pipe[s] * 100 / 69, serial[s]));
@@ -186,7 +188,7 @@ static bool make_tplan(int64_t N, int p, int M, TPlan& pl) {
   }
   pl.grid = f;
   pl.hc = herm_coef_host();
-  if (const char* e = getenv("FAGP_TILED_PAD")) pl.pad_all = atoi(e);
+  if (const char* e = getenv("FAGP_TILED_MASKED")) pl.masked = atoi(e);  // A/B knob
   return true;
 }
 
@@ -300,6 +302,8 @@ __device__ __forceinline__ void tile_body(const double* __restrict__ X, const do
   auto produce = [&](int64_t base) {
     cp_async_wait<0>();
     __syncthreads();
+    // the two items one after the other (advancing them in lockstep needs more registers than the
+    // 32 accumulators leave)
 #pragma unroll 1
     for (int u = 0; u < 2; ++u) {
       if (!pon[u]) continue;
@@ -348,7 +352,7 @@ __device__ __forceinline__ void tile_body(const double* __restrict__ X, const do
         dmma_8x8x4(accT[j][0], accT[j][1], a, bv);
       }
   };
-  const bool full = pl.pad_all || (nva == kWF && nvb == kWF);
+  const bool full = !pl.masked || (nva == kWF && nvb == kWF);
   auto mma_full = [&](const Ops& o) {
 #pragma unroll
     for (int j = 0; j < kWF; ++j)
