@@ -659,6 +659,47 @@ inline size_t potrf_ws_bytes(int64_t m) {
   return align256(sizeof(int)) + align256(32 * 32 * sizeof(double)) + align256(size_t(chol_scratch_len(m)) * sizeof(double));
 }
 
+// D = X^T X for the lower-triangular n x n X (D full symmetric; LAPACK dlauum's product), by
+// recursive halving so the zero upper half of X is never multiplied:
+//   X = [X11 0; X21 X22]:  D22 = X22^T X22 (recursive),  D21 = X22^T X21,
+//                          D11 = X11^T X11 (recursive) + X21^T X21 (lower triangle only)
+// -- about n^3 / 2 flops on the DMMA GEMM instead of the full product's 2 n^3 (C4: 4.6 -> ~1.2 ms
+// at m = 4096).  Leaves (n <= 512) are one lower-only GEMM; the upper triangle is mirrored last.
+__global__ void mirror_lower_kernel(double* D, int64_t n, int64_t ldd) {
+  const int64_t total = n * n;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / n, j = e - (e / n) * n;
+    if (j > i) D[i * ldd + j] = D[j * ldd + i];
+  }
+}
+
+static int lauum_lower_rec(const double* X, int64_t ldx, int64_t n, double* D, int64_t ldd, cudaStream_t s) {
+  if (n <= 512) {
+    GemmArgs g{int(n), int(n), int(n), 1.0, 0.0, X, ldx, 0, X, ldx, 0, D, ldd, 0, 1, nullptr};
+    return gemm(false, g, 1, s, true);
+  }
+  const int64_t h = round_up(n / 2, 64), r = n - h;
+  const double* X21 = X + h * ldx;
+  const double* X22 = X21 + h;
+  int rc = lauum_lower_rec(X22, ldx, r, D + h * ldd + h, ldd, s);
+  if (rc) return rc;
+  GemmArgs g21{int(r), int(h), int(r), 1.0, 0.0, X22, ldx, 0, X21, ldx, 0, D + h * ldd, ldd, 0, 0, nullptr};
+  rc = gemm(false, g21, 1, s, true);
+  if (rc) return rc;
+  rc = lauum_lower_rec(X, ldx, h, D, ldd, s);
+  if (rc) return rc;
+  GemmArgs g11{int(h), int(h), int(r), 1.0, 1.0, X21, ldx, 0, X21, ldx, 0, D, ldd, 0, 1, nullptr};
+  return gemm(false, g11, 1, s, true);
+}
+
+int lauum_lower(const double* X, int64_t ldx, int64_t n, double* D, int64_t ldd, cudaStream_t s) {
+  int rc = lauum_lower_rec(X, ldx, n, D, ldd, s);
+  if (rc) return rc;
+  mirror_lower_kernel<<<int(tmin<int64_t>(ceil_div(n * n, 256), 8 * num_sms())), 256, 0, s>>>(D, n, ldd);
+  FAGP_LAUNCH_CHECK();
+  return FAGP_OK;
+}
+
 }  // namespace la
 }  // namespace fagp
 
@@ -866,8 +907,7 @@ int fagp_factor(const double* packed, const fagp_basis* basis, const double* sqr
   if (predict_op) {
     if (pm) {
       // D = X^T X (X = L^{-1}, lower), then the pair-folded Ct = fold(S D S) and w
-      GemmArgs g{int(m), int(m), int(m), 1.0, 0.0, ws.X, mp, 0, ws.X, mp, 0, ws.D, m, 0, 0, nullptr};
-      int rc = gemm(false, g, 1, s, true);
+      int rc = lauum_lower(ws.X, mp, m, ws.D, m, s);
       if (rc) return rc;
       rc = modal::build_predict_op(ws.D, sqrt_lam, w, basis, predict_op, ws.Lp, ws.X, s);
       if (rc) return rc;
