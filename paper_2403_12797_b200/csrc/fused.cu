@@ -398,6 +398,7 @@ fused_gram_kernel(const double* __restrict__ X, const double* __restrict__ y, do
 // m-fragments, role 2 warps JK2 K2, JT2 T2 and JT1B T1 m-fragments (fragment ids strided by the
 // role's warp count), 9 DMMA per warp per k-step each.  Production, blocks, sub-ranges and the
 // partial flush are those of fused_gram_kernel.
+constexpr int kSplitGramBW = 100;  // row_layout(3, 10).bw
 template <int JK1, int JT1A, int JK2, int JT2, int JT1B, int BR>
 __global__ void __launch_bounds__(kGramNT, 1)
 fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__ y, double c, int64_t N,
@@ -410,6 +411,10 @@ fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__
   constexpr int PR = BR / kGR;
   constexpr int NSLAB = PR == 1 ? 2 : 1;
   const RowLayout rl = row_layout(p, pl.M);
+  // the row stride as a compile-time constant (row_layout(3, 10).bw, checked on the host): every
+  // operand address of a k-step is then a loop-invariant register plus an immediate -- no
+  // per-load address arithmetic in the k-loop
+  constexpr int SBW = kSplitGramBW;
   double* slabs = sm;  // [NSLAB][BR * bw]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int M = pl.M, L = pl.L;
@@ -571,7 +576,7 @@ fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__
   __syncthreads();
 
   auto kstep = [&](const double* cur, int i) {
-    const double* row = cur + (i * 4 + (lane & 3)) * rl.bw;
+    const double* row = cur + (i * 4 + (lane & 3)) * SBW;
     if (role1) {
       const double b0 = row[offB[0]], b1 = row[offB[1]], bt = row[offB[2]];
 #pragma unroll
@@ -652,7 +657,7 @@ fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__
     // k-steps holding a valid row (a CTA's last block may be partial; padding rows are zero)
     const int nks = int(tmax<int64_t>(0, blk_end(n) - blk_base(n)) + 3) / 4;
     if (nks == BR / 4) {
-      SPROF(0, _Pragma("unroll 2") for (int i = 0; i < BR / 4; ++i) kstep(cur, i))
+      SPROF(0, _Pragma("unroll 16") for (int i = 0; i < BR / 4; ++i) kstep(cur, i))
     } else {
       SPROF(0, for (int i = 0; i < nks; ++i) kstep(cur, i))
     }
@@ -794,7 +799,7 @@ static bool make_gplan(int64_t N, int p, int M, GPlan& pl) {
   if (smem > 225 * 1024) return false;
   // split layout (fused_gram_split_kernel): p = 3, M = 10 (the BASELINE C3 shape)
   const char* se = getenv("FAGP_GRAM_SPLIT");
-  const bool split = p == 3 && M == 10 && !(se && se[0] == '0');
+  const bool split = p == 3 && M == 10 && !(se && se[0] == '0') && row_layout(3, 10).bw == kSplitGramBW;
   pl.br = kGR;
   if (split) {
     const char* be = getenv("FAGP_GRAM_BR");  // tuning knob: 128 = double-buffered 128-row slabs
@@ -1007,10 +1012,11 @@ __device__ __forceinline__ void unpack_off(uint32_t v, int (&off)[F]) {
 // A gathered from the row slab by the packed offsets of kappa = 4 ks + (lane & 3), B from the
 // fragment-major operand.  Software-pipelined: the operands of k-step ks + 1 are loaded and
 // multiplied in program order before the DMMAs of k-step ks, so they overlap.
-template <int F, int NF>
-__device__ __forceinline__ void contract(const double* row0, int bw, const uint32_t* offs, const double* B, int k0,
+template <int F, int NF, int BW = 0>
+__device__ __forceinline__ void contract(const double* row0, int bw_rt, const uint32_t* offs, const double* B, int k0,
                                          int k1, int lane, double (&acc)[kPMF][NF][2]) {
   if (k0 >= k1) return;
+  const int bw = BW ? BW : bw_rt;  // compile-time row stride where known: immediate load offsets
   auto load = [&](int ks, double (&ao)[kPMF], double (&bo)[NF]) {
     int off[F];
     unpack_off<F>(offs[4 * ks + (lane & 3)], off);
@@ -1234,13 +1240,15 @@ fused_predict_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView b, con
 //   mean2: A = (phi0[8, M), phi2)     x B = w[8 + a0'][a1][a2] over a1            epilogue phi1[a1]
 // (19% fewer DMMA at C3).  Same blocks, production, warp split and reduction as
 // fused_predict_kernel.
+template <int BW>
 __global__ void __launch_bounds__(kPredNT, 1)
 fused_predict_split_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView b, const VPlan pl,
                            const double* __restrict__ op, double sigma2, double c, double* __restrict__ mean,
                            double* __restrict__ var, uint32_t* flags) {
   constexpr int P = 3;
   extern __shared__ double sm[];
-  const RowLayout rl = row_layout(P, pl.M);
+  RowLayout rl = row_layout(P, pl.M);
+  rl.bw = BW;  // == row_layout(3, M).bw (the launcher picks BW by M)
   const bool want_var = var != nullptr;
   const int M = pl.M, L = pl.L, R = L - 16, R2 = M - 8;
   const int vk1 = (L * L + 3) / 4, vk2 = (R * L + 3) / 4, mk1 = (M * M + 3) / 4, mk2 = (R2 * M + 3) / 4;
@@ -1341,11 +1349,11 @@ fused_predict_split_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView 
         aM1[f][0][e] = aM2[f][0][e] = aM2[f][1][e] = 0.0;
       }
     if (want_var) {
-      contract<2, 2>(row0, rl.bw, offV1, Bv1, half(vk1, kq), half(vk1, kq + 1), lane, aV1);
-      contract<2, 3>(row0, rl.bw, offV2, Bv2, half(vk2, kq), half(vk2, kq + 1), lane, aV2);
+      contract<2, 2, BW>(row0, rl.bw, offV1, Bv1, half(vk1, kq), half(vk1, kq + 1), lane, aV1);
+      contract<2, 3, BW>(row0, rl.bw, offV2, Bv2, half(vk2, kq), half(vk2, kq + 1), lane, aV2);
     }
-    contract<2, 1>(row0, rl.bw, offM1, Bm1, half(mk1, kq), half(mk1, kq + 1), lane, aM1);
-    contract<2, 2>(row0, rl.bw, offM2, Bm2, half(mk2, kq), half(mk2, kq + 1), lane, aM2);
+    contract<2, 1, BW>(row0, rl.bw, offM1, Bm1, half(mk1, kq), half(mk1, kq + 1), lane, aM1);
+    contract<2, 2, BW>(row0, rl.bw, offM2, Bm2, half(mk2, kq), half(mk2, kq + 1), lane, aM2);
 #pragma unroll
     for (int f = 0; f < kPMF; ++f) {
       const double* row = row0 + 8 * f * rl.bw;
@@ -1473,11 +1481,18 @@ int predict(const double* Xs, int64_t Ns, const fagp_basis* b, const double* op,
   const char* se = getenv("FAGP_PREDICT_SPLIT");
   if (b->p == 3 && pl.pN == 1 && b->M >= 9 && b->M <= 12 && !(se && se[0] == '0')) {
     const size_t smem = split_predict_smem(b->M);
-    FAGP_CUDA_TRY(cudaFuncSetAttribute(fused_predict_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(smem)));
-    fused_predict_split_kernel<<<pl.grid, kPredNT, smem, s>>>(Xs, Ns, view(b), pl, op, sigma2, c, mean, var, flags);
-    FAGP_LAUNCH_CHECK();
-    return FAGP_OK;
+    auto go = [&](auto kern) -> int {
+      FAGP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      kern<<<pl.grid, kPredNT, smem, s>>>(Xs, Ns, view(b), pl, op, sigma2, c, mean, var, flags);
+      FAGP_LAUNCH_CHECK();
+      return FAGP_OK;
+    };
+    switch (row_layout(3, b->M).bw) {  // compile-time row strides (M 9, 10: 100; 11: 116; 12: 132)
+      case 100: return go(fused_predict_split_kernel<100>);
+      case 116: return go(fused_predict_split_kernel<116>);
+      case 132: return go(fused_predict_split_kernel<132>);
+      default: return FAGP_EUNSUPPORTED;
+    }
   }
   int rc;
   switch (b->p - pl.pN) {
