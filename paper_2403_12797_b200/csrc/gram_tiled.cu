@@ -227,11 +227,13 @@ __device__ __forceinline__ double prod(const double* row, const int (&off)[F]) {
 
 // One CTA: K tile T over rows [r0, r1), plus t pairs T + ntiles (warp + 16 j), j < JT.  FA = q,
 // FB = p - q factors per side.
-template <int FA, int FB, int JT>
+template <int FA, int FB, int JT, int BW>
 __device__ __forceinline__ void tile_body(const double* __restrict__ X, const double* __restrict__ y, double c,
                                           const BasisView& b, const TPlan& pl, int T, int64_t r0, int64_t r1,
                                           double* __restrict__ part, double* slab, bool& bad_x) {
   const Tile tl = pl.tiles[T];
+  const int bw = BW ? BW : pl.bw;  // compile-time row stride where known (C4: 116, C5: 100): the
+                                   // k-loop's operand addresses become register + immediate
   const int p = pl.p, M = pl.M, L = pl.L;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   int wa, wb;
@@ -285,7 +287,7 @@ __device__ __forceinline__ void tile_body(const double* __restrict__ X, const do
   }
   // the next block's x (BR p doubles) and y (BR) are staged by cp.async while this block is
   // contracted (no registers held across the k-loop)
-  double* xs = slab + (BR + 1) * pl.bw;  // [BR p]
+  double* xs = slab + (BR + 1) * bw;  // [BR p]
   double* ys = xs + BR * p;              // [BR]
   auto load = [&](int64_t base) {
     const int64_t nr = tmin<int64_t>(BR, r1 - base);
@@ -309,7 +311,7 @@ __device__ __forceinline__ void tile_body(const double* __restrict__ X, const do
       if (!pon[u]) continue;
       const double px = xs[prow[u] * p + pdim[u]];
       const double py = (y != nullptr && pdim[u] == p - 1) ? ys[prow[u]] : c;
-      double* row = slab + prow[u] * pl.bw;
+      double* row = slab + prow[u] * bw;
       const bool valid = base + prow[u] < r1;
       double* oph = row + pl.poff + pdim[u] * M;
       double* og = row + pl.goff + pdim[u] * L;
@@ -333,14 +335,14 @@ __device__ __forceinline__ void tile_body(const double* __restrict__ X, const do
     double a[kWF], b[kWF];
   };
   auto ops = [&](int i, Ops& o) {
-    const double* row = slab + (i * 4 + (lane & 3)) * pl.bw;
+    const double* row = slab + (i * 4 + (lane & 3)) * bw;
 #pragma unroll
     for (int j = 0; j < kWF; ++j) o.a[j] = prod<FA>(row, offA[j]);
 #pragma unroll
     for (int k = 0; k < kWF; ++k) o.b[k] = prod<FB>(row, offB[k]);
   };
   auto tstep = [&](int i) {
-    const double* row = slab + (i * 4 + (lane & 3)) * pl.bw;
+    const double* row = slab + (i * 4 + (lane & 3)) * bw;
 #pragma unroll
     for (int j = 0; j < JT; ++j)
       if (tval[j]) {
@@ -386,7 +388,7 @@ __device__ __forceinline__ void tile_body(const double* __restrict__ X, const do
     const int nks = int((tmin<int64_t>(BR, r1 - base) + 3) / 4);
     if (nva > 0 && nvb > 0) {
       if (full) {
-#pragma unroll 2
+#pragma unroll 4
         for (int i = 0; i < nks; ++i) {
           Ops o;
           ops(i, o);
@@ -433,7 +435,7 @@ __device__ __forceinline__ void tile_body(const double* __restrict__ X, const do
         make_double2(accT[j][0], accT[j][1]);
 }
 
-template <int FA, int FB, int JT>
+template <int FA, int FB, int JT, int BW>
 __global__ void __launch_bounds__(kNT, 1)
 tiled_gram_kernel(const double* __restrict__ X, const double* __restrict__ y, double c, BasisView b,
                   const __grid_constant__ TPlan pl, double* __restrict__ ws, uint32_t* flags) {
@@ -445,7 +447,7 @@ tiled_gram_kernel(const double* __restrict__ X, const double* __restrict__ y, do
   const int64_t per = round_up(ceil_div(tmax<int64_t>(pl.N, 1), cnt), 4);
   const int64_t r0 = tmin<int64_t>(pl.N, int64_t(j) * per), r1 = tmin<int64_t>(pl.N, r0 + per);
   bool bad_x = false;
-  tile_body<FA, FB, JT>(X, y, c, b, pl, T, r0, r1, ws + int64_t(cta) * kPartial, slab, bad_x);
+  tile_body<FA, FB, JT, BW>(X, y, c, b, pl, T, r0, r1, ws + int64_t(cta) * kPartial, slab, bad_x);
   if (pl.prof && threadIdx.x == 0) pl.prof[5 * cta] = T;
   if (bad_x) raise_flag(flags, FAGP_FLAG_X_NONFINITE);
 }
@@ -511,15 +513,26 @@ size_t workspace(int64_t N, int p, int M) {
   return size_t(pl.grid) * kPartial * sizeof(double);
 }
 
-template <int FA, int FB, int JT>
-static int launch_jt(const double* X, const double* y, double c, const fagp_basis* b, const TPlan& pl, double* ws,
+template <int FA, int FB, int JT, int BW>
+static int launch_bw(const double* X, const double* y, double c, const fagp_basis* b, const TPlan& pl, double* ws,
                   uint32_t* flags, cudaStream_t s) {
   const size_t smem = (size_t(pl.BR + 1) * pl.bw + size_t(pl.BR) * (pl.p + 1)) * sizeof(double);
-  FAGP_CUDA_TRY(cudaFuncSetAttribute(tiled_gram_kernel<FA, FB, JT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(smem)));
-  tiled_gram_kernel<FA, FB, JT><<<pl.grid, kNT, smem, s>>>(X, y, c, view(b), pl, ws, flags);
+  FAGP_CUDA_TRY(cudaFuncSetAttribute(tiled_gram_kernel<FA, FB, JT, BW>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  tiled_gram_kernel<FA, FB, JT, BW><<<pl.grid, kNT, smem, s>>>(X, y, c, view(b), pl, ws, flags);
   FAGP_LAUNCH_CHECK();
   return FAGP_OK;
+}
+
+// BASELINE C4 (p 4, M 8: stride 116) and C5 (p 5, M 6: stride 100) get compile-time strides
+template <int FA, int FB, int JT>
+static int launch_jt(const double* X, const double* y, double c, const fagp_basis* b, const TPlan& pl, double* ws,
+                     uint32_t* flags, cudaStream_t s) {
+  if constexpr (FA == 2 && FB == 2 && JT == 1)
+    if (pl.bw == 116) return launch_bw<FA, FB, JT, 116>(X, y, c, b, pl, ws, flags, s);
+  if constexpr (FA == 2 && FB == 3 && JT == 1)
+    if (pl.bw == 100) return launch_bw<FA, FB, JT, 100>(X, y, c, b, pl, ws, flags, s);
+  return launch_bw<FA, FB, JT, 0>(X, y, c, b, pl, ws, flags, s);
 }
 
 template <int FA, int FB>
