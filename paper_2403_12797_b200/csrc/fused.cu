@@ -1516,6 +1516,12 @@ size_t workspace(int64_t N, int p, int M);
 int gram(const double* X, const double* y, double c, int64_t N, const fagp_basis* b, double* out, void* ws,
          size_t ws_bytes, uint32_t* flags, cudaStream_t s);
 }  // namespace tiled
+namespace ptiled {  // predict_tiled.cu: the output-tiled fused predict
+bool eligible(int p, int M);
+size_t workspace(int64_t Ns, int p, int M);
+int predict(const double* Xs, int64_t Ns, const fagp_basis* b, const double* op, double sigma2, double c,
+            double* mean, double* var, void* ws, size_t ws_bytes, uint32_t* flags, cudaStream_t s);
+}  // namespace ptiled
 }  // namespace fagp
 
 // =======================================================================================
@@ -1614,6 +1620,7 @@ int64_t fagp_predict_x_wave_rows(const fagp_basis* basis) {
 size_t fagp_predict_x_workspace_size(int64_t Ns, const fagp_basis* basis) {
   if (check_basis(basis) || Ns < 0) return 0;
   if (fused::predict_eligible(basis->p, basis->M)) return 0;
+  if (ptiled::eligible(basis->p, basis->M)) return ptiled::workspace(Ns, basis->p, basis->M);
   return size_t(Ns) * table_width(basis->p, basis->M) * sizeof(double);
 }
 
@@ -1627,6 +1634,9 @@ int fagp_predict_x(const double* Xs, int64_t Ns, const fagp_basis* basis, const 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (fused::predict_eligible(basis->p, basis->M))
     return fused::predict(Xs, Ns, basis, predict_op, sigma2, mean_const, mean, var, flags, s);
+  if (ptiled::eligible(basis->p, basis->M))
+    return ptiled::predict(Xs, Ns, basis, predict_op, sigma2, mean_const, mean, var, workspace, workspace_bytes,
+                           flags, s);
   const size_t table = size_t(Ns) * table_width(basis->p, basis->M) * sizeof(double);
   if (workspace == nullptr || workspace_bytes < table) return FAGP_EWORKSPACE;
   double* Ts = static_cast<double*>(workspace);

@@ -285,7 +285,9 @@ def test_gram_x_matches_table_gram(p, M, N):
 
 
 @pytest.mark.parametrize("p,M,Ns", [(2, 10, 1), (2, 10, 65), (3, 10, 1), (3, 10, 127), (3, 10, 100_001),
-                                    (3, 6, 999), (4, 4, 3001)])
+                                    (3, 6, 999), (4, 4, 3001),
+                                    # output-tiled fused predict (predict_tiled.cu): C4 / C5 shapes, ragged N*
+                                    (4, 8, 1), (4, 8, 3001), (4, 8, 70_001), (5, 6, 7), (5, 6, 2001), (6, 3, 999)])
 def test_predict_x_matches_table_predict(p, M, Ns):
     from paper_2403_12797_b200.posterior import predict_x_device
 
