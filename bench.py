@@ -55,34 +55,50 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-def launches_per_step(m, pair, p=1, fused=False, inverse=False):
-    """Kernels of ours launched by one timed step (no jitter retry), as the ncu launch list of
-    the same step shows (profiles/ncu_summary_*.json)."""
-    if pair and fused and inverse:
-        # fagp_gram_x: fused Gram + partial sum; fagp_predict_x: one fused kernel;
-        # fagp_factor_inv_async at p = 3: expand3 (K -> H), pair_system (+ the t copy), fused
-        # Cholesky inverse, w GEMV, ctc3 + ctc3_op (-> C'', + the w copy); other p: p mode
-        # products, pair_system, inverse, GEMV, ctilde, p mode products, scatter, w copy
-        if p == 3:
-            return 2 + (1 + 1 + 1 + 1 + 2) + 1
-        return 2 + (p + 1 + 1 + 1 + 1 + p + 1 + 1) + 1
-    nblk = -(-m // 32)
-    potrf = nblk + (nblk - 1)  # fused diag+panel kernel per step, trailing GEMM between steps
-    mp = 32
+def routes_of(basis, N, Ns):
+    """(gram, predict, factor) routes the library takes for this shape (fagp_route_info)."""
+    import ctypes
+
+    from paper_2403_12797_b200 import _lib
+
+    out = (ctypes.c_int32 * 3)()
+    _lib.check(_lib.lib().fagp_route_info(N, Ns, basis.ref, ctypes.cast(out, ctypes.c_void_p)), "route_info")
+    return tuple(int(v) for v in out)
+
+
+def _trtri_launches(m):
+    mp, lv = 32, 0
     while mp < m:
         mp *= 2
-    levels = 0
     h = 32
     while h < mp:
-        levels += 1
-        h *= 2
-    trtri = 1 + 1 + 2 * levels  # pad, diag_inv, 2 GEMMs per level
+        lv, h = lv + 1, h * 2
+    return 2 + 2 * lv  # pad, diag_inv, 2 GEMMs per doubling level
+
+
+def _lauum_launches(n):
+    """factor.cu lauum_lower_rec: one GEMM per leaf (n <= 512), two per split."""
+    if n <= 512:
+        return 1
+    h = -(-(n // 2) // 64) * 64
+    return 2 + _lauum_launches(h) + _lauum_launches(n - h)
+
+
+def launches_per_step(m, p, routes):
+    """Kernels of ours launched by one timed step (no jitter retry), by route -- as the ncu launch
+    lists of the same step show (profiles/launches_*.csv, profiles/ncu_summary_*.json)."""
+    gram_r, pred_r, fac_r = routes
+    pair = 2 <= p <= 8
     if pair:
-        factor = p + 1 + 1 + 1 + 1 + trtri + 2 + 1 + 1 + p + 1 + 1
-        if fused:
-            return 2 + factor + 1
-        return 2 + 2 + factor + 2  # basis_eval x2, modal GEMM + reduce, factor, var + mean
-    factor = 1 + 1 + potrf + 1 + trtri + 2 + 1  # build G/t, build A, potrf, zero upper, trtri, GEMVs, operand
+        gram = 2 if gram_r else 4  # fused / tiled kernel + reduce; table: basis_eval + modal GEMM + reduce (+1)
+        pred = 1 if pred_r == 1 else 2 if pred_r == 2 else 3  # tiled: kernel + reduce; table: basis_eval + var + mean
+        if fac_r == 1:  # fagp_factor_inv(_async)
+            fac = 6 if p == 3 else p + 1 + 1 + 1 + 1 + p + 1 + 1
+        else:  # fagp_factor: expand, system (+ t copy), potrf, zero_upper, trtri, w GEMVs, lauum + mirror, C'' fold
+            fac = p + 2 + 1 + 1 + _trtri_launches(m) + 2 + _lauum_launches(m) + 1 + 1 + p + 1 + 1
+        return gram + fac + pred
+    nblk = -(-m // 32)
+    factor = 1 + 1 + 1 + 1 + _trtri_launches(m) + 2 + 1  # build G/t, build A, potrf, zero upper, trtri, GEMVs, operand
     return 2 + 2 + factor + 1  # basis_eval x2, gram + reduce, factor, predict
 
 
@@ -341,6 +357,7 @@ def main():
     Xs = torch.from_numpy(Xsh).cuda()
     kernel = ArdKernelParams.isotropic(p, 1.0, 1.0)
     eng = PosteriorEngine(kernel, M, X.shape[0], Xs.shape[0], NOISE_VAR, 0.0, device=X.device, group=group)
+    routes = routes_of(eng.basis, X.shape[0], Xs.shape[0])
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=X.device)
 
     def barrier():
@@ -403,11 +420,13 @@ def main():
     if g_ms >= p_ms:
         dom, dflops, dms = "fagp_gram_x (eigenfunctions on chip + modal DMMA Gram + t, partial sum)" if pair else \
             "fagp_gram (fused SYRK + reduce)", gram_flops, g_ms
-        traffic = ncu_traffic("fused_gram_split_kernel" if pair and p == 3 and M == 10 else "fused_gram_kernel" if pair else "gram_kernel_fast")
+        traffic = ncu_traffic({1: "fused_gram_split_kernel" if p == 3 and M == 10 else "fused_gram_kernel",
+                               2: "tiled_gram_kernel"}.get(routes[0], "modal_gram_kernel") if pair else "gram_kernel_fast")
     else:
         dom, dflops, dms = "fagp_predict_x (eigenfunctions on chip + modal DMMA variance + mean)" if pair else \
             "fagp_predict (fused triangular GEMM)", pred_flops, p_ms
-        traffic = ncu_traffic(("fused_predict_split_kernel" if p == 3 and 9 <= M <= 12 else "fused_predict_kernel") if pair else "predict_kernel_fast")
+        traffic = ncu_traffic({1: "fused_predict_split_kernel" if p == 3 and 9 <= M <= 12 else "fused_predict_kernel",
+                               2: "tiled_predict_kernel"}.get(routes[1], "modal_var_kernel") if pair else "predict_kernel_fast")
     achieved = dflops / (dms / 1e3) / 1e12
     roofline = {"bound": "tensor", "kernel": dom, "achieved": round(achieved, 3), "peak": peak, "unit": "TFLOP/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
@@ -462,8 +481,9 @@ def main():
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator)",
                "config": config_dict(args, world), "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
-               "clocks": clk.summary(), "gpu_launches": launches_per_step(m, 2 <= p <= 8, p, fused=eng.pred_ws_bytes == 0,
-                                                inverse=eng.inverse_route) * args.steps,
+               "clocks": clk.summary(), "gpu_launches": launches_per_step(m, p, routes) * args.steps,
+               "routes": {"gram": ["table", "fused", "tiled"][routes[0]], "predict": ["table", "fused", "tiled"][routes[1]],
+                          "factor": ["potrf+trtri+lauum", "persistent inverse"][routes[2]]},
                "phases_ms": {"gram": round(g_ms, 3),
                              "allreduce+factor": round(statistics.mean(factor_ms), 3), "predict": round(p_ms, 3)},
                "jitter": eng.jitter.value, "lib": str(_lib.LIB_PATH.name)}

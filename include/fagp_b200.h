@@ -286,6 +286,12 @@ int fagp_predict(const double* Ts, int64_t Ns, const fagp_basis* basis, const do
  * shapes): a host pipeline that predicts in chunks cuts them at multiples of this, so only the
  * last chunk has a partial wave. */
 int64_t fagp_predict_x_wave_rows(const fagp_basis* basis);
+/* Which kernels the point-input entries run for this shape (no compute, no device needed):
+ * out[0] = fagp_gram_x route, out[1] = fagp_predict_x route (0: basis table + tiled table kernels,
+ * 1: one-CTA fused kernel, 2: output-tiled fused kernel), out[2] = factor route (0: fagp_factor,
+ * blocked potrf + trtri + lauum; 1: fagp_factor_inv, the persistent Cholesky inverse).
+ * Diagnostics / bench accounting; replaces nothing in the reference. */
+int fagp_route_info(int64_t N, int64_t Ns, const fagp_basis* basis, int32_t* out);
 size_t fagp_predict_x_workspace_size(int64_t Ns, const fagp_basis* basis);
 int fagp_predict_x(const double* Xs, int64_t Ns, const fagp_basis* basis, const double* predict_op,
                    double sigma2, double mean_const, double* mean, double* var, uint32_t* flags,

@@ -79,6 +79,7 @@ SIGNATURES = {
     "fagp_gram_x_pipelined": (ctypes.c_int, [_P, _I64, _BASIS, _P, _D, _P, _P, _P, _SZ, _P, _P]),
     "fagp_gram_x_signal": (ctypes.c_int, [_P, _I32, _P]),
     "fagp_predict_x_wave_rows": (_I64, [_BASIS]),
+    "fagp_route_info": (ctypes.c_int, [_I64, _I64, _BASIS, _P]),
     "fagp_predict_x_workspace_size": (_SZ, [_I64, _BASIS]),
     "fagp_predict_x": (ctypes.c_int, [_P, _I64, _BASIS, _P, _D, _D, _P, _P, _P, _P, _SZ, _P]),
     "fagp_factor_workspace_size": (_SZ, [_I64]),

@@ -1612,6 +1612,16 @@ int fagp_gram_x_signal(uint32_t* ready, int32_t k, void* stream) {
   return FAGP_OK;
 }
 
+int fagp_route_info(int64_t N, int64_t Ns, const fagp_basis* basis, int32_t* out) {
+  int st = check_basis(basis);
+  if (st) return st;
+  if (out == nullptr || N < 0 || Ns < 0) return FAGP_EINVAL;
+  out[0] = fused::gram_eligible(N, basis->p, basis->M) ? 1 : tiled::eligible(N, basis->p, basis->M) ? 2 : 0;
+  out[1] = fused::predict_eligible(basis->p, basis->M) ? 1 : ptiled::eligible(basis->p, basis->M) ? 2 : 0;
+  out[2] = (modal_on(basis->p, basis->M) && basis->m <= 2048) ? 1 : 0;  // factor.cu kFactorInvMaxM
+  return FAGP_OK;
+}
+
 int64_t fagp_predict_x_wave_rows(const fagp_basis* basis) {
   if (check_basis(basis) || !fused::predict_eligible(basis->p, basis->M)) return 0;
   return int64_t(num_sms()) * fused::kPR;
