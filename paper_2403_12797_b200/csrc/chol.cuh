@@ -11,7 +11,10 @@ __host__ __device__ inline int64_t chol_scratch_len(int64_t m) { return m + 32 *
 
 // Lower Cholesky in place (upper triangle zeroed), LAPACK 1-based *info on breakdown.
 // FAGP_EUNSUPPORTED when the device cannot co-schedule the grid (the caller falls back).
-int potrf_persistent(double* A, int64_t m, int64_t lda, int* info, double* scratch, cudaStream_t s);
+// info_off is added to the reported breakdown column (a diagonal block of a larger matrix); the
+// launch returns at once when *info is already set.
+int potrf_persistent(double* A, int64_t m, int64_t lda, int* info, double* scratch, cudaStream_t s,
+                     int info_off = 0);
 
 // scratch doubles: L_kk^{-1} x 2 | panels (T blocks) | flag
 // [2 L^{-1} blocks | T panels | flag + 2 barrier counters (2 doubles, zeroed per launch) |

@@ -471,14 +471,14 @@ inline int64_t trtri_dim(int64_t m) {
   return d;
 }
 
-__global__ void pad_lower_kernel(const double* L, int64_t m, int64_t mp, double* Lp) {
+__global__ void pad_lower_kernel(const double* L, int64_t m, int64_t ldl, int64_t mp, double* Lp) {
   const int64_t total = mp * mp;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * blockDim.x) {
     const int64_t i = e / mp, j = e - (e / mp) * mp;
     double v;
     if (i < m && j < m)
-      v = j <= i ? L[i * m + j] : 0.0;
+      v = j <= i ? L[i * ldl + j] : 0.0;
     else
       v = (i == j) ? 1.0 : 0.0;
     Lp[e] = v;
@@ -498,10 +498,10 @@ __global__ void diag_inv_kernel(const double* Lp, int64_t mp, double* X) {
 }
 
 // X = inv(Lp) (mp x mp, lower).  ws needs mp*mp (Lp) + mp*mp (X) + mp*mp/4 (Tmp) doubles.
-int trtri_padded(const double* L, int64_t m, double* Lp, double* X, double* Tmp, cudaStream_t s) {
+int trtri_padded(const double* L, int64_t m, double* Lp, double* X, double* Tmp, cudaStream_t s, int64_t ldl = 0) {
   const int64_t mp = trtri_dim(m);
   const int grid = int(tmin<int64_t>(ceil_div(mp * mp, 256), 8 * num_sms()));
-  pad_lower_kernel<<<grid, 256, 0, s>>>(L, m, mp, Lp);
+  pad_lower_kernel<<<grid, 256, 0, s>>>(L, m, ldl ? ldl : m, mp, Lp);
   FAGP_LAUNCH_CHECK();
   FAGP_CUDA_TRY(cudaMemsetAsync(X, 0, size_t(mp) * mp * sizeof(double), s));
   diag_inv_kernel<<<unsigned(mp / 32), 32, 0, s>>>(Lp, mp, X);
@@ -517,6 +517,43 @@ int trtri_padded(const double* L, int64_t m, double* Lp, double* X, double* Tmp,
     GemmArgs g2{int(h), int(h), int(h), -1.0, 0.0, X + h * (mp + 1), mp, dstride, Tmp, h, h * h, X + h * mp, mp, dstride, 0, nullptr};
     st = gemm(false, g2, count, s);
     if (st) return st;
+  }
+  return FAGP_OK;
+}
+
+// Large systems (C4: m 4096, C5: 7776): right-looking Cholesky over kBigNB-column panels whose
+// diagonal blocks run the persistent kernel (same pivot test, the breakdown column offset to the
+// global one) and whose panel solve and trailing update are GEMMs on the FP64 tensor cores:
+//   L_kk = chol(A_kk);  P = A_ik L_kk^{-T} (TRTRI of the block + GEMM);  A_ij -= P_i P_j^T
+//   (lower-triangle tiles only);  A_ik = P
+// The persistent kernel alone walks 32-column steps (latency-bound at m in the thousands: 32 ms
+// at m = 7776); here it only ever sees kBigNB columns.  work: Lp / X / Tmp of trtri_dim(kBigNB)
+// and a panel buffer of m x kBigNB doubles.  The upper triangle is left as is (callers zero it).
+constexpr int64_t kBigNB = 512;
+constexpr int64_t kBigMinM = 3000;
+__global__ void zero_upper_kernel(double* A, int64_t m);
+
+int potrf_big(double* A, int64_t m, int64_t lda, int* info, double* scratch, double* Lp, double* X, double* Tmp,
+              double* P, cudaStream_t s) {
+  const int64_t bp = trtri_dim(kBigNB);
+  for (int64_t k0 = 0; k0 < m; k0 += kBigNB) {
+    const int64_t b = tmin<int64_t>(kBigNB, m - k0);
+    double* Akk = A + k0 * lda + k0;
+    int rc = potrf_persistent(Akk, b, lda, info, scratch, s, int(k0));
+    if (rc) return rc;
+    const int64_t rest = m - k0 - b;
+    if (rest <= 0) break;
+    rc = trtri_padded(Akk, b, Lp, X, Tmp, s, lda);  // X = L_kk^{-1}, row stride bp
+    if (rc) return rc;
+    double* A21 = A + (k0 + b) * lda + k0;
+    GemmArgs pan{int(rest), int(b), int(b), 1.0, 0.0, A21, lda, 0, X, bp, 0, P, b, 0, 0, info};
+    rc = gemm(true, pan, 1, s);  // P = A21 L_kk^{-T}
+    if (rc) return rc;
+    GemmArgs upd{int(rest), int(rest), int(b), -1.0, 1.0, P, b, 0, P, b, 0, A21 + b, lda, 0, 1, info};
+    rc = gemm(true, upd, 1, s);  // A22 -= P P^T (lower tiles)
+    if (rc) return rc;
+    FAGP_CUDA_TRY(cudaMemcpy2DAsync(A21, size_t(lda) * sizeof(double), P, size_t(b) * sizeof(double),
+                                    size_t(b) * sizeof(double), size_t(rest), cudaMemcpyDeviceToDevice, s));
   }
   return FAGP_OK;
 }
@@ -655,8 +692,15 @@ inline FactorWs carve(void* base, int64_t m) {
   return w;
 }
 
+// [info | Dinv | chol scratch | blocked-route scratch: Lp, X, Tmp of trtri_dim(kBigNB), panel m x kBigNB]
+inline size_t potrf_big_bytes(int64_t m) {
+  const size_t bp = size_t(trtri_dim(kBigNB));
+  return 2 * align256(bp * bp * sizeof(double)) + align256(bp * bp / 4 * sizeof(double) + 8) +
+         align256(size_t(m) * kBigNB * sizeof(double));
+}
 inline size_t potrf_ws_bytes(int64_t m) {
-  return align256(sizeof(int)) + align256(32 * 32 * sizeof(double)) + align256(size_t(chol_scratch_len(m)) * sizeof(double));
+  return align256(sizeof(int)) + align256(32 * 32 * sizeof(double)) + align256(size_t(chol_scratch_len(m)) * sizeof(double)) +
+         potrf_big_bytes(m);
 }
 
 // D = X^T X for the lower-triangular n x n X (D full symmetric; LAPACK dlauum's product), by
@@ -754,8 +798,22 @@ int fagp_potrf(double* A, int64_t m, int32_t* info_dev, void* workspace, size_t 
   if (workspace == nullptr || workspace_bytes < potrf_ws_bytes(m)) return FAGP_EWORKSPACE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   FAGP_CUDA_TRY(cudaMemsetAsync(info_dev, 0, sizeof(int32_t), s));
-  double* diag = reinterpret_cast<double*>(static_cast<char*>(workspace) + align256(sizeof(int)) +
-                                           align256(32 * 32 * sizeof(double)));
+  char* w = static_cast<char*>(workspace) + align256(sizeof(int)) + align256(32 * 32 * sizeof(double));
+  double* diag = reinterpret_cast<double*>(w);
+  const char* e = getenv("FAGP_POTRF");  // "big": the blocked large-m route at any m (tests)
+  if (m >= kBigMinM || (e && strcmp(e, "big") == 0)) {
+    const size_t bp = size_t(trtri_dim(kBigNB));
+    char* q = w + align256(size_t(chol_scratch_len(m)) * sizeof(double));
+    double* Lp = reinterpret_cast<double*>(q);
+    double* X = reinterpret_cast<double*>(q + align256(bp * bp * sizeof(double)));
+    double* Tmp = reinterpret_cast<double*>(q + 2 * align256(bp * bp * sizeof(double)));
+    double* P = reinterpret_cast<double*>(q + 2 * align256(bp * bp * sizeof(double)) + align256(bp * bp / 4 * sizeof(double) + 8));
+    int rc = potrf_big(A, m, m, reinterpret_cast<int*>(info_dev), diag, Lp, X, Tmp, P, s);
+    if (rc) return rc;
+    zero_upper_kernel<<<int(tmin<int64_t>(ceil_div(m * m, 256), 8 * num_sms())), 256, 0, s>>>(A, m);
+    FAGP_LAUNCH_CHECK();
+    return FAGP_OK;
+  }
   return potrf(A, m, m, reinterpret_cast<int*>(info_dev), diag, s);
 }
 
@@ -881,7 +939,10 @@ int fagp_factor(const double* packed, const fagp_basis* basis, const double* sqr
       if (rc1) return rc1;
     }
     FAGP_CUDA_TRY(cudaMemsetAsync(ws.info, 0, sizeof(int), s));
-    int rc = potrf(L, m, m, ws.info, ws.chol, s);
+    // (the block TRTRI buffers and D double as the blocked factorisation's scratch: both are
+    // only needed after it)
+    int rc = m >= kBigMinM ? potrf_big(L, m, m, ws.info, ws.chol, ws.Lp, ws.X, ws.Tmp, ws.D, s)
+                           : potrf(L, m, m, ws.info, ws.chol, s);
     if (rc) return rc;
     FAGP_CUDA_TRY(cudaMemcpyAsync(&info_h, ws.info, sizeof(int), cudaMemcpyDeviceToHost, s));
     FAGP_CUDA_TRY(cudaStreamSynchronize(s));

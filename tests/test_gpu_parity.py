@@ -230,17 +230,19 @@ def test_c3_full_size_properties():
     assert rel_err(a.var[idx], ref["var"]) <= MEAN_VAR_RTOL
 
 
-@pytest.mark.parametrize("impl", ["persistent", "blocked"])
-@pytest.mark.parametrize("m", [1, 5, 31, 32, 33, 64, 100, 257, 1000])
+@pytest.mark.parametrize("impl", ["persistent", "blocked", "big"])
+@pytest.mark.parametrize("m", [1, 5, 31, 32, 33, 64, 100, 257, 1000, 1100])
 def test_potrf_matches_lapack(m, impl, monkeypatch):
-    """fagp_potrf (persistent cooperative kernel, and the blocked fallback) against LAPACK
-    dpotrf on SPD matrices, and LAPACK's 1-based info on an indefinite one."""
+    """fagp_potrf (persistent cooperative kernel, the blocked fallback, and the large-m route of
+    512-column panels used from m = 3000 on -- forced here at small m) against LAPACK dpotrf on SPD
+    matrices, and LAPACK's 1-based info on an indefinite one (breakdown inside a later panel for
+    the large-m route at m = 1000, 1100)."""
     import scipy.linalg as sla
 
     from paper_2403_12797_b200.linalg import potrf
 
-    if impl == "blocked":
-        monkeypatch.setenv("FAGP_POTRF", "blocked")
+    if impl != "persistent":
+        monkeypatch.setenv("FAGP_POTRF", impl)
     rng = np.random.default_rng(m)
     B = rng.standard_normal((m, m))
     A = B @ B.T + m * np.eye(m)
