@@ -5,7 +5,7 @@
 set -e
 mkdir -p /tmp/gprof
 cd paper_2403_12797_b200
-for f in basis gram factor predict literal modal chol fused; do
+for f in basis gram factor predict literal modal chol fused exact gram_tiled predict_tiled; do
   extra=""; [ $f = fused ] && extra="-DFAGP_GRAM_PROFILE"
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC $extra -I ../include -c csrc/$f.cu -o /tmp/gprof/$f.o &
 done
