@@ -48,7 +48,7 @@ CONFIGS = {
 METRIC = "posterior mean+var samples/s (N=1e6, p=3, M=10); % FP64 tensor peak"
 NOISE_VAR = 0.0025
 FP64_PEAK_FILE = ROOT / "profiles" / "fp64_peak_r01.json"
-NCU_SUMMARY_FILE = ROOT / "profiles" / "ncu_summary_r02f.json"
+NCU_SUMMARY_FILES = (ROOT / "profiles" / "ncu_summary_r04s.json", ROOT / "profiles" / "ncu_summary_r04s_c4tiled.json")
 
 
 def log(*a):
@@ -181,13 +181,14 @@ def fp64_peak():
 def ncu_traffic(kernel):
     """DRAM bytes per launch (read + write) of the kernel whose name starts with `kernel`,
     from the committed ncu --set full summary (None when it was not captured)."""
-    try:
-        d = json.loads(NCU_SUMMARY_FILE.read_text())
-        for name, ent in d["kernels"].items():
-            if name.split("<")[0].split("::")[-1] == kernel:
-                return ent.get("dram_bytes_per_launch")
-    except (OSError, KeyError, ValueError):
-        pass
+    for f in NCU_SUMMARY_FILES:
+        try:
+            d = json.loads(f.read_text())
+            for name, ent in d["kernels"].items():
+                if name.split("<")[0].split("::")[-1] == kernel:
+                    return ent.get("dram_bytes_per_launch")
+        except (OSError, KeyError, ValueError):
+            pass
     return None
 
 

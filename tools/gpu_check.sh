@@ -17,7 +17,7 @@ for s in $STAGES; do
     bench) timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench rc=$?" >> gpurun_out/${TAG}_bench.err ;;
     benchref) timeout 900 python bench.py --impl reference > gpurun_out/${TAG}_bench_ref.json 2> gpurun_out/${TAG}_bench_ref.err ;;
     ncu) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/${TAG}_ncu_launch.out 2>&1 ;;
-    full) timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"fused_gram|fused_predict|cholinv_persistent" -c 3 -o gpurun_out/${TAG}_prof python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/${TAG}_ncu_full.out 2>&1 ;;
+    full) timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"fused_gram|fused_predict|cholinv_persistent|tiled_gram|tiled_predict" -c 3 -o gpurun_out/${TAG}_prof python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/${TAG}_ncu_full.out 2>&1 ;;
   esac
 done
 tail -3 gpurun_out/${TAG}_pytest_gpu.txt 2>/dev/null; cat gpurun_out/${TAG}_smoke.txt 2>/dev/null; cat gpurun_out/${TAG}_bench.json 2>/dev/null; tail -3 gpurun_out/${TAG}_bench.err 2>/dev/null
