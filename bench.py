@@ -393,6 +393,32 @@ def main():
     barrier()
     if eng.factor_needs_retry():
         raise RuntimeError("the synthetic system needed jitter: the timed steps ran the async factor's attempt 0 only")
+    # the same step replayed as one CUDA graph (async-factor shapes, one rank): the launch-bound
+    # configs (C1 / C2) show the host issue gaps the graph removes
+    graph = None
+    if world == 1:
+        try:
+            g = eng.capture(X, y, Xs)
+        except Exception as exc:  # noqa: BLE001 - reported, never fatal for the bench
+            g = None
+            log("graph capture failed:", repr(exc))
+        if g is not None:
+            gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+            for _ in range(2):
+                eng.replay()
+            torch.cuda.synchronize()
+            for k in range(args.steps):
+                flush.fill_(float(k))
+                gev[k][0].record(stream)
+                eng.replay()
+                gev[k][1].record(stream)
+            torch.cuda.synchronize()
+            if eng.factor_needs_retry():
+                raise RuntimeError("the synthetic system needed jitter in the graph replay")
+            eng.check(X, Xs, y)
+            gms = statistics.mean(a.elapsed_time(b) for a, b in gev)
+            graph = {"ms_per_step": round(gms, 4), "value": round(Ns / (gms / 1e3), 1),
+                     "what": "the same step (flags, Gram, async factor, predict) replayed as one CUDA graph"}
     step_ms = [e[0].elapsed_time(e[4]) for e in ev]
     gram_ms = [e[1].elapsed_time(e[2]) for e in ev]
     factor_ms = [e[2].elapsed_time(e[3]) for e in ev]
@@ -472,6 +498,31 @@ def main():
                "h2d_bytes_per_step": int((Xh.size + yh.size + Xsh.size) * 8),
                "d2h_bytes_per_step": int(2 * Xsh.shape[0] * 8),
                "path": "fagp_posterior(pinned host tensors) -> host numpy mean, var"}
+        # the drop-in case: plain numpy arrays in (the engine stages them through its pinned buffers)
+        class TrainNp:
+            X = Xh
+            y = yh
+
+        for _ in range(2):
+            fagp_posterior(TrainNp, Xsh, model, memory_cap=None, group=group)
+        tn = []
+        gc.disable()
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = fagp_posterior(TrainNp, Xsh, model, memory_cap=None, group=group)
+            torch.cuda.synchronize()
+            tn.append(time.perf_counter() - t0)
+        gc.enable()
+        tnm = statistics.mean(tn)
+        if world > 1:
+            tt = torch.tensor([tnm], dtype=torch.float64, device=X.device)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            tnm = float(tt.item())
+        e2e["numpy_input"] = {"value": Ns / tnm, "ms_per_step": tnm * 1e3,
+                              "path": "fagp_posterior(numpy arrays) -> host numpy mean, var (host copy into pinned staging inside the timed call)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -487,7 +538,7 @@ def main():
                           "factor": ["potrf+trtri+lauum", "persistent inverse"][routes[2]]},
                "phases_ms": {"gram": round(g_ms, 3),
                              "allreduce+factor": round(statistics.mean(factor_ms), 3), "predict": round(p_ms, 3)},
-               "jitter": eng.jitter.value, "lib": str(_lib.LIB_PATH.name)}
+               "jitter": eng.jitter.value, "lib": str(_lib.LIB_PATH.name), "graph": graph}
         print(json.dumps(out), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

@@ -292,6 +292,19 @@ int64_t fagp_predict_x_wave_rows(const fagp_basis* basis);
  * blocked potrf + trtri + lauum; 1: fagp_factor_inv, the persistent Cholesky inverse).
  * Diagnostics / bench accounting; replaces nothing in the reference. */
 int fagp_route_info(int64_t N, int64_t Ns, const fagp_basis* basis, int32_t* out);
+/* HOST memcpy (dst pinned staging buffer, src the caller's pageable array) over `threads` threads
+ * with non-temporal stores, so the H2D DMA that follows reads DRAM rather than dirty CPU cache
+ * lines.  The staging step of fagp_posterior's host path for numpy inputs (posterior.py:267-318
+ * takes numpy arrays); no device work. */
+int fagp_host_copy(void* dst, const void* src, size_t bytes, int32_t threads);
+int fagp_host_copy_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+                      int32_t threads);
+/* Host staging of exactly the rows fagp_gram_x_upload_chunk(k) will copy: from the caller's
+ * pageable X_src / y_src (N x p, N) into pinned X_pinned / y_pinned laid out like X / y, with
+ * fagp_host_copy's threads and streaming stores -- so chunk k can be staged while chunk k-1 is
+ * in flight (the numpy-input host path of posterior.py:267-318). */
+int fagp_gram_x_stage_chunk(const double* X_src, const double* y_src, int64_t N, const fagp_basis* basis, int32_t k,
+                            double* X_pinned, double* y_pinned, int32_t threads);
 size_t fagp_predict_x_workspace_size(int64_t Ns, const fagp_basis* basis);
 int fagp_predict_x(const double* Xs, int64_t Ns, const fagp_basis* basis, const double* predict_op,
                    double sigma2, double mean_const, double* mean, double* var, uint32_t* flags,

@@ -16,7 +16,7 @@ from pathlib import Path
 PKG_DIR = Path(__file__).resolve().parent
 CSRC = PKG_DIR / "csrc"
 LIB_PATH = PKG_DIR / "libfagp_b200.so"
-SOURCES = ("basis.cu", "gram.cu", "factor.cu", "predict.cu", "literal.cu", "modal.cu", "chol.cu", "fused.cu", "exact.cu", "gram_tiled.cu", "predict_tiled.cu")
+SOURCES = ("basis.cu", "gram.cu", "factor.cu", "predict.cu", "literal.cu", "modal.cu", "chol.cu", "fused.cu", "exact.cu", "gram_tiled.cu", "predict_tiled.cu", "host.cu")
 ARCH_FLAGS = ("-gencode", "arch=compute_100a,code=sm_100a")
 
 

@@ -927,6 +927,41 @@ int upload_chunk(const double* Xh, const double* yh, int64_t N, int p, int M, in
   return FAGP_OK;
 }
 
+// host staging of the rows chunk k reads (the rows upload_chunk copies, the same geometry) from a
+// caller's pageable arrays into pinned buffers laid out like the device ones
+int stage_chunk(const double* Xsrc, const double* ysrc, int64_t N, int p, int M, int k, double* Xdst, double* ydst,
+                int threads) {
+  GPlan pl;
+  if (!make_gplan(N, p, M, pl)) {
+    if (k != 0) return FAGP_EINVAL;
+    int rc = fagp_host_copy(Xdst, Xsrc, size_t(N) * p * sizeof(double), threads);
+    if (rc == FAGP_OK && ysrc && ydst) rc = fagp_host_copy(ydst, ysrc, size_t(N) * sizeof(double), threads);
+    return rc;
+  }
+  if (k < 0 || k >= pl.S) return FAGP_EINVAL;
+  const int64_t bpc = pl.bpc;
+  const int64_t off = (int64_t(k) * bpc / pl.S) * pl.br;
+  const int64_t sub_rows = tmin<int64_t>((int64_t(k + 1) * bpc / pl.S) * pl.br, pl.rows_per_cta) - off;
+  const int64_t head = N - off - sub_rows;
+  const int64_t full = head < 0 ? 0 : tmin<int64_t>(pl.grid, head / pl.rows_per_cta + 1);
+  int rc = FAGP_OK;
+  if (full > 0) {
+    const size_t pitch = size_t(pl.rows_per_cta) * sizeof(double);
+    rc = fagp_host_copy_2d(Xdst + off * p, pitch * p, Xsrc + off * p, pitch * p, size_t(sub_rows) * p * 8, size_t(full),
+                           threads);
+    if (rc == FAGP_OK && ysrc && ydst)
+      rc = fagp_host_copy_2d(ydst + off, pitch, ysrc + off, pitch, size_t(sub_rows) * 8, size_t(full), threads);
+  }
+  if (rc == FAGP_OK && full < pl.grid) {
+    const int64_t a = full * pl.rows_per_cta + off, e = tmin<int64_t>(N, a + sub_rows);
+    if (e > a) {
+      rc = fagp_host_copy(Xdst + a * p, Xsrc + a * p, size_t(e - a) * p * 8, threads);
+      if (rc == FAGP_OK && ysrc && ydst) rc = fagp_host_copy(ydst + a, ysrc + a, size_t(e - a) * 8, threads);
+    }
+  }
+  return rc;
+}
+
 // chunks [k0, k1) of the plan; the last chunk also sums the partials into `out`
 int gram(const double* X, const double* y, double c, int64_t N, const fagp_basis* b, int k0, int k1, double* out,
          void* ws, size_t ws_bytes, uint32_t* flags, cudaStream_t s, const unsigned* ready) {
@@ -1549,6 +1584,15 @@ int fagp_gram_x_upload_chunk(const double* X_host, const double* y_host, int64_t
   if (st) return st;
   if (N < 0 || (N > 0 && (X_host == nullptr || X == nullptr))) return FAGP_EINVAL;
   return fused::upload_chunk(X_host, y_host, N, basis->p, basis->M, k, X, y, static_cast<cudaStream_t>(stream));
+}
+
+int fagp_gram_x_stage_chunk(const double* X_src, const double* y_src, int64_t N, const fagp_basis* basis, int32_t k,
+                            double* X_pinned, double* y_pinned, int32_t threads) {
+  int st = check_basis(basis);
+  if (st) return st;
+  if (N < 0 || (N > 0 && (X_src == nullptr || X_pinned == nullptr))) return FAGP_EINVAL;
+  if (N == 0) return FAGP_OK;
+  return fused::stage_chunk(X_src, y_src, N, basis->p, basis->M, k, X_pinned, y_pinned, threads);
 }
 
 int fagp_gram_x_chunk(const double* X, int64_t N, const fagp_basis* basis, const double* y, double mean_const,

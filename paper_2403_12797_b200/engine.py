@@ -31,6 +31,20 @@ _GPU_TRACE = None  # diagnostics: a list collects [(mark, ms since entry)] per r
 _TRACE = None  # diagnostics: set to a list to collect run_host phase times in ms (tools/e2e_probe.py)
 
 
+def _parallel_copy(dst, src):
+    """dst[...] = src (C-contiguous float64 arrays of the same size) through fagp_host_copy:
+    threads and non-temporal stores (staging a caller's numpy inputs into pinned memory is
+    memcpy-bound at ~5 GB/s on one core, and a DMA from freshly written, cache-dirty lines runs at
+    about half speed)."""
+    import numpy as np
+
+    s = np.ascontiguousarray(src, dtype=np.float64)
+    if s.size != dst.size:
+        raise ValueError("staging copy: size mismatch")
+    threads = min(8, os.cpu_count() or 1)
+    _lib.check(_lib.lib().fagp_host_copy(dst.ctypes.data, s.ctypes.data, s.nbytes, threads), "host_copy")
+
+
 def _free_refcount():
     """sys.getrefcount of a pool entry's ndarray that nobody else holds, measured on the same
     code path as _out_buffer's check (pool tuple + loop name + call argument): the interpreter's
@@ -207,6 +221,42 @@ class PosteriorEngine:
                 self.stage_predict(Xs)
         return self.mean, self.var
 
+    def capture(self, X, y, Xs):
+        """Record one device step -- flags, Gram, asynchronous factor, predict -- as a CUDA graph
+        over these buffers (replay() re-runs it with whatever X, y, X* then hold): a step of ~10
+        launches becomes one graph launch, no host round trips between the kernels.  Only for the
+        shapes with the asynchronous factor route and no process group (the jitter decision and
+        the all-reduce stay on the host path); returns None otherwise.  After a replay the caller
+        synchronises and checks factor_needs_retry() (the breakdown status is copied out by the
+        graph itself)."""
+        import torch
+
+        if not self.inverse_route or self.group is not None:
+            return None
+
+        def step():
+            self.flags.zero_()
+            self.stage_gram(X, y)
+            self.stage_factor_async()
+            self.stage_predict(Xs)
+
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):  # warm-up outside the capture (lazy module loading, workspaces)
+            step()
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            step()
+        self._graph = g
+        return g
+
+    def replay(self):
+        """Launch the captured step (capture() first); returns the device (mean, var)."""
+        self._graph.replay()
+        return self.mean, (self.var if self.want_var else None)
+
     def _retry_factor(self, X, Xs, y, fault_flip):
         """The async attempt broke down: run the full jitter schedule (blocking) and re-apply the
         fault hook; raises the reference's NumericalError if even the last attempt fails."""
@@ -233,6 +283,28 @@ class PosteriorEngine:
             self._stage = {}
         return self.X, self.y, self.Xs
 
+    def _staging_source(self, a, shape):
+        """The C-contiguous float64 host array behind `a` when it must be staged (not a pinned
+        tensor already), else None."""
+        import numpy as np
+        import torch
+
+        if isinstance(a, torch.Tensor):
+            if a.is_pinned() and a.dtype == torch.float64 and a.is_contiguous():
+                return None
+            a = a.detach().cpu().numpy()
+        src = np.ascontiguousarray(np.asarray(a, dtype=np.float64)).reshape(shape)
+        return src
+
+    def _stage_buf(self, key, shape):
+        import torch
+
+        buf = self._stage.get(key)
+        if buf is None or tuple(buf.shape) != tuple(shape):
+            buf = torch.empty(shape, dtype=torch.float64, pin_memory=True)
+            self._stage[key] = buf
+        return buf
+
     def _pinned(self, a, key, shape):
         """Host source for an async H2D copy: a pinned CPU tensor as is, anything else staged
         into an engine-owned pinned buffer (one host memcpy)."""
@@ -246,7 +318,7 @@ class PosteriorEngine:
             buf = torch.empty(shape, dtype=torch.float64, pin_memory=True)
             self._stage[key] = buf
         src = a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a, dtype=np.float64)
-        np.copyto(buf.numpy(), src.reshape(shape), casting="same_kind")
+        _parallel_copy(buf.numpy(), src.reshape(shape))
         return buf
 
     def run_host(self, Xh, yh, Xsh, fault_flip=False):
@@ -277,9 +349,23 @@ class PosteriorEngine:
         self._host_flags = None
         X, y, Xs = self._host_buffers()
         p = b.p
-        Xh = self._pinned(Xh, "X", (self.N, p))
-        yh = self._pinned(yh, "y", (self.N,))
-        Xsh = self._pinned(Xsh, "Xs", (self.Ns, p))
+        # pageable (numpy) train inputs are staged chunk by chunk right before each chunk's upload
+        # (fagp_gram_x_stage_chunk), so staging chunk k overlaps the DMA of chunk k - 1 and the
+        # Gram on the chunks already landed; pinned tensors go up as they are
+        x_src, y_src = self._staging_source(Xh, (self.N, p)), self._staging_source(yh, (self.N,))
+        staged = x_src is not None and y_src is not None
+        if staged:
+            Xh, yh = self._stage_buf("X", (self.N, p)), self._stage_buf("y", (self.N,))
+        else:
+            Xh = self._pinned(Xh, "X", (self.N, p))
+            yh = self._pinned(yh, "y", (self.N,))
+        Xsh_src = Xsh  # staged (when not pinned already) once the Gram is queued: overlaps it
+        threads = min(8, os.cpu_count() or 1)
+
+        def stage(k):
+            if staged:
+                _lib.check(L.fagp_gram_x_stage_chunk(x_src.ctypes.data, y_src.ctypes.data, self.N, b.ref, k,
+                                                     _lib.ptr(Xh), _lib.ptr(yh), threads), "stage")
         self.flags.zero_()
         nch = int(L.fagp_gram_x_chunks(self.N, b.ref))
         ready = self._ready_words(nch)
@@ -294,17 +380,27 @@ class PosteriorEngine:
             # the copy stream uploads chunk k and then sets ready word k (a stream-ordered 4-byte
             # H2D copy); ONE Gram launch waits on the words chunk by chunk.  The copies are
             # queued first, so nothing the host does after the launch can hold them back.
-            for k in range(nch):
+            # (staged inputs: chunk 0 goes up first, then the Gram is launched, then chunks 1.. are
+            # staged and uploaded while it contracts -- the launch waits on the ready words)
+            def upload(k):
+                stage(k)
                 _lib.check(L.fagp_gram_x_upload_chunk(_lib.ptr(Xh), _lib.ptr(yh), self.N, b.ref, k, _lib.ptr(X),
                                                       _lib.ptr(y), sin), "upload")
                 _lib.check(L.fagp_gram_x_signal(_lib.ptr(ready), k, sin), "signal")
                 mark(f"up{k}", self.s_in)
+
+            first = 1 if staged else nch
+            for k in range(first):
+                upload(k)
             _lib.check(L.fagp_gram_x_pipelined(_lib.ptr(X), self.N, b.ref, _lib.ptr(y), self.mean_const,
                                                _lib.ptr(ready), _lib.ptr(self.packed), _lib.ptr(self.gram_ws),
                                                self.gram_ws_bytes, self._flag(0), _lib.stream_handle(cs)), "gram")
             mark("gram", cs)
+            for k in range(first, nch):
+                upload(k)
         else:  # table-path shapes: chunk launches behind events
             for k in range(nch):
+                stage(k)
                 _lib.check(L.fagp_gram_x_upload_chunk(_lib.ptr(Xh), _lib.ptr(yh), self.N, b.ref, k, _lib.ptr(X),
                                                       _lib.ptr(y), sin), "upload")
                 ev = torch.cuda.Event()
@@ -315,17 +411,34 @@ class PosteriorEngine:
                                                _lib.ptr(self.packed), _lib.ptr(self.gram_ws), self.gram_ws_bytes,
                                                self._flag(0), _lib.stream_handle(cs)), "gram")
                 mark(f"gram{k}", cs)
-        with torch.cuda.stream(self.s_in):
-            if self.Ns:
-                Xs.copy_(Xsh, non_blocking=True)
-            ev_xs = torch.cuda.Event()
-            ev_xs.record(self.s_in)
-        mark("xs_up", self.s_in)
+        xs_src = self._staging_source(Xsh_src, (self.Ns, p))
+
+        def upload_xs():
+            xs_host = self._pinned(Xsh_src, "Xs", (self.Ns, p))
+            with torch.cuda.stream(self.s_in):
+                if self.Ns:
+                    Xs.copy_(xs_host, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.s_in)
+            mark("xs_up", self.s_in)
+            return ev
+
+        # a pinned X* goes up right behind the train rows; a pageable one is staged on the host
+        # after the factorisation is queued (the staging then overlaps the Gram tail and factor)
+        ev_xs = upload_xs() if xs_src is None else None
         if trace is not None:
             trace.append(time.perf_counter())
         self.stage_reduce()
         asynchronous = self.stage_factor_async()
         mark("factor", cs)
+        if ev_xs is None:
+            # pageable X*: staged and uploaded per predict chunk (below), chunk k + 1's host copy
+            # overlapping chunk k's predict
+            xs_stage = self._stage_buf("Xs", (self.Ns, p))
+            ev_xs = torch.cuda.Event()
+            ev_xs.record(cs)  # (nothing to wait for before the first chunk's own upload)
+        else:
+            xs_stage = None
         if trace is not None:
             trace.append(time.perf_counter())
         cs.wait_event(ev_xs)
@@ -339,6 +452,14 @@ class PosteriorEngine:
         if trace is not None:
             trace.append(time.perf_counter())
         for ci, (a, e) in enumerate(self._predict_chunks()):
+            if xs_stage is not None and e > a:
+                _parallel_copy(xs_stage[a:e].numpy(), xs_src[a:e])
+                with torch.cuda.stream(self.s_in):
+                    Xs[a:e].copy_(xs_stage[a:e], non_blocking=True)
+                    evc = torch.cuda.Event()
+                    evc.record(self.s_in)
+                mark(f"xs{ci}", self.s_in)
+                cs.wait_event(evc)
             _lib.check(L.fagp_predict_x(_lib.ptr(Xs[a:e]), e - a, b.ref, _lib.ptr(self.predict_op), self.noise_var,
                                         self.mean_const, _lib.ptr(self.mean[a:e]),
                                         _lib.ptr(self.var[a:e] if self.want_var else None), self._flag(1),

@@ -53,3 +53,21 @@ def test_host_only_entry_points():
     assert lib.fagp_multi_indices(2, 3, buf) == 0
     assert list(buf)[:6] == [1, 1, 1, 1, 1, 2]
     assert lib.fagp_multi_indices(0, 3, buf) == _lib.FAGP_EINVAL
+
+
+def test_host_copy_streams_bitwise():
+    """fagp_host_copy (threads + non-temporal stores: the host staging of numpy inputs) is a plain
+    memcpy: bitwise, any length, any destination alignment, any thread count."""
+    import numpy as np
+
+    from paper_2403_12797_b200 import _lib
+
+    L = _lib.load()
+    rng = np.random.default_rng(5)
+    for n, off, th in [(0, 0, 4), (1, 0, 1), (1001, 1, 3), (3_000_003, 0, 8), (5_000_001, 1, 16)]:
+        a = rng.standard_normal(n)
+        buf = np.zeros(n + 2)
+        b = buf[off:off + n]
+        assert L.fagp_host_copy(b.ctypes.data if n else None, a.ctypes.data if n else None, a.nbytes, th) == 0
+        assert np.array_equal(a, b)
+        assert buf[off + n:].sum() == 0.0 and (off == 0 or buf[0] == 0.0)

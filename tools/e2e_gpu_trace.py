@@ -15,7 +15,10 @@ from paper_2403_12797_b200.datagen import generate, test_inputs, train_seed  # n
 p, M, N = 3, 10, 1_000_000
 ds = generate(N, p, train_seed(p), 0.05)
 Xs = test_inputs(N, p)
-Xp, yp, Xsp = (torch.from_numpy(a).pin_memory() for a in (ds.X, ds.y, Xs))
+if "--numpy" in sys.argv:  # the drop-in case: plain numpy inputs, staged by the engine
+    Xp, yp, Xsp = ds.X, ds.y, Xs
+else:
+    Xp, yp, Xsp = (torch.from_numpy(a).pin_memory() for a in (ds.X, ds.y, Xs))
 model = F.GpModel(F.ArdKernelParams.isotropic(p, 1.0, 1.0), 0.0025, n_eigen=M)
 
 
