@@ -42,7 +42,14 @@ struct GemmArgs {
   int64_t ldc, sC;
   int lower_only;
   const int* info;  // skip all work when *info != 0 (after a Cholesky breakdown)
+  // triangular operands: the K range of an output tile shrinks (bits; op(A) is M x K, op(B) K x N)
+  //   kTriKminCol: op(B)[k][n] = 0 for k < n (lower)      -> k >= col0
+  //   kTriKmaxRow: op(A)[m][k] = 0 for k > m (lower)      -> k <  row0 + GT
+  //   kTriKminRow: op(A)[m][k] = 0 for k < m (upper)      -> k >= row0
+  //   kTriKmaxCol: op(B)[k][n] = 0 for k > n (upper)      -> k <  col0 + GT
+  int tri;
 };
+constexpr int kTriKminCol = 1, kTriKmaxRow = 2, kTriKminRow = 4, kTriKmaxCol = 8;
 
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(GNT) dgemm_kernel(GemmArgs g) {
@@ -62,7 +69,13 @@ __global__ void __launch_bounds__(GNT) dgemm_kernel(GemmArgs g) {
 #pragma unroll
     for (int t = 0; t < 4; ++t) acc[s][t][0] = acc[s][t][1] = 0.0;
 
-  for (int k0 = 0; k0 < g.K; k0 += GK) {
+  int kb = 0, ke = g.K;
+  if (g.tri & kTriKminCol) kb = tmax(kb, col0);
+  if (g.tri & kTriKminRow) kb = tmax(kb, row0);
+  if (g.tri & kTriKmaxRow) ke = tmin(ke, row0 + GT);
+  if (g.tri & kTriKmaxCol) ke = tmin(ke, col0 + GT);
+  kb = kb / GK * GK;  // (the skipped range is exactly zero in the triangular operand)
+  for (int k0 = kb; k0 < ke; k0 += GK) {
 #pragma unroll
     for (int q = 0; q < (GT * GK) / GNT; ++q) {
       const int e = tid + q * GNT;
@@ -510,11 +523,13 @@ int trtri_padded(const double* L, int64_t m, double* Lp, double* X, double* Tmp,
     const int count = int(mp / (2 * h));
     const int64_t dstride = 2 * h * (mp + 1);
     // Tmp_q = L21_q * X11_q
-    GemmArgs g1{int(h), int(h), int(h), 1.0, 0.0, Lp + h * mp, mp, dstride, X, mp, dstride, Tmp, h, h * h, 0, nullptr};
+    GemmArgs g1{int(h), int(h), int(h), 1.0, 0.0, Lp + h * mp, mp, dstride, X, mp, dstride, Tmp, h, h * h, 0, nullptr,
+                kTriKminCol};  // X11 lower triangular
     int st = gemm(false, g1, count, s);
     if (st) return st;
     // X21_q = -X22_q * Tmp_q
-    GemmArgs g2{int(h), int(h), int(h), -1.0, 0.0, X + h * (mp + 1), mp, dstride, Tmp, h, h * h, X + h * mp, mp, dstride, 0, nullptr};
+    GemmArgs g2{int(h), int(h), int(h), -1.0, 0.0, X + h * (mp + 1), mp, dstride, Tmp, h, h * h, X + h * mp, mp, dstride, 0, nullptr,
+                kTriKmaxRow};  // X22 lower triangular
     st = gemm(false, g2, count, s);
     if (st) return st;
   }
@@ -546,7 +561,8 @@ int potrf_big(double* A, int64_t m, int64_t lda, int* info, double* scratch, dou
     rc = trtri_padded(Akk, b, Lp, X, Tmp, s, lda);  // X = L_kk^{-1}, row stride bp
     if (rc) return rc;
     double* A21 = A + (k0 + b) * lda + k0;
-    GemmArgs pan{int(rest), int(b), int(b), 1.0, 0.0, A21, lda, 0, X, bp, 0, P, b, 0, 0, info};
+    GemmArgs pan{int(rest), int(b), int(b), 1.0, 0.0, A21, lda, 0, X, bp, 0, P, b, 0, 0, info,
+                 kTriKmaxCol};  // op(B) = L_kk^{-T}, upper triangular
     rc = gemm(true, pan, 1, s);  // P = A21 L_kk^{-T}
     if (rc) return rc;
     GemmArgs upd{int(rest), int(rest), int(b), -1.0, 1.0, P, b, 0, P, b, 0, A21 + b, lda, 0, 1, info};
@@ -719,7 +735,8 @@ __global__ void mirror_lower_kernel(double* D, int64_t n, int64_t ldd) {
 
 static int lauum_lower_rec(const double* X, int64_t ldx, int64_t n, double* D, int64_t ldd, cudaStream_t s) {
   if (n <= 512) {
-    GemmArgs g{int(n), int(n), int(n), 1.0, 0.0, X, ldx, 0, X, ldx, 0, D, ldd, 0, 1, nullptr};
+    GemmArgs g{int(n), int(n), int(n), 1.0, 0.0, X, ldx, 0, X, ldx, 0, D, ldd, 0, 1, nullptr,
+               kTriKminRow | kTriKminCol};  // X^T upper, X lower
     return gemm(false, g, 1, s, true);
   }
   const int64_t h = round_up(n / 2, 64), r = n - h;
@@ -727,7 +744,8 @@ static int lauum_lower_rec(const double* X, int64_t ldx, int64_t n, double* D, i
   const double* X22 = X21 + h;
   int rc = lauum_lower_rec(X22, ldx, r, D + h * ldd + h, ldd, s);
   if (rc) return rc;
-  GemmArgs g21{int(r), int(h), int(r), 1.0, 0.0, X22, ldx, 0, X21, ldx, 0, D + h * ldd, ldd, 0, 0, nullptr};
+  GemmArgs g21{int(r), int(h), int(r), 1.0, 0.0, X22, ldx, 0, X21, ldx, 0, D + h * ldd, ldd, 0, 0, nullptr,
+               kTriKminRow};  // op(A) = X22^T, upper triangular
   rc = gemm(false, g21, 1, s, true);
   if (rc) return rc;
   rc = lauum_lower_rec(X, ldx, h, D, ldd, s);
