@@ -94,7 +94,10 @@ inline HermCoef herm_coef_host() {
 }
 
 // eval_phi_g_dim with the recurrence unrolled to kHermMax steps (guarded by M, L) and the
-// coefficients from `hc` (kernel parameters); identical operations and results.
+// coefficients from `hc` (kernel parameters); identical operations and results.  kScaled: out_phi
+// receives r * phi and out_rphi is ignored (a caller reading only r*phi of a dimension stores that
+// alone, with r = 1 for the others -- one store stream per task, no divergence).
+template <bool kScaled = false>
 __device__ __forceinline__ void eval_phi_g_dim_u(double x, double r, const BasisView& b, int d, const HermCoef& hc,
                                                  double* out_phi, double* out_g, double* out_rphi) {
   const int M = b.M, L = modal_L(M);
@@ -107,8 +110,12 @@ __device__ __forceinline__ void eval_phi_g_dim_u(double x, double r, const Basis
   double hg = __dmul_rn(yz, kSqrt2), hgm = 1.0;
   auto put_phi = [&](int k, double h) {
     const double v = __dmul_rn(env, h);
-    out_phi[k] = v;
-    if (out_rphi) out_rphi[k] = __dmul_rn(r, v);
+    if constexpr (kScaled) {
+      out_phi[k] = __dmul_rn(r, v);
+    } else {
+      out_phi[k] = v;
+      if (out_rphi) out_rphi[k] = __dmul_rn(r, v);
+    }
   };
   put_phi(0, 1.0);
   out_g[0] = amp;
@@ -133,10 +140,12 @@ __device__ __forceinline__ void eval_phi_g_dim_u(double x, double r, const Basis
 
 // eval_phi_g_dim_u for T independent (point, dimension) tasks advanced in lockstep (T chains
 // per thread hide each other's FP64 latency); identical operations and results per task.
+// out_phi[t] receives s[t] * phi (s = 1 leaves phi bit-identical; s = r gives the r*phi slot of
+// the last dimension): one store stream per task, so the warp's tasks never diverge.
 template <int T>
-__device__ __forceinline__ void eval_phi_g_dim_uT(const double (&x)[T], const double (&r)[T], const BasisView& b,
+__device__ __forceinline__ void eval_phi_g_dim_uT(const double (&x)[T], const double (&s)[T], const BasisView& b,
                                                   const int (&d)[T], const HermCoef& hc, double* const (&out_phi)[T],
-                                                  double* const (&out_g)[T], double* const (&out_rphi)[T]) {
+                                                  double* const (&out_g)[T]) {
   const int M = b.M, L = modal_L(M);
   double zr[T], env[T], amp[T], yz[T], hp[T], hpm[T], hg[T], hgm[T];
 #pragma unroll
@@ -152,9 +161,7 @@ __device__ __forceinline__ void eval_phi_g_dim_uT(const double (&x)[T], const do
     hgm[t] = 1.0;
   }
   auto put_phi = [&](int t, int k, double h) {
-    const double v = __dmul_rn(env[t], h);
-    out_phi[t][k] = v;
-    if (out_rphi[t]) out_rphi[t][k] = __dmul_rn(r[t], v);
+    out_phi[t][k] = __dmul_rn(s[t], __dmul_rn(env[t], h));
   };
 #pragma unroll
   for (int t = 0; t < T; ++t) {

@@ -468,31 +468,31 @@ fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__
     if (!plane) return;
     double rr[PR];
     int dd[PR];
-    double *ophi[PR], *og[PR], *orphi[PR];
+    double *ophi[PR], *og[PR];
     bool valid[PR];
+    // the split Gram reads phi of the last dimension only as r*phi: those tasks write r*phi into
+    // the rphi slot and no bare phi, the others phi (scale 1) -- 29 stores per task at C3
+    const bool last = pdim == p - 1;
 #pragma unroll
     for (int t = 0; t < PR; ++t) {
       double* row = slab + (prow + t * kGR) * rl.bw;
       valid[t] = blk_base(j) + prow + t * kGR < blk_end(j);
       if (valid[t]) bad_x |= not_finite(pr.x[t]);
-      rr[t] = __dsub_rn(pr.y[t], c);  // r = y - c (posterior.py:229)
+      rr[t] = last ? __dsub_rn(pr.y[t], c) : 1.0;  // r = y - c (posterior.py:229)
       dd[t] = pdim;
-      ophi[t] = row + rl.poff + pdim * M;
+      ophi[t] = last ? row + rl.rpoff : row + rl.poff + pdim * M;
       og[t] = row + rl.goff + pdim * L;
-      orphi[t] = pdim == p - 1 ? row + rl.rpoff : nullptr;
       if (pdim == 0) {
         row[rl.one] = 1.0;
         row[rl.zero] = 0.0;
       }
     }
-    eval_phi_g_dim_uT<PR>(pr.x, rr, b, dd, pl.hc, ophi, og, orphi);  // padding rows: x = 0, then zeroed
+    eval_phi_g_dim_uT<PR>(pr.x, rr, b, dd, pl.hc, ophi, og);  // padding rows: x = 0, then zeroed
 #pragma unroll
     for (int t = 0; t < PR; ++t) {
       if (valid[t]) continue;
       for (int k = 0; k < M; ++k) ophi[t][k] = 0.0;
       for (int k = 0; k < L; ++k) og[t][k] = 0.0;
-      if (orphi[t])
-        for (int k = 0; k < M; ++k) orphi[t][k] = 0.0;
     }
   };
   __syncthreads();

@@ -313,21 +313,22 @@ __device__ __forceinline__ void tile_body(const double* __restrict__ X, const do
       const double py = (y != nullptr && pdim[u] == p - 1) ? ys[prow[u]] : c;
       double* row = slab + prow[u] * bw;
       const bool valid = base + prow[u] < r1;
-      double* oph = row + pl.poff + pdim[u] * M;
+      // the B side reads the last dimension only as r*phi: that task stores r*phi alone, the
+      // others phi (scale 1)
+      const bool last = pdim[u] == p - 1;
+      double* oph = last ? row + pl.rpoff : row + pl.poff + pdim[u] * M;
       double* og = row + pl.goff + pdim[u] * L;
-      double* orp = pdim[u] == p - 1 ? row + pl.rpoff : nullptr;
       if (pdim[u] == 0) {
         row[pl.one] = 1.0;
         row[pl.zero] = 0.0;
       }
       if (valid) {
         bad_x |= not_finite(px);
-        eval_phi_g_dim_u(px, __dsub_rn(py, c), b, pdim[u], pl.hc, oph, og, orp);  // r = y - c (posterior.py:229)
+        // r = y - c (posterior.py:229)
+        eval_phi_g_dim_u<true>(px, last ? __dsub_rn(py, c) : 1.0, b, pdim[u], pl.hc, oph, og, nullptr);
       } else {  // rows past the range contribute zero
         for (int k = 0; k < M; ++k) oph[k] = 0.0;
         for (int k = 0; k < L; ++k) og[k] = 0.0;
-        if (orp)
-          for (int k = 0; k < M; ++k) orp[k] = 0.0;
       }
     }
   };
