@@ -7,6 +7,11 @@ compute-sanitizer (memcheck / racecheck / synccheck):
                               and the plain launch
   fused_predict_split_kernel  p = 3 split predict
   (+ the rest of a small p = 3, M = 10 posterior: expand3, pair_system, ctc3, ...)
+  tiled_gram_kernel / tiled_predict_kernel   output-tiled p = 4 (M = 8) and p = 5 (M = 6) paths,
+                              whose m = 4096 / 7776 factors run potrf_big (persistent diagonal
+                              blocks + triangular-clipped DGEMM panels), trtri and lauum
+  graph                       the p = 3 step captured as a CUDA graph and replayed
+  host_staging                numpy inputs through fagp_host_copy (non-temporal stores, worker pool)
 
 Usage (on the GPU box):
   compute-sanitizer --tool memcheck  --error-exitcode 9 python tools/sanitize_cases.py [case ...]
@@ -89,7 +94,49 @@ def posterior():
     assert np.all(np.isfinite(r.mean)) and np.all(r.var >= 0)
 
 
-CASES = {"cholinv": cholinv, "gram_pipelined": gram_pipelined, "posterior": posterior}
+def _model(p, M):
+    return F.GpModel(F.ArdKernelParams.isotropic(p, 1.0, 1.0), 0.0025, n_eigen=M)
+
+
+def tiled():
+    rng = np.random.default_rng(4)
+    for p, M, N, Ns in ((4, 8, 3000, 700), (5, 6, 1500, 300)):
+        X = rng.uniform(-1, 1, (N, p))
+        y = np.cos(X).sum(1)
+        Xs = rng.uniform(-1, 1, (Ns, p))
+        r = F.fagp_posterior(F.Dataset(X, y, 0.0, 0, ((-1.0, 1.0),) * p), Xs, _model(p, M), memory_cap=None)
+        assert np.all(np.isfinite(r.mean)) and np.all(r.var >= -1e-9), (p, M)
+
+
+def graph():
+    from paper_2403_12797_b200.engine import PosteriorEngine
+
+    rng = np.random.default_rng(5)
+    N, Ns = 5000, 2000
+    X = dev.to_device(rng.uniform(-1, 1, (N, 3)))
+    y = dev.to_device(np.cos(dev.to_host(X)).sum(1))
+    Xs = dev.to_device(rng.uniform(-1, 1, (Ns, 3)))
+    eng = PosteriorEngine(F.ArdKernelParams.isotropic(3, 1.0, 1.0), 10, N, Ns, 0.0025)
+    if eng.capture(X, y, Xs) is not None:
+        for _ in range(2):
+            mean, var = eng.replay()
+        torch.cuda.synchronize()
+        assert not eng.factor_needs_retry()
+        assert np.all(np.isfinite(dev.to_host(mean))) and np.all(dev.to_host(var) >= -1e-9)
+
+
+def host_staging():
+    from paper_2403_12797_b200 import engine
+
+    rng = np.random.default_rng(6)
+    src = rng.standard_normal(1 << 20)
+    dst = torch.empty(src.shape[0], dtype=torch.float64).pin_memory()
+    engine._parallel_copy(dst.numpy(), src)
+    assert np.array_equal(dst.numpy(), src)
+
+
+CASES = {"cholinv": cholinv, "gram_pipelined": gram_pipelined, "posterior": posterior, "tiled": tiled,
+         "graph": graph, "host_staging": host_staging}
 
 if __name__ == "__main__":
     torch.cuda.set_device(0)
