@@ -575,42 +575,44 @@ fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__
   for (int q = 0; q < NACC; ++q) acc[q][0] = acc[q][1] = 0.0;
   __syncthreads();
 
-  auto kstep = [&](const double* cur, int i) {
+  // one lambda per role, the role branch hoisted out of the k-loop below: a branch inside every
+  // k-step kept the scheduler from overlapping k-step i + 1's loads with k-step i's DMMAs
+  auto kstep1 = [&](const double* cur, int i) {
     const double* row = cur + (i * 4 + (lane & 3)) * SBW;
-    if (role1) {
-      const double b0 = row[offB[0]], b1 = row[offB[1]], bt = row[offB[2]];
+    const double b0 = row[offB[0]], b1 = row[offB[1]], bt = row[offB[2]];
 #pragma unroll
-      for (int j = 0; j < JK1; ++j) {
-        const double a = __dmul_rn(row[offA[j][0]], row[offA[j][1]]);
-        dmma_8x8x4(acc[2 * j][0], acc[2 * j][1], a, b0);
-        dmma_8x8x4(acc[2 * j + 1][0], acc[2 * j + 1][1], a, b1);
-      }
+    for (int j = 0; j < JK1; ++j) {
+      const double a = __dmul_rn(row[offA[j][0]], row[offA[j][1]]);
+      dmma_8x8x4(acc[2 * j][0], acc[2 * j][1], a, b0);
+      dmma_8x8x4(acc[2 * j + 1][0], acc[2 * j + 1][1], a, b1);
+    }
 #pragma unroll
-      for (int j = 0; j < JT1A; ++j) {
-        const double a = __dmul_rn(row[offA[JK1 + j][0]], row[offA[JK1 + j][1]]);
-        dmma_8x8x4(acc[2 * JK1 + j][0], acc[2 * JK1 + j][1], a, bt);
-      }
-    } else {
-      const double b0 = row[offB[0]], b1 = row[offB[1]], b2 = row[offB[2]], p0 = row[offB[3]], p1 = row[offB[4]];
-      const double bt = row[rl.rpoff + col];
+    for (int j = 0; j < JT1A; ++j) {
+      const double a = __dmul_rn(row[offA[JK1 + j][0]], row[offA[JK1 + j][1]]);
+      dmma_8x8x4(acc[2 * JK1 + j][0], acc[2 * JK1 + j][1], a, bt);
+    }
+  };
+  auto kstep2 = [&](const double* cur, int i) {
+    const double* row = cur + (i * 4 + (lane & 3)) * SBW;
+    const double b0 = row[offB[0]], b1 = row[offB[1]], b2 = row[offB[2]], p0 = row[offB[3]], p1 = row[offB[4]];
+    const double bt = row[rl.rpoff + col];
 #pragma unroll
-      for (int j = 0; j < JK2; ++j) {
-        const double a = __dmul_rn(row[offA[j][0]], row[offA[j][1]]);
-        dmma_8x8x4(acc[3 * j][0], acc[3 * j][1], a, b0);
-        dmma_8x8x4(acc[3 * j + 1][0], acc[3 * j + 1][1], a, b1);
-        dmma_8x8x4(acc[3 * j + 2][0], acc[3 * j + 2][1], a, b2);
-      }
+    for (int j = 0; j < JK2; ++j) {
+      const double a = __dmul_rn(row[offA[j][0]], row[offA[j][1]]);
+      dmma_8x8x4(acc[3 * j][0], acc[3 * j][1], a, b0);
+      dmma_8x8x4(acc[3 * j + 1][0], acc[3 * j + 1][1], a, b1);
+      dmma_8x8x4(acc[3 * j + 2][0], acc[3 * j + 2][1], a, b2);
+    }
 #pragma unroll
-      for (int j = 0; j < JT2; ++j) {
-        const double a = __dmul_rn(row[offA[JK2 + j][0]], row[offA[JK2 + j][1]]);
-        dmma_8x8x4(acc[3 * JK2 + 2 * j][0], acc[3 * JK2 + 2 * j][1], a, p0);
-        dmma_8x8x4(acc[3 * JK2 + 2 * j + 1][0], acc[3 * JK2 + 2 * j + 1][1], a, p1);
-      }
+    for (int j = 0; j < JT2; ++j) {
+      const double a = __dmul_rn(row[offA[JK2 + j][0]], row[offA[JK2 + j][1]]);
+      dmma_8x8x4(acc[3 * JK2 + 2 * j][0], acc[3 * JK2 + 2 * j][1], a, p0);
+      dmma_8x8x4(acc[3 * JK2 + 2 * j + 1][0], acc[3 * JK2 + 2 * j + 1][1], a, p1);
+    }
 #pragma unroll
-      for (int j = 0; j < JT1B; ++j) {
-        const double a = __dmul_rn(row[offA[JK2 + JT2 + j][0]], row[offA[JK2 + JT2 + j][1]]);
-        dmma_8x8x4(acc[3 * JK2 + 2 * JT2 + j][0], acc[3 * JK2 + 2 * JT2 + j][1], a, bt);
-      }
+    for (int j = 0; j < JT1B; ++j) {
+      const double a = __dmul_rn(row[offA[JK2 + JT2 + j][0]], row[offA[JK2 + JT2 + j][1]]);
+      dmma_8x8x4(acc[3 * JK2 + 2 * JT2 + j][0], acc[3 * JK2 + 2 * JT2 + j][1], a, bt);
     }
   };
   auto flush = [&](int k) {
@@ -657,9 +659,15 @@ fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__
     // k-steps holding a valid row (a CTA's last block may be partial; padding rows are zero)
     const int nks = int(tmax<int64_t>(0, blk_end(n) - blk_base(n)) + 3) / 4;
     if (nks == BR / 4) {
-      SPROF(0, _Pragma("unroll 16") for (int i = 0; i < BR / 4; ++i) kstep(cur, i))
+      if (role1) {
+        SPROF(0, _Pragma("unroll 16") for (int i = 0; i < BR / 4; ++i) kstep1(cur, i))
+      } else {
+        SPROF(0, _Pragma("unroll 16") for (int i = 0; i < BR / 4; ++i) kstep2(cur, i))
+      }
+    } else if (role1) {
+      SPROF(0, for (int i = 0; i < nks; ++i) kstep1(cur, i))
     } else {
-      SPROF(0, for (int i = 0; i < nks; ++i) kstep(cur, i))
+      SPROF(0, for (int i = 0; i < nks; ++i) kstep2(cur, i))
     }
     if (pl.once) {
       SPROF(2, if (n + 1 == nblk) flush(0))
