@@ -135,8 +135,179 @@ __global__ void __launch_bounds__(GNT) dgemm_kernel(GemmArgs g) {
   }
 }
 
+// Pipelined variants for the m >= 3000 factor's GEMMs (blocked potrf panels and trailing update,
+// TRTRI levels, lauum): BM x BN output tile per CTA, WM x WN warps with a (BM/WM) x (BN/WN) warp tile,
+// K slabs of 16 staged by 8-byte cp.async (zero-filled past the edges, any alignment) into a
+// STG-deep ring so the next slabs' loads overlap this slab's DMMAs.  Shared layouts keep every
+// fragment read conflict-free: row strides = 4 (mod 16) doubles, [m][k] / [k][m] as the operand is
+// stored (the transposed operand is copied as it lies, coalesced, and read transposed).  Same
+// triangular K clipping, lower-only tiles, batching and info skip as above.
+constexpr int BK = 16;
+constexpr int BSK = BK + 4;  // [row][k] stride
+
+__device__ __forceinline__ void cp_async_8zf(double* smem, const double* gmem, bool valid) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 8 : 0));
+}
+
+template <int BM, int BN, int WM, int WN, int STG>
+struct BigCfg {
+  static constexpr int NT = 32 * WM * WN;
+  static constexpr int FM = BM / WM / 8, FN = BN / WN / 8;
+  static constexpr int AOP = BM * BSK > BK * (BM + 4) ? BM * BSK : BK * (BM + 4);
+  static constexpr int BOP = BN * BSK > BK * (BN + 4) ? BN * BSK : BK * (BN + 4);
+  static constexpr size_t smem = size_t(STG) * (AOP + BOP) * sizeof(double);
+};
+
+template <int BM, int BN, int WM, int WN, int STG, int MINB, bool TA, bool TB>
+__global__ void __launch_bounds__(32 * WM * WN, MINB) dgemm_big_kernel(GemmArgs g) {
+  using Cf = BigCfg<BM, BN, WM, WN, STG>;
+  constexpr int NT = Cf::NT, FM = Cf::FM, FN = Cf::FN, AOP = Cf::AOP, BOP = Cf::BOP;
+  constexpr int SRA = BM + 4, SRB = BN + 4;  // [k][row] strides
+  if (g.info && *g.info) return;
+  const int row0 = blockIdx.y * BM, col0 = blockIdx.x * BN;
+  if (g.lower_only && col0 > row0 + BM - 1) return;
+  const double* A = g.A + blockIdx.z * g.sA;
+  const double* B = g.B + blockIdx.z * g.sB;
+  double* C = g.C + blockIdx.z * g.sC;
+  extern __shared__ double gsm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / WN, wn = warp % WN;
+  int kb = 0, ke = g.K;
+  if (g.tri & kTriKminCol) kb = tmax(kb, col0);
+  if (g.tri & kTriKminRow) kb = tmax(kb, row0);
+  if (g.tri & kTriKmaxRow) ke = tmin(ke, row0 + BM);
+  if (g.tri & kTriKmaxCol) ke = tmin(ke, col0 + BN);
+  kb = kb / BK * BK;  // (tile edges are multiples of BK: the clipped range is whole slabs)
+  const int nslab = ke > kb ? (ke - kb + BK - 1) / BK : 0;
+
+  auto load = [&](int slab) {
+    double* As = gsm + (slab % STG) * (AOP + BOP);
+    double* Bs = As + AOP;
+    const int k0 = kb + slab * BK;
+#pragma unroll
+    for (int q = 0; q < (BM * BK) / NT; ++q) {
+      const int e = tid + q * NT;
+      if (TA) {  // A stored K x M: [k][m]
+        const int k = e / BM, r = e % BM, gr = row0 + r, gk = k0 + k;
+        const bool ok = gr < g.M && gk < g.K;
+        cp_async_8zf(As + k * SRA + r, ok ? A + int64_t(gk) * g.lda + gr : A, ok);
+      } else {  // [m][k]
+        const int r = e / BK, k = e % BK, gr = row0 + r, gk = k0 + k;
+        const bool ok = gr < g.M && gk < g.K;
+        cp_async_8zf(As + r * BSK + k, ok ? A + int64_t(gr) * g.lda + gk : A, ok);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < (BN * BK) / NT; ++q) {
+      const int e = tid + q * NT;
+      if (TB) {  // B stored N x K: [n][k]
+        const int n = e / BK, k = e % BK, gn = col0 + n, gk = k0 + k;
+        const bool ok = gn < g.N && gk < g.K;
+        cp_async_8zf(Bs + n * BSK + k, ok ? B + int64_t(gn) * g.ldb + gk : B, ok);
+      } else {  // [k][n]
+        const int k = e / BN, n = e % BN, gn = col0 + n, gk = k0 + k;
+        const bool ok = gn < g.N && gk < g.K;
+        cp_async_8zf(Bs + k * SRB + n, ok ? B + int64_t(gk) * g.ldb + gn : B, ok);
+      }
+    }
+  };
+
+  double acc[FM][FN][2];
+#pragma unroll
+  for (int f = 0; f < FM; ++f)
+#pragma unroll
+    for (int t = 0; t < FN; ++t) acc[f][t][0] = acc[f][t][1] = 0.0;
+#pragma unroll
+  for (int st = 0; st < STG - 1; ++st) {
+    if (st < nslab) load(st);
+    cp_async_commit();
+  }
+  const int ar = wm * (BM / WM) + (lane >> 2), bc = wn * (BN / WN) + (lane >> 2), kl = lane & 3;
+  for (int slab = 0; slab < nslab; ++slab) {
+    cp_async_wait<STG - 2>();
+    __syncthreads();  // slab visible to all; the ring slot the next load overwrites is free
+    if (slab + STG - 1 < nslab) load(slab + STG - 1);
+    cp_async_commit();
+    const double* As = gsm + (slab % STG) * (AOP + BOP);
+    const double* Bs = As + AOP;
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      const int k = kk * 4 + kl;
+      double a[FM], b[FN];
+#pragma unroll
+      for (int f = 0; f < FM; ++f) a[f] = TA ? As[k * SRA + ar + 8 * f] : As[(ar + 8 * f) * BSK + k];
+#pragma unroll
+      for (int t = 0; t < FN; ++t) b[t] = TB ? Bs[(bc + 8 * t) * BSK + k] : Bs[k * SRB + bc + 8 * t];
+#pragma unroll
+      for (int f = 0; f < FM; ++f)
+#pragma unroll
+        for (int t = 0; t < FN; ++t) dmma_8x8x4(acc[f][t][0], acc[f][t][1], a[f], b[t]);
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int f = 0; f < FM; ++f) {
+    const int i = row0 + wm * (BM / WM) + f * 8 + (lane >> 2);
+    if (i >= g.M) continue;
+#pragma unroll
+    for (int t = 0; t < FN; ++t) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = col0 + wn * (BN / WN) + t * 8 + 2 * (lane & 3) + e;
+        if (j >= g.N || (g.lower_only && j > i)) continue;
+        double* c = C + int64_t(i) * g.ldc + j;
+        const double v = g.alpha * acc[f][t][e];
+        *c = (g.beta == 0.0) ? v : fma(g.beta, *c, v);
+      }
+    }
+  }
+}
+
+template <int BM, int BN, int WM, int WN, int STG, int MINB, bool TA, bool TB>
+static int launch_big1(const GemmArgs& g, int batch, cudaStream_t s) {
+  using Cf = BigCfg<BM, BN, WM, WN, STG>;
+  auto kern = dgemm_big_kernel<BM, BN, WM, WN, STG, MINB, TA, TB>;
+  static bool attr_set[kMaxDevices];  // the smem opt-in is per device context
+  int dev = 0;
+  FAGP_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev >= kMaxDevices || !attr_set[dev]) {
+    FAGP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cf::smem)));
+    if (dev < kMaxDevices) attr_set[dev] = true;
+  }
+  dim3 grid(unsigned(ceil_div(g.N, BN)), unsigned(ceil_div(g.M, BM)), unsigned(batch));
+  kern<<<grid, Cf::NT, Cf::smem, s>>>(g);
+  FAGP_LAUNCH_CHECK();
+  return FAGP_OK;
+}
+
+template <int BM, int BN, int WM, int WN, int STG, int MINB>
+static int launch_big(const GemmArgs& g, int batch, cudaStream_t s, bool transA, bool transB) {
+  if (transA)
+    return transB ? launch_big1<BM, BN, WM, WN, STG, MINB, true, true>(g, batch, s)
+                  : launch_big1<BM, BN, WM, WN, STG, MINB, true, false>(g, batch, s);
+  return transB ? launch_big1<BM, BN, WM, WN, STG, MINB, false, true>(g, batch, s)
+                : launch_big1<BM, BN, WM, WN, STG, MINB, false, false>(g, batch, s);
+}
+
 inline int gemm(bool transB, const GemmArgs& g, int batch, cudaStream_t s, bool transA = false) {
   if (g.M <= 0 || g.N <= 0 || batch <= 0) return FAGP_OK;
+  static const int big_mode = [] {  // FAGP_GEMM_BIG: 0 = the unpipelined kernel everywhere; 2, 3 tile configs
+    const char* e = getenv("FAGP_GEMM_BIG");
+    return e ? atoi(e) : 3;
+  }();
+  // a large tile where it fills the GPU: both output sides >= 256 and K >= 64
+  if (big_mode && g.M >= 256 && g.N >= 256 && g.K >= 64) {
+    // measured (profiles/dgemm_cfg_probe_r05.txt, 4096^3 and the factor's shapes): 64 x 64 tiles
+    // with the cp.async ring, 4 CTAs / SM, 31-33 TF/s against 25-30 for the unpipelined kernel;
+    // 128 x 64 (2 CTAs / SM) 30-32; 128 x 128 tiles with 8 or 16 warps 27-32, and slower inside
+    // the factor (coarser lower-only / triangular tiles)
+    switch (big_mode) {
+      case 2: return launch_big<128, 64, 4, 2, 3, 2>(g, batch, s, transA, transB);  // 32 x 32 warp tiles, 2 CTAs / SM
+      case 3: return launch_big<64, 64, 2, 2, 3, 4>(g, batch, s, transA, transB);   // 32 x 32 warp tiles, 4 CTAs / SM
+      default: break;
+    }
+  }
   dim3 grid(unsigned(ceil_div(g.N, GT)), unsigned(ceil_div(g.M, GT)), unsigned(batch));
   if (transA) {
     if (transB)

@@ -530,3 +530,21 @@ def test_host_pipeline_chunking_is_bitwise_invariant(subranges, chunks, monkeypa
     Host.X, Host.y = torch.from_numpy(X).pin_memory(), y
     got = F.fagp_posterior(Host, Xs, model, memory_cap=None)
     assert np.array_equal(got.mean, ref.mean) and np.array_equal(got.var, ref.var)
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(256, 256, 64), (300, 257, 70), (513, 640, 129), (1000, 384, 1000)])
+def test_dgemm_large_tile_matches_numpy(M, N, K, ta, tb):
+    """The 128 x 128-tile DGEMM (both output sides >= 256, K >= 64: the m >= 3000 factor's GEMMs),
+    every transpose combination, ragged edges, alpha / beta accumulation."""
+    from paper_2403_12797_b200.linalg import dgemm
+
+    rng = np.random.default_rng(M + 7 * N + 13 * K + 2 * ta + tb)
+    a = rng.standard_normal((K, M) if ta else (M, K))
+    b = rng.standard_normal((N, K) if tb else (K, N))
+    c0 = rng.standard_normal((M, N))
+    ref = -0.5 * ((a.T if ta else a) @ (b.T if tb else b)) + 2.0 * c0
+    out = dev.to_device(c0)
+    got = dev.to_host(dgemm(a, b, trans_a=bool(ta), trans_b=bool(tb), alpha=-0.5, beta=2.0, out=out))
+    scale = np.abs(a).max() * np.abs(b).max() * K
+    assert np.abs(got - ref).max() <= 1e-14 * scale
