@@ -29,7 +29,9 @@
 //    variance come out of the same pass.
 // Shapes whose output does not fit these layouts use the tiled table kernels (modal.cu,
 // gram.cu, predict.cu) -- see fagp_gram_x / fagp_predict_x.
+#include <algorithm>
 #include <cstring>
+#include <type_traits>
 
 #include "common.cuh"
 #include "eigfun.cuh"
@@ -127,6 +129,10 @@ struct GPlan {
   int split, W1, R, R2;          // warps in role 1; L - 16; M - 8
   int kmf1, kmf2, tmf1, tmf2;    // m-fragments of K1, K2, T1, T2
   int baseK2, baseT1, baseT2;    // fragment offsets of the sections in a partial
+  // physical warp -> slot (slot < W1: role-1 warp index, else W1 + role-2 index): warp w issues on
+  // SM sub-partition w % 4, and the slots' useful DMMA counts differ (reduced classes), so the
+  // slots are dealt to balance the sub-partitions (C3: 36 -> 34 DMMA per k-step on the busiest)
+  unsigned char wslot[kGramW];
   // launch mode: once = one partial per (CTA, row group) flushed at the end of the launch
   // (slot cta G + grp) instead of one per sub-range; ready (nullable) = per-sub-range words a
   // host pipeline sets non-zero (by a stream-ordered H2D copy) once the sub-range's rows landed
@@ -518,8 +524,9 @@ fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__
       off[1] = rl.one;
     }
   };
-  const bool role1 = warp < pl.W1;
-  const int wi = role1 ? warp : warp - pl.W1, WR = role1 ? pl.W1 : kGramW - pl.W1;
+  const int slot = pl.wslot[warp];
+  const bool role1 = slot < pl.W1;
+  const int wi = role1 ? slot : slot - pl.W1, WR = role1 ? pl.W1 : kGramW - pl.W1;
   constexpr int NJ = (JK1 + JT1A) > (JK2 + JT2 + JT1B) ? (JK1 + JT1A) : (JK2 + JT2 + JT1B);
   constexpr int NACC = (2 * JK1 + JT1A) > (3 * JK2 + 2 * JT2 + JT1B) ? (2 * JK1 + JT1A) : (3 * JK2 + 2 * JT2 + JT1B);
   int offA[NJ][2], offB[5];
@@ -575,13 +582,17 @@ fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__
   for (int q = 0; q < NACC; ++q) acc[q][0] = acc[q][1] = 0.0;
   __syncthreads();
 
-  // one lambda per role, the role branch hoisted out of the k-loop below: a branch inside every
-  // k-step kept the scheduler from overlapping k-step i + 1's loads with k-step i's DMMAs
-  auto kstep1 = [&](const double* cur, int i) {
+  // one straight-line k-step per warp class, the class branch hoisted out of the k-loop below (a
+  // branch inside every k-step kept the scheduler from overlapping k-step i + 1's loads with
+  // k-step i's DMMAs).  Classes: role 1 with NK1 K1 m-fragments (+ JT1A T1), role 2 with JK2 K2,
+  // NT2 T2 and NT1B T1 m-fragments.  At C3 the slots past the last fragment (9 of 144 DMMA per
+  // k-step) belong to warps of the reduced classes, which skip them at no per-k-step cost.
+  auto kstep1 = [&](const double* cur, int i, auto nk1) {
+    constexpr int NK1 = decltype(nk1)::value;
     const double* row = cur + (i * 4 + (lane & 3)) * SBW;
     const double b0 = row[offB[0]], b1 = row[offB[1]], bt = row[offB[2]];
 #pragma unroll
-    for (int j = 0; j < JK1; ++j) {
+    for (int j = 0; j < NK1; ++j) {
       const double a = __dmul_rn(row[offA[j][0]], row[offA[j][1]]);
       dmma_8x8x4(acc[2 * j][0], acc[2 * j][1], a, b0);
       dmma_8x8x4(acc[2 * j + 1][0], acc[2 * j + 1][1], a, b1);
@@ -592,10 +603,10 @@ fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__
       dmma_8x8x4(acc[2 * JK1 + j][0], acc[2 * JK1 + j][1], a, bt);
     }
   };
-  auto kstep2 = [&](const double* cur, int i) {
+  auto kstep2 = [&](const double* cur, int i, auto nt2, auto nt1b) {
+    constexpr int NT2 = decltype(nt2)::value, NT1B = decltype(nt1b)::value;
     const double* row = cur + (i * 4 + (lane & 3)) * SBW;
-    const double b0 = row[offB[0]], b1 = row[offB[1]], b2 = row[offB[2]], p0 = row[offB[3]], p1 = row[offB[4]];
-    const double bt = row[rl.rpoff + col];
+    const double b0 = row[offB[0]], b1 = row[offB[1]], b2 = row[offB[2]];
 #pragma unroll
     for (int j = 0; j < JK2; ++j) {
       const double a = __dmul_rn(row[offA[j][0]], row[offA[j][1]]);
@@ -603,16 +614,66 @@ fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__
       dmma_8x8x4(acc[3 * j + 1][0], acc[3 * j + 1][1], a, b1);
       dmma_8x8x4(acc[3 * j + 2][0], acc[3 * j + 2][1], a, b2);
     }
+    if constexpr (NT2 > 0) {
+      const double p0 = row[offB[3]], p1 = row[offB[4]];
 #pragma unroll
-    for (int j = 0; j < JT2; ++j) {
-      const double a = __dmul_rn(row[offA[JK2 + j][0]], row[offA[JK2 + j][1]]);
-      dmma_8x8x4(acc[3 * JK2 + 2 * j][0], acc[3 * JK2 + 2 * j][1], a, p0);
-      dmma_8x8x4(acc[3 * JK2 + 2 * j + 1][0], acc[3 * JK2 + 2 * j + 1][1], a, p1);
+      for (int j = 0; j < NT2; ++j) {
+        const double a = __dmul_rn(row[offA[JK2 + j][0]], row[offA[JK2 + j][1]]);
+        dmma_8x8x4(acc[3 * JK2 + 2 * j][0], acc[3 * JK2 + 2 * j][1], a, p0);
+        dmma_8x8x4(acc[3 * JK2 + 2 * j + 1][0], acc[3 * JK2 + 2 * j + 1][1], a, p1);
+      }
     }
+    if constexpr (NT1B > 0) {
+      const double bt = row[rl.rpoff + col];
 #pragma unroll
-    for (int j = 0; j < JT1B; ++j) {
-      const double a = __dmul_rn(row[offA[JK2 + JT2 + j][0]], row[offA[JK2 + JT2 + j][1]]);
-      dmma_8x8x4(acc[3 * JK2 + 2 * JT2 + j][0], acc[3 * JK2 + 2 * JT2 + j][1], a, bt);
+      for (int j = 0; j < NT1B; ++j) {
+        const double a = __dmul_rn(row[offA[JK2 + JT2 + j][0]], row[offA[JK2 + JT2 + j][1]]);
+        dmma_8x8x4(acc[3 * JK2 + 2 * JT2 + j][0], acc[3 * JK2 + 2 * JT2 + j][1], a, bt);
+      }
+    }
+  };
+  // this warp's class from its valid slots (prefixes): 0 role 1 full, 1 role 1 with JK1 - 1 K1
+  // fragments, 2 role 2 full, 3 role 2 without its T1B fragment, 4 without T2 and T1B; any other
+  // pattern runs the full class of its role (dummy slots compute discarded fragments)
+  int cls;
+  {
+    int nk = 0, nt = 0, nb = 0;
+    if (role1) {
+#pragma unroll
+      for (int j = 0; j < JK1; ++j) nk += fragOf[2 * j] >= 0;
+#pragma unroll
+      for (int j = 0; j < JT1A; ++j) nt += fragOf[2 * JK1 + j] >= 0;
+      cls = (nk == JK1 - 1 && nt == JT1A) ? 1 : 0;
+    } else {
+#pragma unroll
+      for (int j = 0; j < JK2; ++j) nk += fragOf[3 * j] >= 0;
+#pragma unroll
+      for (int j = 0; j < JT2; ++j) nt += fragOf[3 * JK2 + 2 * j] >= 0;
+#pragma unroll
+      for (int j = 0; j < JT1B; ++j) nb += fragOf[3 * JK2 + 2 * JT2 + j] >= 0;
+      cls = (nk == JK2 && nt == JT2 && nb == 0) ? 3 : (nk == JK2 && nt == 0 && nb == 0) ? 4 : 2;
+    }
+  }
+  using I0 = std::integral_constant<int, 0>;
+  using IK1 = std::integral_constant<int, JK1>;
+  using IK1m = std::integral_constant<int, (JK1 > 0 ? JK1 - 1 : 0)>;
+  using IT2 = std::integral_constant<int, JT2>;
+  using IT1B = std::integral_constant<int, JT1B>;
+  auto kloop = [&](const double* cur, int nks, auto body) {
+    if (nks == BR / 4) {
+#pragma unroll 16
+      for (int i = 0; i < BR / 4; ++i) body(cur, i);
+    } else {
+      for (int i = 0; i < nks; ++i) body(cur, i);
+    }
+  };
+  auto contract_block = [&](const double* cur, int nks) {
+    switch (cls) {
+      case 1: kloop(cur, nks, [&](const double* c, int i) { kstep1(c, i, IK1m{}); }); break;
+      case 2: kloop(cur, nks, [&](const double* c, int i) { kstep2(c, i, IT2{}, IT1B{}); }); break;
+      case 3: kloop(cur, nks, [&](const double* c, int i) { kstep2(c, i, IT2{}, I0{}); }); break;
+      case 4: kloop(cur, nks, [&](const double* c, int i) { kstep2(c, i, I0{}, I0{}); }); break;
+      default: kloop(cur, nks, [&](const double* c, int i) { kstep1(c, i, IK1{}); }); break;
     }
   };
   auto flush = [&](int k) {
@@ -658,17 +719,7 @@ fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__
     }
     // k-steps holding a valid row (a CTA's last block may be partial; padding rows are zero)
     const int nks = int(tmax<int64_t>(0, blk_end(n) - blk_base(n)) + 3) / 4;
-    if (nks == BR / 4) {
-      if (role1) {
-        SPROF(0, _Pragma("unroll 16") for (int i = 0; i < BR / 4; ++i) kstep1(cur, i))
-      } else {
-        SPROF(0, _Pragma("unroll 16") for (int i = 0; i < BR / 4; ++i) kstep2(cur, i))
-      }
-    } else if (role1) {
-      SPROF(0, for (int i = 0; i < nks; ++i) kstep1(cur, i))
-    } else {
-      SPROF(0, for (int i = 0; i < nks; ++i) kstep2(cur, i))
-    }
+    SPROF(0, contract_block(cur, nks))
     if (pl.once) {
       SPROF(2, if (n + 1 == nblk) flush(0))
     } else {
@@ -767,6 +818,45 @@ static int64_t ipow(int64_t b, int e) {
 constexpr int kGramShapes[][2] = {{1, 1}, {3, 1}, {4, 2}};
 
 // Plan for N rows; false when the shape needs the tiled table path.
+
+// Useful DMMA per k-step of each split slot (template split <4, 1, 2, 1, 1>; a slot's skipped
+// fragments are those of the reduced classes in fused_gram_split_kernel, others count in full),
+// then slots placed on the 4 SM sub-partitions largest first, each onto the least-loaded
+// sub-partition with a free warp slot (4 warps each).
+static void split_warp_map(GPlan& pl) {
+  constexpr int JK1 = 4, JT1A = 1, JK2 = 2, JT2 = 1, JT1B = 1;
+  const int W2 = kGramW - pl.W1;
+  int load[kGramW];
+  for (int sl = 0; sl < kGramW; ++sl) {
+    int nk = 0, nt = 0, nb = 0;
+    if (sl < pl.W1) {
+      for (int j = 0; j < JK1; ++j) nk += sl + pl.W1 * j < pl.kmf1;
+      for (int j = 0; j < JT1A; ++j) nt += sl + pl.W1 * j < pl.tmf1;
+      load[sl] = (nk == JK1 - 1 && nt == JT1A) ? 2 * (JK1 - 1) + JT1A : 2 * JK1 + JT1A;
+    } else {
+      const int wi = sl - pl.W1;
+      for (int j = 0; j < JK2; ++j) nk += wi + W2 * j < pl.kmf2;
+      for (int j = 0; j < JT2; ++j) nt += wi + W2 * j < pl.tmf2;
+      for (int j = 0; j < JT1B; ++j) nb += pl.W1 * JT1A + wi + W2 * j < pl.tmf1;
+      load[sl] = (nk == JK2 && nt == JT2 && nb == 0)  ? 3 * JK2 + 2 * JT2
+                 : (nk == JK2 && nt == 0 && nb == 0) ? 3 * JK2
+                                                      : 3 * JK2 + 2 * JT2 + JT1B;
+    }
+  }
+  int order[kGramW];
+  for (int sl = 0; sl < kGramW; ++sl) order[sl] = sl;
+  std::stable_sort(order, order + kGramW, [&](int a, int b) { return load[a] > load[b]; });
+  int sp_load[4] = {0, 0, 0, 0}, sp_used[4] = {0, 0, 0, 0};
+  for (int k = 0; k < kGramW; ++k) {
+    int best = -1;
+    for (int q = 0; q < 4; ++q)
+      if (sp_used[q] < kGramW / 4 && (best < 0 || sp_load[q] < sp_load[best])) best = q;
+    pl.wslot[best + 4 * sp_used[best]] = static_cast<unsigned char>(order[k]);
+    sp_load[best] += load[order[k]];
+    ++sp_used[best];
+  }
+}
+
 static bool make_gplan(int64_t N, int p, int M, GPlan& pl) {
   std::memset(&pl, 0, sizeof(pl));
   if (!modal_on(p, M) || p > kMaxF || M > 12 || kGR * p > kGramNT) return false;
@@ -848,6 +938,7 @@ static bool make_gplan(int64_t N, int p, int M, GPlan& pl) {
     pl.G = 1;
     pl.WG = kGramW;
     pl.nparts = pl.grid * pl.S;
+    split_warp_map(pl);
   }
   return true;
 }
