@@ -21,6 +21,7 @@
 //    (eigfun.cuh, one exponential shared by phi and g).
 //  * Tiles are dealt to the CTAs by a per-row cost (k-steps + production / epilogue), rows split
 //    evenly over a tile's CTAs.
+#include <type_traits>
 #include <cstdio>
 #include <cstring>
 
@@ -295,8 +296,7 @@ tiled_predict_kernel(const double* __restrict__ Xs, BasisView b, const __grid_co
         for (int j = 0; j < kCF; ++j) acc[f][j][0] = acc[f][j][1] = 0.0;
       const double* rowA = slab + (rg * 16 + (lane >> 2)) * bw;  // m-fragment f: + 8 f rows
       const double* Bw = Bt + (cg * kCF) * 32 + lane;
-#pragma unroll 4
-      for (int ks = 0; ks < nks; ++ks) {
+      auto kstep = [&](int ks) {
         const uint32_t pk = offA[4 * ks + (lane & 3)];
         double a[kRF], bb[kCF];
 #pragma unroll
@@ -307,7 +307,9 @@ tiled_predict_kernel(const double* __restrict__ Xs, BasisView b, const __grid_co
         for (int f = 0; f < kRF; ++f)
 #pragma unroll
           for (int j = 0; j < kCF; ++j) dmma_8x8x4(acc[f][j][0], acc[f][j][1], a[f], bb[j]);
-      }
+      };
+#pragma unroll 4
+      for (int ks = 0; ks < nks; ++ks) kstep(ks);
       // epilogue: Y[row][col] * prod_{d >= q} (g | phi)_d[row][col digits], summed over the columns
 #pragma unroll
       for (int f = 0; f < kRF; ++f) {
