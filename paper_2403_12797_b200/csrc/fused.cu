@@ -737,10 +737,14 @@ fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__
 
 // out[e] = sum over the partials (fixed order: deterministic) of entry e of [K | t], read from
 // the fragment-major partial layout; non-finite -> PHI flag
-constexpr int kPSE = 8, kPSG = 64;  // partial_sum: entries per CTA x partial groups (many groups: C2-size
-                                     // plans have ~2400 partials per entry)
-__global__ void __launch_bounds__(kPSE * kPSG) partial_sum_kernel(const double* __restrict__ ws, const GPlan pl,
-                                                                  double* __restrict__ out, uint32_t* flags) {
+// partial_sum: PSE entries per CTA x PSG partial groups, 512 threads.  Many groups for the C2-size
+// plans (~2400 partials per entry); few for the one-launch plans (C3: 148), whose CTAs then cover 64
+// entries and the final group sum is 8 adds instead of a 64-long chain
+constexpr int kPSE = 8, kPSG = 64;
+template <int PSE, int PSG>
+__global__ void __launch_bounds__(PSE * PSG) partial_sum_kernel(const double* __restrict__ ws, const GPlan pl,
+                                                                double* __restrict__ out, uint32_t* flags) {
+  constexpr int kPSE = PSE, kPSG = PSG;
   __shared__ double red[kPSG][kPSE];
   const int NFK = int(ceil_div(pl.KB, 8)), NFT = int(ceil_div(pl.TB, 8));
   const int grp = int(threadIdx.x) / kPSE, el = int(threadIdx.x) % kPSE;
@@ -1079,7 +1083,8 @@ int gram(const double* X, const double* y, double c, int64_t N, const fagp_basis
     static bool loaded = false;
     if (!loaded) {
       cudaFuncAttributes fa;
-      FAGP_CUDA_TRY(cudaFuncGetAttributes(&fa, partial_sum_kernel));
+      FAGP_CUDA_TRY(cudaFuncGetAttributes(&fa, partial_sum_kernel<64, 8>));
+      FAGP_CUDA_TRY(cudaFuncGetAttributes(&fa, partial_sum_kernel<kPSE, kPSG>));
       loaded = true;
     }
   }
@@ -1101,7 +1106,10 @@ int gram(const double* X, const double* y, double c, int64_t N, const fagp_basis
   FAGP_LAUNCH_CHECK();
   if (k1 == pl.S) {
     if (pl.once) pl.nparts = pl.grid * pl.G;
-    partial_sum_kernel<<<unsigned(ceil_div(pl.len, kPSE)), kPSE * kPSG, 0, s>>>(w, pl, out, flags);
+    if (pl.nparts <= 1024)
+      partial_sum_kernel<64, 8><<<unsigned(ceil_div(pl.len, 64)), 512, 0, s>>>(w, pl, out, flags);
+    else
+      partial_sum_kernel<kPSE, kPSG><<<unsigned(ceil_div(pl.len, kPSE)), kPSE * kPSG, 0, s>>>(w, pl, out, flags);
     FAGP_LAUNCH_CHECK();
   }
   return FAGP_OK;
