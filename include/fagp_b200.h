@@ -297,6 +297,11 @@ int fagp_route_info(int64_t N, int64_t Ns, const fagp_basis* basis, int32_t* out
  * lines.  The staging step of fagp_posterior's host path for numpy inputs (posterior.py:267-318
  * takes numpy arrays); no device work. */
 int fagp_host_copy(void* dst, const void* src, size_t bytes, int32_t threads);
+/* 1 when [p, p + bytes) is pinned host memory the device can access at the same address (mapped
+ * under unified addressing), else 0: fagp_predict_x's mean / var may then point straight into it
+ * (zero-copy results: the kernel's stores cross PCIe as it runs, no D2H copy follows).  No device
+ * work. */
+int fagp_host_mapped(const void* p, size_t bytes);
 int fagp_host_copy_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
                       int32_t threads);
 /* Host staging of exactly the rows fagp_gram_x_upload_chunk(k) will copy: from the caller's

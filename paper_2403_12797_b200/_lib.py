@@ -81,6 +81,7 @@ SIGNATURES = {
     "fagp_predict_x_wave_rows": (_I64, [_BASIS]),
     "fagp_route_info": (ctypes.c_int, [_I64, _I64, _BASIS, _P]),
     "fagp_host_copy": (ctypes.c_int, [_P, _P, _SZ, _I32]),
+    "fagp_host_mapped": (ctypes.c_int, [_P, _SZ]),
     "fagp_host_copy_2d": (ctypes.c_int, [_P, _SZ, _P, _SZ, _SZ, _SZ, _I32]),
     "fagp_gram_x_stage_chunk": (ctypes.c_int, [_P, _P, _I64, _BASIS, _I32, _P, _P, _I32]),
     "fagp_predict_x_workspace_size": (_SZ, [_I64, _BASIS]),

@@ -142,3 +142,22 @@ extern "C" int fagp_host_copy(void* dst, const void* src, size_t bytes, int32_t 
   pool().run(int(nt), [&](int t) { stream_copy(d + cut(t), s + cut(t), cut(t + 1) - cut(t)); });
   return FAGP_OK;
 }
+
+// 1 when the device can write the host range [p, p + bytes) through the same address (pinned and
+// mapped: cudaHostAlloc'd memory under unified addressing), else 0.  No device work.
+extern "C" int fagp_host_mapped(const void* p, size_t bytes) {
+  if (p == nullptr) return 0;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  if (at.type != cudaMemoryTypeHost || at.devicePointer != p) return 0;
+  const char* last = static_cast<const char*>(p) + (bytes ? bytes - 1 : 0);
+  cudaPointerAttributes at2{};
+  if (cudaPointerGetAttributes(&at2, last) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return at2.type == cudaMemoryTypeHost && at2.devicePointer == last ? 1 : 0;
+}

@@ -449,9 +449,14 @@ class PosteriorEngine:
             self.set_mean_weights()
         rows = 2 if self.want_var else 1
         out, o = self._out_buffer(rows)
+        # zero-copy results: the predict kernels store mean / var straight into the pinned result
+        # buffer (mapped under unified addressing), so no D2H copy trails the last chunk and, with
+        # a pinned X*, no chunking is needed at all
+        zc = self.ZERO_COPY_OUT and self._mapped(out)
+        chunks = self._predict_chunks() if (not zc or xs_stage is not None) else [(0, self.Ns)]
         if trace is not None:
             trace.append(time.perf_counter())
-        for ci, (a, e) in enumerate(self._predict_chunks()):
+        for ci, (a, e) in enumerate(chunks):
             if xs_stage is not None and e > a:
                 _parallel_copy(xs_stage[a:e].numpy(), xs_src[a:e])
                 with torch.cuda.stream(self.s_in):
@@ -460,14 +465,17 @@ class PosteriorEngine:
                     evc.record(self.s_in)
                 mark(f"xs{ci}", self.s_in)
                 cs.wait_event(evc)
+            dm = out[0, a:e] if zc else self.mean[a:e]
+            dv = (out[1, a:e] if zc else self.var[a:e]) if self.want_var else None
             _lib.check(L.fagp_predict_x(_lib.ptr(Xs[a:e]), e - a, b.ref, _lib.ptr(self.predict_op), self.noise_var,
-                                        self.mean_const, _lib.ptr(self.mean[a:e]),
-                                        _lib.ptr(self.var[a:e] if self.want_var else None), self._flag(1),
+                                        self.mean_const, _lib.ptr(dm), _lib.ptr(dv), self._flag(1),
                                         _lib.ptr(self.pred_ws), self.pred_ws_bytes, _lib.stream_handle(cs)),
                        "predict")
             ev = torch.cuda.Event()
             ev.record(cs)
             mark(f"pred{ci}", cs)
+            if zc:
+                continue
             self.s_out.wait_event(ev)
             with torch.cuda.stream(self.s_out):
                 out[0, a:e].copy_(self.mean[a:e], non_blocking=True)
@@ -499,6 +507,16 @@ class PosteriorEngine:
             if self.want_var:
                 out[1].copy_(self.var)
         return o[0], (o[1] if self.want_var else None)
+
+    ZERO_COPY_OUT = True  # predict into the pinned result buffer when the device can map it
+
+    def _mapped(self, out):
+        """Whether the pinned result buffer is device-accessible at its own address (cached)."""
+        key = (out.data_ptr(), out.numel())
+        cache = self.__dict__.setdefault("_mapped_cache", {})
+        if key not in cache:
+            cache[key] = bool(_lib.lib().fagp_host_mapped(out.data_ptr(), out.numel() * out.element_size()))
+        return cache[key]
 
     def _predict_chunks(self):
         """Row ranges of the chunked predict, cut at whole waves of the fused predict (every chunk
