@@ -376,7 +376,17 @@ class PosteriorEngine:
         ready.zero_()
         self.s_in.wait_stream(cs)
         sin = _lib.stream_handle(self.s_in)
-        if self.pipelined_gram:
+        # zero-copy train rows: pinned (mapped) X / y are read by the Gram kernel itself across
+        # PCIe as it contracts (bitwise the device-resident launch), no upload chunks or ready words
+        zc_in = (self.ZERO_COPY_IN and self.pipelined_gram and not staged and self._mapped(Xh)
+                 and self._mapped(yh))
+        if zc_in:
+            _lib.check(L.fagp_gram_x(_lib.ptr(Xh), self.N, b.ref, _lib.ptr(yh), self.mean_const, _lib.ptr(self.packed),
+                                     _lib.ptr(self.gram_ws), self.gram_ws_bytes, self._flag(0),
+                                     _lib.stream_handle(cs)), "gram")
+            mark("gram", cs)
+            X, y = Xh, yh  # (error reports and retries read the rows where they are)
+        elif self.pipelined_gram:
             # the copy stream uploads chunk k and then sets ready word k (a stream-ordered 4-byte
             # H2D copy); ONE Gram launch waits on the words chunk by chunk.  The copies are
             # queued first, so nothing the host does after the launch can hold them back.
@@ -413,10 +423,15 @@ class PosteriorEngine:
                 mark(f"gram{k}", cs)
         xs_src = self._staging_source(Xsh_src, (self.Ns, p))
 
+        xs_read = Xs  # what the predict reads: the device copy, or a mapped pinned X* itself
+
         def upload_xs():
+            nonlocal xs_read
             xs_host = self._pinned(Xsh_src, "Xs", (self.Ns, p))
             with torch.cuda.stream(self.s_in):
-                if self.Ns:
+                if self.Ns and zc_in and self._mapped(xs_host):
+                    xs_read = xs_host  # zero-copy: the predict loads its rows across PCIe
+                elif self.Ns:
                     Xs.copy_(xs_host, non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(self.s_in)
@@ -426,6 +441,7 @@ class PosteriorEngine:
         # a pinned X* goes up right behind the train rows; a pageable one is staged on the host
         # after the factorisation is queued (the staging then overlaps the Gram tail and factor)
         ev_xs = upload_xs() if xs_src is None else None
+        Xs = xs_read
         if trace is not None:
             trace.append(time.perf_counter())
         self.stage_reduce()
@@ -509,9 +525,10 @@ class PosteriorEngine:
         return o[0], (o[1] if self.want_var else None)
 
     ZERO_COPY_OUT = True  # predict into the pinned result buffer when the device can map it
+    ZERO_COPY_IN = True  # Gram / predict read pinned (mapped) X, y, X* in place (fused routes)
 
     def _mapped(self, out):
-        """Whether the pinned result buffer is device-accessible at its own address (cached)."""
+        """Whether a pinned host tensor is device-accessible at its own address (cached)."""
         key = (out.data_ptr(), out.numel())
         cache = self.__dict__.setdefault("_mapped_cache", {})
         if key not in cache:
