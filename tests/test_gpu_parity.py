@@ -548,3 +548,34 @@ def test_dgemm_large_tile_matches_numpy(M, N, K, ta, tb):
     got = dev.to_host(dgemm(a, b, trans_a=bool(ta), trans_b=bool(tb), alpha=-0.5, beta=2.0, out=out))
     scale = np.abs(a).max() * np.abs(b).max() * K
     assert np.abs(got - ref).max() <= 1e-14 * scale
+
+
+@pytest.mark.parametrize("zc_in,zc_out", [(True, True), (False, True), (True, False), (False, False)])
+def test_host_path_zero_copy_is_bitwise_invariant(zc_in, zc_out, monkeypatch):
+    """Pinned X, y, X*: the kernels read them in place and store mean / var straight into the
+    pinned result buffer (zero-copy), or the copy pipelines run -- the same bits either way, equal
+    to the device-resident path."""
+    from paper_2403_12797_b200.engine import PosteriorEngine
+
+    rng = np.random.default_rng(8)
+    N, Ns = 120_007, 70_001
+    X = rng.uniform(-1, 1, (N, 3))
+    y = np.cos(X).sum(1) + 0.05 * rng.standard_normal(N)
+    Xs = rng.uniform(-1, 1, (Ns, 3))
+    model = F.GpModel(F.ArdKernelParams.isotropic(3, 1.0, 1.0), 0.0025, n_eigen=10)
+
+    class Dev:
+        pass
+
+    Dev.X, Dev.y = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    ref = F.fagp_posterior(Dev, torch.from_numpy(Xs).cuda(), model, memory_cap=None)
+    monkeypatch.setattr(PosteriorEngine, "ZERO_COPY_IN", zc_in)
+    monkeypatch.setattr(PosteriorEngine, "ZERO_COPY_OUT", zc_out)
+
+    class Host:
+        pass
+
+    Host.X, Host.y = torch.from_numpy(X).pin_memory(), torch.from_numpy(y).pin_memory()
+    for _ in range(2):  # a second call reuses the engine and its pooled result buffers
+        got = F.fagp_posterior(Host, torch.from_numpy(Xs).pin_memory(), model, memory_cap=None)
+        assert np.array_equal(got.mean, ref.mean) and np.array_equal(got.var, ref.var)
