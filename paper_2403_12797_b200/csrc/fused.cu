@@ -9,22 +9,24 @@
 //   mean_i   = c + sum_a w[a] prod_d phi_{d,a_d}(x*_i)                  (posterior.py:247)
 // What changes here is the B200 mapping:
 //
-//  * Producer/consumer CTAs.  Two producer warps evaluate the 1-D eigenfunctions of the next
-//    64-row block (mercer.py:122-143, 276-281, bit-faithful op order, eigfun.cuh) into a
-//    double-buffered shared-memory row slab while the consumer warps run the DMMA contraction
-//    on the current block; one __syncthreads per block flips the buffers.  Nothing but X (and
-//    y) is read from HBM: 24 B per row at p = 3 instead of the 752 B table row.
+//  * Production / contraction phases.  Every block of rows (128 rows, 256 in the split Gram) starts
+//    with a production phase in which all warps evaluate the 1-D eigenfunctions (one or two
+//    (row, dimension) items per thread; mercer.py:122-143, 276-281, bit-faithful op order,
+//    eigfun.cuh) into a shared-memory row slab, then all warps run the DMMA contraction over it.
+//    (A dedicated producer warp group overlapping the contraction was measured slower: its
+//    dependent FP64 recurrence chains starve behind the DMMAs in the shared FP64 pipe.)  Nothing
+//    but X (and y) is read from HBM: 24 B per row at p = 3 instead of the 752 B table row.
 //  * Register-generated DMMA fragments.  Every mma.m8n8k4.f64 operand that is a product of
 //    basis values (g g, phi phi, r phi) is formed in the thread that feeds it to the tensor
 //    core (FA/FB/FK LDS.64 + DMULs, conflict-free thanks to a row stride == 4 mod 16 doubles),
 //    so generated operands never round-trip through shared memory.
 //  * Gram: each CTA owns a contiguous row range and accumulates the WHOLE output ([K | t]:
-//    46 x 3 + 13 x 2 8x8 fragments at C3) in registers of 14 consumer warps; one CTA per SM,
+//    46 x 3 + 13 x 2 8x8 fragments at C3) in registers of its 16 warps; one CTA per SM,
 //    persistent; per-CTA partials are summed in a fixed order by a second small kernel
 //    (deterministic, no float atomics) -- the same buffer the multi-GPU path all-reduces.
 //  * Predict: the variance operand C'' and the mean weights are staged once per CTA into
-//    shared memory in fragment-major order (one conflict-free LDS.64 per B fragment); 8
-//    consumer warps = 4 row groups x 2 K-halves (split-K reduced through shared memory);
+//    shared memory in fragment-major order (one conflict-free LDS.64 per B fragment); 16
+//    warps = 8 row groups (16 rows each) x 2 K-halves (split-K reduced through shared memory);
 //    the g / phi epilogue products and the 4-lane row reductions stay in registers; mean and
 //    variance come out of the same pass.
 // Shapes whose output does not fit these layouts use the tiled table kernels (modal.cu,
