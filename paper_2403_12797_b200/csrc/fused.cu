@@ -1410,7 +1410,7 @@ fused_predict_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView b, con
 //   mean2: A = (phi0[8, M), phi2)     x B = w[8 + a0'][a1][a2] over a1            epilogue phi1[a1]
 // (19% fewer DMMA at C3).  Same blocks, production, warp split and reduction as
 // fused_predict_kernel.
-template <int BW, int MM = 0>
+template <int BW, int MM = 0, int G = 1>
 __global__ void __launch_bounds__(kPredNT, 1)
 fused_predict_split_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView b, const VPlan pl,
                            const double* __restrict__ op, double sigma2, double c, double* __restrict__ mean,
@@ -1433,6 +1433,17 @@ fused_predict_split_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView 
   uint32_t* offM1 = offV2 + vk2 * 4;
   uint32_t* offM2 = offM1 + mk1 * 4;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // G independent warp groups (G = 2: two 8-warp halves on alternating 64-row blocks, one group's
+  // production and epilogue overlapping the other's DMMA phase); each group has its own slab,
+  // reduction buffer and named barrier
+  constexpr int WG = kPredW / G, RB = kPR / G, GT = WG * 32;
+  const int gid = warp / WG, gw = warp % WG, gt = tid % GT;
+  auto gsync = [&]() {
+    if constexpr (G == 1)
+      __syncthreads();
+    else
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + gid), "r"(GT) : "memory");
+  };
   const double* w = op + pl.KP * pl.NP;
   const int64_t KM = int64_t(M) * M;
   auto pack2 = [&](int o0, int o1) { return uint32_t(o0) | (uint32_t(o1) << 8); };
@@ -1465,16 +1476,19 @@ fused_predict_split_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView 
   for (int k = tid; k < mk2 * 4; k += kPredNT)
     offM2[k] = k < R2 * M ? pack2(rl.poff + 8 + k / M, rl.poff + 2 * M + k % M) : pack2(rl.zero, rl.one);
   bool bad_x = false, bad = false;
-  const bool plane = tid < kPR * P;
-  const int prow = tid / P, pdim = tid - (tid / P) * P;
+  const bool plane = gt < RB * P;
+  const int prow = gt / P, pdim = gt - (gt / P) * P;
+  const int64_t nb = (Ns + RB - 1) / RB;
+  double* const gslab = slab + gid * RB * rl.bw;
+  double* const gred = red + gid * kPKS * RB * 2;
   auto load_x = [&](int64_t blk) -> double {
-    const int64_t r = blk * kPR + prow;
-    return (plane && blk < pl.nblocks && r < Ns) ? Xs[r * P + pdim] : 0.0;
+    const int64_t r = blk * RB + prow;
+    return (plane && blk < nb && r < Ns) ? Xs[r * P + pdim] : 0.0;
   };
   auto produce = [&](double x, int64_t blk) {
     if (!plane) return;
-    double* row = slab + prow * rl.bw;
-    if (blk * kPR + prow < Ns) {
+    double* row = gslab + prow * rl.bw;
+    if (blk * RB + prow < Ns) {
       bad_x |= not_finite(x);
       eval_phi_g_dim_u(x, 0.0, b, pdim, pl.hc, row + rl.poff + pdim * M, row + rl.goff + pdim * L, nullptr);
     } else {
@@ -1486,9 +1500,9 @@ fused_predict_split_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView 
       row[rl.zero] = 0.0;
     }
   };
-  const int64_t blk0 = blockIdx.x, stride = gridDim.x;
+  const int64_t blk0 = int64_t(blockIdx.x) * G + gid, stride = int64_t(gridDim.x) * G;
   double xn = load_x(blk0);
-  const int mg = warp % (kPredW / kPKS), kq = warp / (kPredW / kPKS);
+  const int mg = gw % (WG / kPKS), kq = gw / (WG / kPKS);
   auto half = [&](int n, int q) { return q * n / kPKS; };
   // epilogue offsets: var1 g0[nu < 16], var2 g1[k1 < L], mean1 phi0[a0 < 8], mean2 phi1[a1 < M]
   int oE1[2][2], oE2[3][2], oM1[1][2], oM2[2][2];
@@ -1504,12 +1518,22 @@ fused_predict_split_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView 
     for (int nf = 0; nf < 2; ++nf) oM2[nf][e] = nf * 8 + cc < M ? rl.poff + M + nf * 8 + cc : rl.zero;
   }
   __syncthreads();
+  // stagger: group 1 starts producing once group 0 has produced its first block, so the groups'
+  // DMMA phases are offset by a production phase from the start
+  bool staggered = G == 1 || gid == 1;
+  if constexpr (G == 2)
+    if (gid == 1) asm volatile("bar.sync 3, %0;" ::"r"(kPredNT) : "memory");
 
-  for (int64_t blk = blk0; blk < pl.nblocks; blk += stride) {
+  for (int64_t blk = blk0; blk < nb; blk += stride) {
     produce(xn, blk);
     xn = load_x(blk + stride);
-    __syncthreads();
-    const double* row0 = slab + (mg * 16 + (lane >> 2)) * rl.bw;
+    gsync();
+    if constexpr (G == 2)
+      if (!staggered) {
+        asm volatile("bar.arrive 3, %0;" ::"r"(kPredNT) : "memory");
+        staggered = true;
+      }
+    const double* row0 = gslab + (mg * 16 + (lane >> 2)) * rl.bw;
     double aV1[kPMF][2][2], aV2[kPMF][3][2], aM1[kPMF][1][2], aM2[kPMF][2][2];
 #pragma unroll
     for (int f = 0; f < kPMF; ++f)
@@ -1567,19 +1591,19 @@ fused_predict_split_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView 
       ms += __shfl_xor_sync(0xffffffffu, ms, 2);
       if ((lane & 3) == 0) {
         const int r = mg * 16 + 8 * f + (lane >> 2);
-        red[(kq * kPR + r) * 2 + 0] = vs;
-        red[(kq * kPR + r) * 2 + 1] = ms;
+        gred[(kq * RB + r) * 2 + 0] = vs;
+        gred[(kq * RB + r) * 2 + 1] = ms;
       }
     }
-    __syncthreads();
-    if (tid < kPR) {
-      const int64_t row_i = blk * kPR + tid;
+    gsync();
+    if (gt < RB) {
+      const int64_t row_i = blk * RB + gt;
       if (row_i < Ns) {
-        double vs = red[tid * 2], ms = red[tid * 2 + 1];
+        double vs = gred[gt * 2], ms = gred[gt * 2 + 1];
 #pragma unroll
         for (int q = 1; q < kPKS; ++q) {
-          vs += red[(q * kPR + tid) * 2];
-          ms += red[(q * kPR + tid) * 2 + 1];
+          vs += gred[(q * RB + gt) * 2];
+          ms += gred[(q * RB + gt) * 2 + 1];
         }
         const double mm = c + ms;  // posterior.py:247
         mean[row_i] = mm;
@@ -1592,6 +1616,8 @@ fused_predict_split_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView 
       }
     }
   }
+  if constexpr (G == 2)
+    if (!staggered) asm volatile("bar.arrive 3, %0;" ::"r"(kPredNT) : "memory");  // group 0 had no block
   if (bad_x) raise_flag(flags, FAGP_FLAG_X_NONFINITE);
   if (bad) raise_flag(flags, FAGP_FLAG_PHI_NONFINITE);
 }
@@ -1678,11 +1704,16 @@ int predict(const double* Xs, int64_t Ns, const fagp_basis* b, const double* op,
       FAGP_LAUNCH_CHECK();
       return FAGP_OK;
     };
+    const char* sg = getenv("FAGP_PREDICT_GROUPS");
+    const bool g2 = !(sg && sg[0] == '1');
     switch (row_layout(3, b->M).bw) {  // compile-time row strides (M 9, 10: 100; 11: 116; 12: 132)
       // M as a template argument: compile-time section bounds (0.82 -> 0.76 ms at C3)
-      case 100: return b->M == 10 ? go(fused_predict_split_kernel<100, 10>) : go(fused_predict_split_kernel<100, 9>);
-      case 116: return go(fused_predict_split_kernel<116, 11>);
-      case 132: return go(fused_predict_split_kernel<132, 12>);
+      case 100:
+        if (b->M == 10)
+          return g2 ? go(fused_predict_split_kernel<100, 10, 2>) : go(fused_predict_split_kernel<100, 10, 1>);
+        return g2 ? go(fused_predict_split_kernel<100, 9, 2>) : go(fused_predict_split_kernel<100, 9, 1>);
+      case 116: return g2 ? go(fused_predict_split_kernel<116, 11, 2>) : go(fused_predict_split_kernel<116, 11, 1>);
+      case 132: return g2 ? go(fused_predict_split_kernel<132, 12, 2>) : go(fused_predict_split_kernel<132, 12, 1>);
       default: return FAGP_EUNSUPPORTED;
     }
   }
