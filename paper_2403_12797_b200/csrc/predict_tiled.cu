@@ -148,7 +148,7 @@ static bool make_pplan(int64_t Ns, int p, int M, PPlan& pl) {
 }
 
 static size_t smem_bytes(const PPlan& pl) {
-  return (size_t(kMaxKS) * kTN * 32 + size_t(kBR + 1) * pl.bw + size_t(kBR) * pl.p + 2 * 4 * kBR) * sizeof(double) +
+  return (size_t(kMaxKS) * kTN * 32 + size_t(kBR + 2) * pl.bw + size_t(kBR) * pl.p + 2 * 4 * kBR) * sizeof(double) +
          size_t(kMaxKS) * 4 * sizeof(uint32_t);
 }
 
@@ -185,18 +185,32 @@ __device__ __forceinline__ double prod_pk(const double* row, uint32_t pk) {
   return v;
 }
 
-template <int FA, int FB, int BW>
+// G independent warp groups: G = 2 runs two 8-warp halves (2 row groups x 4 column groups each) on
+// alternating 32-row blocks of the CTA's rows, each with its own slab, staging and reduction
+// buffers and named barrier, so one group's production and epilogue overlap the other's DMMAs.
+template <int FA, int FB, int BW, int G = 1>
 __global__ void __launch_bounds__(kNT, 1)
 tiled_predict_kernel(const double* __restrict__ Xs, BasisView b, const __grid_constant__ PPlan pl,
                      const double* __restrict__ op, double* __restrict__ part, uint32_t* flags) {
   extern __shared__ double sm[];
   const int bw = BW ? BW : pl.bw;
+  constexpr int GT = kNT / G, RB = kBR / G, NRG = 4 / G;  // threads, rows, row groups per group
   double* Bt = sm;                              // [kMaxKS][kTN][32] fragment-major operand slice
-  double* slab = Bt + kMaxKS * kTN * 32;        // [(kBR + 1) * bw]
-  double* xs = slab + (kBR + 1) * bw;           // [kBR p] staged x of the next block
-  double* red = xs + kBR * pl.p;                // [4][kBR] column-group partials, double buffered x2
-  uint32_t* offA = reinterpret_cast<uint32_t*>(red + 2 * 4 * kBR);  // [kMaxKS * 4]
+  double* slab0 = Bt + kMaxKS * kTN * 32;       // [G][(RB + 1) * bw]
+  double* xs0 = slab0 + (kBR + 2) * bw;         // [G][RB p] staged x of the group's next block
+  double* red0 = xs0 + kBR * pl.p;              // [G][2][4][RB] column-group partials, double buffered
+  uint32_t* offA = reinterpret_cast<uint32_t*>(red0 + 2 * 4 * kBR);  // [kMaxKS * 4]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = warp / (kW / G), gw = warp % (kW / G), gt = tid % GT;
+  double* const slab = slab0 + gid * (RB + 1) * bw;
+  double* const xs = xs0 + gid * RB * pl.p;
+  double* const red = red0 + gid * 2 * 4 * RB;
+  auto gsync = [&]() {
+    if constexpr (G == 1)
+      __syncthreads();
+    else
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + gid), "r"(GT) : "memory");
+  };
   const int p = pl.p, M = pl.M, L = pl.L;
   const int cta = int(blockIdx.x);
   int T = 0;
@@ -231,7 +245,9 @@ tiled_predict_kernel(const double* __restrict__ Xs, BasisView b, const __grid_co
     offA[i] = pack_offs<FA>(i < tl.nka ? kA : nA, nA, 0, R, sec, pl);
   }
   // B-side offsets of this thread's epilogue columns: n-fragment cg * 4 + j, column 2 (lane & 3) + e
-  const int rg = warp & 3, cg = warp >> 2;  // SMSP = warp % 4 = row group: one warp of each column group per SMSP
+  // G = 1: SMSP = warp % 4 = row group, one warp of each column group per SMSP; G = 2: each SMSP
+  // holds two warps of each group
+  const int rg = gw % NRG, cg = gw / NRG;
   uint32_t offB[kCF][2];
 #pragma unroll
   for (int j = 0; j < kCF; ++j)
@@ -248,15 +264,15 @@ tiled_predict_kernel(const double* __restrict__ Xs, BasisView b, const __grid_co
   bool pon[2];
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
-    const int it = tid + u * kNT;
-    pon[u] = it < kBR * p;
-    prow[u] = pon[u] ? it / p : kBR;
+    const int it = gt + u * GT;
+    pon[u] = it < RB * p;
+    prow[u] = pon[u] ? it / p : RB;
     pdim[u] = pon[u] ? it - (it / p) * p : 0;
   }
   bool bad_x = false;
   auto load = [&](int64_t base) {
-    const int64_t nr = tmin<int64_t>(kBR, r1 - base);
-    for (int e = tid; e < kBR * p; e += kNT) {
+    const int64_t nr = tmin<int64_t>(RB, r1 - base);
+    for (int e = gt; e < RB * p; e += GT) {
       const bool ok = e < nr * p;
       cp_async_8z(xs + e, ok ? Xs + base * p + e : Xs, ok);
     }
@@ -264,7 +280,7 @@ tiled_predict_kernel(const double* __restrict__ Xs, BasisView b, const __grid_co
   };
   auto produce = [&](int64_t base) {
     cp_async_wait<0>();
-    __syncthreads();
+    gsync();
 #pragma unroll 1
     for (int u = 0; u < 2; ++u) {
       if (!pon[u]) continue;
@@ -280,13 +296,23 @@ tiled_predict_kernel(const double* __restrict__ Xs, BasisView b, const __grid_co
     }
   };
 
-  const int64_t nblk = ceil_div(tmax<int64_t>(0, r1 - r0), kBR);
-  if (nblk > 0) load(r0);
-  for (int64_t n = 0; n < nblk; ++n) {
-    const int64_t base = r0 + n * kBR;
+  const int64_t nblk = ceil_div(tmax<int64_t>(0, r1 - r0), RB);
+  if (gid < nblk) load(r0 + gid * RB);
+  // stagger (G = 2): group 1 starts once group 0 has produced its first block
+  bool staggered = G == 1 || gid == 1;
+  if constexpr (G == 2)
+    if (gid == 1) asm volatile("bar.sync 3, %0;" ::"r"(kNT) : "memory");
+  int it = 0;
+  for (int64_t n = gid; n < nblk; n += G, ++it) {
+    const int64_t base = r0 + n * RB;
     produce(base);
-    __syncthreads();  // slab complete, staging free
-    if (n + 1 < nblk) load(base + kBR);
+    gsync();  // slab complete, staging free
+    if constexpr (G == 2)
+      if (!staggered) {
+        asm volatile("bar.arrive 3, %0;" ::"r"(kNT) : "memory");
+        staggered = true;
+      }
+    if (n + G < nblk) load(base + G * RB);
     double s[kRF] = {0.0, 0.0};
     if (active) {
       double acc[kRF][kCF][2];
@@ -325,16 +351,18 @@ tiled_predict_kernel(const double* __restrict__ Xs, BasisView b, const __grid_co
       s[f] += __shfl_xor_sync(0xffffffffu, s[f], 1);
       s[f] += __shfl_xor_sync(0xffffffffu, s[f], 2);
     }
-    double* rb = red + (n & 1) * 4 * kBR;
+    double* rb = red + (it & 1) * 4 * RB;
     if ((lane & 3) == 0)
 #pragma unroll
-      for (int f = 0; f < kRF; ++f) rb[cg * kBR + rg * 16 + 8 * f + (lane >> 2)] = s[f];
-    __syncthreads();
-    if (tid < kBR && base + tid < r1) {
-      const double v = ((rb[tid] + rb[kBR + tid]) + rb[2 * kBR + tid]) + rb[3 * kBR + tid];
-      part[int64_t(T) * pl.Ns + base + tid] = v;
+      for (int f = 0; f < kRF; ++f) rb[cg * RB + rg * 16 + 8 * f + (lane >> 2)] = s[f];
+    gsync();
+    if (gt < RB && base + gt < r1) {
+      const double v = ((rb[gt] + rb[RB + gt]) + rb[2 * RB + gt]) + rb[3 * RB + gt];
+      part[int64_t(T) * pl.Ns + base + gt] = v;
     }
   }
+  if constexpr (G == 2)
+    if (!staggered) asm volatile("bar.arrive 3, %0;" ::"r"(kNT) : "memory");  // group 0 had no block
   if (bad_x) raise_flag(flags, FAGP_FLAG_X_NONFINITE);
 }
 
@@ -375,9 +403,13 @@ template <int FA, int FB, int BW>
 static int launch_bw(const double* Xs, const fagp_basis* b, const PPlan& pl, const double* op, double* part,
                      uint32_t* flags, cudaStream_t s) {
   const size_t smem = smem_bytes(pl);
-  FAGP_CUDA_TRY(cudaFuncSetAttribute(tiled_predict_kernel<FA, FB, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(smem)));
-  tiled_predict_kernel<FA, FB, BW><<<pl.grid, kNT, smem, s>>>(Xs, view(b), pl, op, part, flags);
+  const char* sg = getenv("FAGP_PREDICT_GROUPS");
+  // two groups where the epilogue is light (FB <= 2: C4 5.26 -> 5.10 ms); at FB = 3 (C5) the
+  // 32-row blocks' heavier epilogue and production cost more than the overlap buys (32.6 -> 34.3 ms)
+  const bool g2 = FB <= 2 && !(sg && sg[0] == '1');
+  auto kern = g2 ? tiled_predict_kernel<FA, FB, BW, 2> : tiled_predict_kernel<FA, FB, BW, 1>;
+  FAGP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  kern<<<pl.grid, kNT, smem, s>>>(Xs, view(b), pl, op, part, flags);
   FAGP_LAUNCH_CHECK();
   return FAGP_OK;
 }
