@@ -1,6 +1,7 @@
 """Event-timed fagp_predict_x (the hot predict entry) at BASELINE configs: ms per launch and the
 fraction of the measured FP64 DMMA peak on the modal flop count.   python tools/predict_time.py c3"""
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -26,7 +27,10 @@ for name in sys.argv[1:] or ["c3"]:
         predict_x_device(f, Xs)
     torch.cuda.synchronize()
     ts = []
-    for _ in range(5):
+    flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device="cuda") if os.environ.get("PT_FLUSH") else None
+    for k in range(5):
+        if flush is not None:  # PT_FLUSH=1: evict L2 (256 MiB write) between launches, as bench.py does
+            flush.fill_(float(k))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         predict_x_device(f, Xs)
@@ -34,6 +38,7 @@ for name in sys.argv[1:] or ["c3"]:
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     ms = min(ts)
+    mean_ms = sum(ts) / len(ts)
     L = 2 * M - 1
     fl = 2 * Ns * (L**p + M**p)
-    print(f"{name}: predict_x {ms:.3f} ms  {fl / ms / 1e9:.2f} TF/s  frac {fl / ms / 1e9 / PEAK:.3f}", flush=True)
+    print(f"{name}: predict_x {ms:.3f} ms  {fl / ms / 1e9:.2f} TF/s  frac {fl / ms / 1e9 / PEAK:.3f}  (mean {mean_ms:.3f} ms)", flush=True)
