@@ -1187,15 +1187,15 @@ __device__ __forceinline__ void contract(const double* row0, int bw_rt, const ui
 
 // contract() with compile-time k-step bounds: a plain loop the compiler unrolls and schedules
 // itself (loads of later k-steps hoisted over earlier DMMAs), as in the Gram's k-loop.
-#ifndef FAGP_PRED_UNROLL
-#define FAGP_PRED_UNROLL 64  // (measured: 8 -> 0.750 ms, 4 / 16 -> 0.743, 64 = full -> 0.735 at C3)
-#endif
-#define FAGP_PRAGMA_(x) _Pragma(#x)
-#define FAGP_UNROLL_(n) FAGP_PRAGMA_(unroll n)
-template <int F, int NF, int BW, int K0, int K1>
+// UNR: the k-loop unroll.  One lockstep CTA: full (measured: 8 -> 0.750 ms, 4 / 16 -> 0.743, 64 =
+// full -> 0.735 at C3).  Two warp groups: 16 -- the groups run different phases at once, so the
+// fully unrolled kernel (97 KB of SASS) keeps its production and both contraction halves hot
+// together and, behind the Gram's code in the step, runs out of the SM's instruction cache (0.720
+// ms in the step, 0.682 alone; unroll 16: 0.682 in the step, profiles/predict_groups_r06.txt)
+template <int F, int NF, int BW, int K0, int K1, int UNR>
 __device__ __forceinline__ void contract_ct(const double* row0, const uint32_t* offs, const double* B, int lane,
                                             double (&acc)[kPMF][NF][2]) {
-  FAGP_UNROLL_(FAGP_PRED_UNROLL)
+#pragma unroll UNR
   for (int ks = K0; ks < K1; ++ks) {
     int off[F];
     unpack_off<F>(offs[4 * ks + (lane & 3)], off);
@@ -1548,14 +1548,19 @@ fused_predict_split_kernel(const double* __restrict__ Xs, int64_t Ns, BasisView 
       constexpr int cvk1 = (cL * cL + 3) / 4, cvk2 = (cR * cL + 3) / 4, cmk1 = (MM * MM + 3) / 4,
                     cmk2 = (cR2 * MM + 3) / 4;
       static_assert(kPKS == 2, "two K halves");
+#ifdef FAGP_PRED_UNROLL
+      constexpr int UNR = FAGP_PRED_UNROLL;
+#else
+      constexpr int UNR = G == 1 ? 64 : 16;
+#endif
       auto sections = [&](auto q) {
         constexpr int Q = decltype(q)::value;
         if (want_var) {
-          contract_ct<2, 2, BW, Q * cvk1 / 2, (Q + 1) * cvk1 / 2>(row0, offV1, Bv1, lane, aV1);
-          contract_ct<2, 3, BW, Q * cvk2 / 2, (Q + 1) * cvk2 / 2>(row0, offV2, Bv2, lane, aV2);
+          contract_ct<2, 2, BW, Q * cvk1 / 2, (Q + 1) * cvk1 / 2, UNR>(row0, offV1, Bv1, lane, aV1);
+          contract_ct<2, 3, BW, Q * cvk2 / 2, (Q + 1) * cvk2 / 2, UNR>(row0, offV2, Bv2, lane, aV2);
         }
-        contract_ct<2, 1, BW, Q * cmk1 / 2, (Q + 1) * cmk1 / 2>(row0, offM1, Bm1, lane, aM1);
-        contract_ct<2, 2, BW, Q * cmk2 / 2, (Q + 1) * cmk2 / 2>(row0, offM2, Bm2, lane, aM2);
+        contract_ct<2, 1, BW, Q * cmk1 / 2, (Q + 1) * cmk1 / 2, UNR>(row0, offM1, Bm1, lane, aM1);
+        contract_ct<2, 2, BW, Q * cmk2 / 2, (Q + 1) * cmk2 / 2, UNR>(row0, offM2, Bm2, lane, aM2);
       };
       if (kq == 0)
         sections(std::integral_constant<int, 0>{});
