@@ -407,6 +407,10 @@ fused_gram_kernel(const double* __restrict__ X, const double* __restrict__ y, do
 // role's warp count), 9 DMMA per warp per k-step each.  Production, blocks, sub-ranges and the
 // partial flush are those of fused_gram_kernel.
 constexpr int kSplitGramBW = 100;  // row_layout(3, 10).bw
+#ifndef FAGP_GRAM_UNROLL
+#define FAGP_GRAM_UNROLL 8  // split Gram k-loop unroll per 64-k-step block (measured 4 / 8 / 16 / 32: 0.689 / 0.679 / 0.687 / 0.712 ms at C3: the 5 warp classes run different straight-line k-steps at once, so longer unrolls spill out of the instruction cache)
+#endif
+constexpr int kGramUnroll = FAGP_GRAM_UNROLL;
 template <int JK1, int JT1A, int JK2, int JT2, int JT1B, int BR>
 __global__ void __launch_bounds__(kGramNT, 1)
 fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__ y, double c, int64_t N,
@@ -663,7 +667,7 @@ fused_gram_split_kernel(const double* __restrict__ X, const double* __restrict__
   using IT1B = std::integral_constant<int, JT1B>;
   auto kloop = [&](const double* cur, int nks, auto body) {
     if (nks == BR / 4) {
-#pragma unroll 16
+#pragma unroll kGramUnroll
       for (int i = 0; i < BR / 4; ++i) body(cur, i);
     } else {
       for (int i = 0; i < nks; ++i) body(cur, i);
