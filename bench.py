@@ -48,7 +48,8 @@ CONFIGS = {
 METRIC = "posterior mean+var samples/s (N=1e6, p=3, M=10); % FP64 tensor peak"
 NOISE_VAR = 0.0025
 FP64_PEAK_FILE = ROOT / "profiles" / "fp64_peak_r01.json"
-NCU_SUMMARY_FILES = (ROOT / "profiles" / "ncu_summary_r05.json", ROOT / "profiles" / "ncu_summary_r04s.json",
+NCU_SUMMARY_FILES = (ROOT / "profiles" / "ncu_summary_r06n.json", ROOT / "profiles" / "ncu_summary_r05.json",
+                     ROOT / "profiles" / "ncu_summary_r04s.json",
                      ROOT / "profiles" / "ncu_summary_r04s_c4tiled.json")
 
 
