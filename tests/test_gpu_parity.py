@@ -579,3 +579,33 @@ def test_host_path_zero_copy_is_bitwise_invariant(zc_in, zc_out, monkeypatch):
     for _ in range(2):  # a second call reuses the engine and its pooled result buffers
         got = F.fagp_posterior(Host, torch.from_numpy(Xs).pin_memory(), model, memory_cap=None)
         assert np.array_equal(got.mean, ref.mean) and np.array_equal(got.var, ref.var)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p,M,Ns", [(3, 10, 1), (3, 10, 63), (3, 10, 64), (3, 10, 65), (3, 10, 129), (3, 10, 3000),
+                                    (3, 10, 148 * 128 + 5), (3, 9, 777), (3, 11, 4097), (3, 12, 200),
+                                    # tiled predict: two groups where FB <= 2 (p = 4), one at p = 5
+                                    (4, 8, 1), (4, 8, 33), (4, 8, 70_001), (5, 6, 2001)])
+def test_predict_groups_bitwise(p, M, Ns, monkeypatch):
+    """The two-warp-group predict kernels (split predict: 64-row blocks per group, named barriers,
+    staggered start; tiled predict: 32-row blocks per group) against the one-group CTA, bitwise:
+    each row's partial sums run the same k-steps in the same order.  Covers groups without a
+    block (N* < 64, the last CTA's second group), one-CTA grids and ragged last blocks."""
+    from paper_2403_12797_b200.posterior import gram_x_packed, predict_x_device
+
+    rng = np.random.default_rng(11 * p + M)
+    N = 3000
+    X = rng.uniform(-1, 1, (N, p))
+    y = np.cos(X).sum(1) + 0.05 * rng.standard_normal(N)
+    Xs = rng.uniform(-1.5, 1.5, (Ns, p))
+    basis = F.Basis(F.ArdKernelParams.isotropic(p, 1.0, 1.0), M)
+    Xd, yd, Xsd = dev.to_device(X), dev.to_device(y), dev.to_device(Xs)
+    f, st, _ = factor_packed(basis, gram_x_packed(basis, Xd, yd, 0.1), 0.0025, 0.1, N)
+    assert st == 0
+    out = {}
+    for g in ("1", "2"):
+        monkeypatch.setenv("FAGP_PREDICT_GROUPS", g)
+        out[g] = [dev.to_host(a) for a in predict_x_device(f, Xsd)]
+    for a, b in zip(out["1"], out["2"]):
+        assert np.array_equal(a, b)
+    assert np.all(np.isfinite(out["2"][0])) and np.all(out["2"][1] >= -1e-12)
