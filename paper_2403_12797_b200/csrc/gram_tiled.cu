@@ -41,6 +41,11 @@
 namespace fagp {
 namespace tiled {
 
+#ifndef FAGP_TILED_UNROLL
+#define FAGP_TILED_UNROLL 4
+#endif
+constexpr int kTiledUnroll = FAGP_TILED_UNROLL;  // k-loop unroll of the full-fragment path
+
 constexpr int kW = 16, kNT = kW * 32;  // 16 warps
 constexpr int kTF = 16;                // fragments per tile side
 constexpr int kWF = 4;                 // fragments per warp side
@@ -389,7 +394,7 @@ __device__ __forceinline__ void tile_body(const double* __restrict__ X, const do
     const int nks = int((tmin<int64_t>(BR, r1 - base) + 3) / 4);
     if (nva > 0 && nvb > 0) {
       if (full) {
-#pragma unroll 4
+#pragma unroll kTiledUnroll
         for (int i = 0; i < nks; ++i) {
           Ops o;
           ops(i, o);
