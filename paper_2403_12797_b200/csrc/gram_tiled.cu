@@ -75,8 +75,32 @@ struct TPlan {
   int64_t N;
   Tile tiles[kMaxTiles];
   int first[kMaxTiles], cnt[kMaxTiles];  // CTAs [first, first + cnt) work on tile t
+  int sbase[kMaxTiles];                  // tile t's partials: slots [sbase, sbase + cnt)
+  // span = 1: the CTAs cut the tiles' total work (cost x rows, tile-major) evenly, so a CTA may
+  // finish one tile and start the next (two partial slots); span = 0: whole CTAs per tile, rows
+  // split evenly over a tile's CTAs
+  int span;
+  int wcost[kMaxTiles];                  // per-row cost of tile t (tile_cost)
+  int64_t wstart[kMaxTiles + 1];         // work before tile t (wcost x N, prefix sums)
+  int nslots;
   HermCoef hc;
 };
+
+// (tile, first row) at work position w of a spanning plan, rows rounded down to whole k-steps;
+// the same integer arithmetic on the host (slot layout) and in the kernel (row ranges)
+__host__ __device__ __forceinline__ void span_pos(const TPlan& pl, int64_t w, int& t, int64_t& row) {
+  if (w >= pl.wstart[pl.ntiles]) {
+    t = pl.ntiles - 1;
+    row = pl.N;
+    return;
+  }
+  t = 0;
+  while (t + 1 < pl.ntiles && pl.wstart[t + 1] <= w) ++t;
+  row = ((w - pl.wstart[t]) / pl.wcost[t]) & ~int64_t(3);
+}
+__host__ __device__ __forceinline__ int64_t span_bound(const TPlan& pl, int i) {
+  return pl.wstart[pl.ntiles] / pl.grid * i + pl.wstart[pl.ntiles] % pl.grid * i / pl.grid;
+}
 
 static int64_t ipow(int64_t b, int e) {
   int64_t r = 1;
@@ -189,9 +213,60 @@ static bool make_tplan(int64_t N, int p, int M, TPlan& pl) {
   int f = 0;
   for (int t = 0; t < pl.ntiles; ++t) {
     pl.first[t] = f;
+    pl.sbase[t] = f;
     f += pl.cnt[t];
   }
   pl.grid = f;
+  pl.nslots = f;
+  // whole CTAs per tile leave the makespan at cost x rows / min count (C5: 11 equal tiles on 148
+  // SMs -> 13 or 14 CTAs per tile, the 13-CTA tiles 7% longer); large N spans the tiles instead
+  // (measured: C5 121.0 -> 119.8 ms; C4, whose deal is within 0.3% of even, 20.27 -> 20.43 ms, so
+  // only a deal more than 2% off even spans)
+  double mk = 0.0, tot = 0.0;
+  for (int t = 0; t < pl.ntiles; ++t) {
+    const double ct = tile_cost(pl.tiles[t].na, pl.tiles[t].nb);
+    mk = ct / pl.cnt[t] > mk ? ct / pl.cnt[t] : mk;
+    tot += ct;
+  }
+  const char* se = getenv("FAGP_TILED_SPAN");
+  pl.span = pl.ntiles < G && N >= 4096 && mk * G > 1.02 * tot;
+  if (se) pl.span = pl.ntiles < G && N >= 4096 && se[0] != '0';  // A/B knob: force either deal
+  if (pl.span) {
+    const TPlan whole = pl;  // the whole-CTA deal, kept if the spanning one is not well formed
+    pl.grid = G;
+    pl.wstart[0] = 0;
+    for (int t = 0; t < pl.ntiles; ++t) {
+      pl.wcost[t] = tile_cost(pl.tiles[t].na, pl.tiles[t].nb);
+      pl.wstart[t + 1] = pl.wstart[t] + int64_t(pl.wcost[t]) * N;
+      pl.first[t] = -1;
+      pl.cnt[t] = 0;
+    }
+    int slots = 0;
+    for (int i = 0; i < G; ++i) {
+      int ts, te;
+      int64_t rs, re;
+      span_pos(pl, span_bound(pl, i), ts, rs);
+      span_pos(pl, span_bound(pl, i + 1), te, re);
+      for (int t = ts; t <= te; ++t) {
+        const int64_t r0 = t == ts ? rs : 0, r1 = t == te ? re : N;
+        if (r0 >= r1) continue;
+        if (pl.first[t] < 0) {
+          pl.first[t] = i;
+          pl.sbase[t] = slots;
+        }
+        if (pl.first[t] + pl.cnt[t] != i) pl.span = 0;  // contributors must be consecutive CTAs
+        ++pl.cnt[t];
+        ++slots;
+      }
+    }
+    for (int t = 0; t < pl.ntiles; ++t)
+      if (pl.cnt[t] == 0) pl.span = 0;
+    pl.nslots = slots;
+    if (!pl.span) {
+      pl = whole;
+      pl.span = 0;
+    }
+  }
   pl.hc = herm_coef_host();
   if (const char* e = getenv("FAGP_TILED_MASKED")) pl.masked = atoi(e);  // A/B knob
   return true;
@@ -447,14 +522,31 @@ tiled_gram_kernel(const double* __restrict__ X, const double* __restrict__ y, do
                   const __grid_constant__ TPlan pl, double* __restrict__ ws, uint32_t* flags) {
   extern __shared__ double slab[];  // [(BR + 1) * bw] row slab | [BR p] x | [BR] y staging
   const int cta = int(blockIdx.x);
-  int T = 0;
-  while (T + 1 < pl.ntiles && cta >= pl.first[T + 1]) ++T;
-  const int j = cta - pl.first[T], cnt = pl.cnt[T];
-  const int64_t per = round_up(ceil_div(tmax<int64_t>(pl.N, 1), cnt), 4);
-  const int64_t r0 = tmin<int64_t>(pl.N, int64_t(j) * per), r1 = tmin<int64_t>(pl.N, r0 + per);
   bool bad_x = false;
-  tile_body<FA, FB, JT, BW>(X, y, c, b, pl, T, r0, r1, ws + int64_t(cta) * kPartial, slab, bad_x);
-  if (pl.prof && threadIdx.x == 0) pl.prof[5 * cta] = T;
+  if (pl.span) {  // this CTA's share of the tile-major work: one or two (tile, row range) segments
+    int ts, te;
+    int64_t rs, re;
+    span_pos(pl, span_bound(pl, cta), ts, rs);
+    span_pos(pl, span_bound(pl, cta + 1), te, re);
+    bool any = false;
+    for (int T = ts; T <= te; ++T) {
+      const int64_t r0 = T == ts ? rs : 0, r1 = T == te ? re : pl.N;
+      if (r0 >= r1) continue;
+      if (any) __syncthreads();  // the previous segment's slab reads are done
+      tile_body<FA, FB, JT, BW>(X, y, c, b, pl, T, r0, r1,
+                                ws + int64_t(pl.sbase[T] + cta - pl.first[T]) * kPartial, slab, bad_x);
+      if (pl.prof && threadIdx.x == 0 && !any) pl.prof[5 * cta] = T;
+      any = true;
+    }
+  } else {
+    int T = 0;
+    while (T + 1 < pl.ntiles && cta >= pl.first[T + 1]) ++T;
+    const int j = cta - pl.first[T], cnt = pl.cnt[T];
+    const int64_t per = round_up(ceil_div(tmax<int64_t>(pl.N, 1), cnt), 4);
+    const int64_t r0 = tmin<int64_t>(pl.N, int64_t(j) * per), r1 = tmin<int64_t>(pl.N, r0 + per);
+    tile_body<FA, FB, JT, BW>(X, y, c, b, pl, T, r0, r1, ws + int64_t(cta) * kPartial, slab, bad_x);
+    if (pl.prof && threadIdx.x == 0) pl.prof[5 * cta] = T;
+  }
   if (bad_x) raise_flag(flags, FAGP_FLAG_X_NONFINITE);
 }
 
@@ -490,7 +582,7 @@ __global__ void __launch_bounds__(256) reduce_kernel(const double* __restrict__ 
     idx = int64_t(kTF * kTF + pi / pl.ntiles) * 64;
   }
   idx += (ca % 8) * 8 + (cb % 8);
-  const double* src = ws + int64_t(pl.first[T]) * kPartial + idx;
+  const double* src = ws + int64_t(pl.sbase[T]) * kPartial + idx;
   const int n = pl.cnt[T];
   double s = 0.0;
   int i = 0;
@@ -516,7 +608,7 @@ bool eligible(int64_t N, int p, int M) {
 size_t workspace(int64_t N, int p, int M) {
   TPlan pl;
   if (!make_tplan(N, p, M, pl)) return 0;
-  return size_t(pl.grid) * kPartial * sizeof(double);
+  return size_t(pl.nslots) * kPartial * sizeof(double);
 }
 
 template <int FA, int FB, int JT, int BW>
@@ -554,7 +646,7 @@ int gram(const double* X, const double* y, double c, int64_t N, const fagp_basis
 #ifdef FAGP_TILED_PROF  // diagnostics build: per-CTA phase cycles printed to stderr
   FAGP_CUDA_TRY(cudaMalloc(&pl.prof, size_t(5) * pl.grid * sizeof(long long)));
 #endif
-  if (ws == nullptr || ws_bytes < size_t(pl.grid) * kPartial * sizeof(double)) return FAGP_EWORKSPACE;
+  if (ws == nullptr || ws_bytes < size_t(pl.nslots) * kPartial * sizeof(double)) return FAGP_EWORKSPACE;
   double* w = static_cast<double*>(ws);
   int rc;
   const int key = pl.q * 10 + (pl.p - pl.q);

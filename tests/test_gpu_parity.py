@@ -609,3 +609,25 @@ def test_predict_groups_bitwise(p, M, Ns, monkeypatch):
     for a, b in zip(out["1"], out["2"]):
         assert np.array_equal(a, b)
     assert np.all(np.isfinite(out["2"][0])) and np.all(out["2"][1] >= -1e-12)
+
+
+@pytest.mark.parametrize("p,M,N", [(4, 8, 70_001), (5, 6, 50_003), (5, 6, 4096)])
+def test_tiled_gram_span_deal(p, M, N, monkeypatch):
+    """The tiled Gram's two CTA deals -- whole CTAs per tile, and CTAs cutting the tile-major work
+    evenly (a CTA may finish one tile and start the next, two partial slots) -- agree with each
+    other and with the table path, each deterministic."""
+    from paper_2403_12797_b200.posterior import gram_x_packed
+
+    rng = np.random.default_rng(31 * p + N)
+    X = rng.uniform(-1, 1, (N, p))
+    y = np.cos(X).sum(1) + 0.05 * rng.standard_normal(N)
+    basis = F.Basis(F.ArdKernelParams.isotropic(p, 1.0, 1.0), M)
+    Xd, yd = dev.to_device(X), dev.to_device(y)
+    ref = dev.to_host(gram_packed(basis, _stage_tables(basis, Xd, None, None), yd, 0.3))
+    got = {}
+    for sp in ("0", "1"):
+        monkeypatch.setenv("FAGP_TILED_SPAN", sp)
+        got[sp] = dev.to_host(gram_x_packed(basis, Xd, yd, 0.3))
+        assert np.array_equal(got[sp], dev.to_host(gram_x_packed(basis, Xd, yd, 0.3)))
+        assert scaled_err(got[sp], ref) <= 1e-13, (sp, scaled_err(got[sp], ref))
+    assert scaled_err(got["1"], got["0"]) <= 1e-13
