@@ -48,9 +48,13 @@ CONFIGS = {
 METRIC = "posterior mean+var samples/s (N=1e6, p=3, M=10); % FP64 tensor peak"
 NOISE_VAR = 0.0025
 FP64_PEAK_FILE = ROOT / "profiles" / "fp64_peak_r01.json"
-NCU_SUMMARY_FILES = (ROOT / "profiles" / "ncu_summary_r06n.json", ROOT / "profiles" / "ncu_summary_r05.json",
-                     ROOT / "profiles" / "ncu_summary_r04s.json",
-                     ROOT / "profiles" / "ncu_summary_r04s_c4tiled.json")
+# committed ncu --set full summaries and the config each was captured on (traffic is per launch of
+# that config's kernel, so it is only reported for the same config)
+NCU_SUMMARY_FILES = ((ROOT / "profiles" / "ncu_summary_r06n.json", "c3"), (ROOT / "profiles" / "ncu_summary_r05.json", "c3"),
+                     (ROOT / "profiles" / "ncu_summary_r04s.json", "c3"),
+                     (ROOT / "profiles" / "ncu_summary_r06_c5tiled.json", "c5"),
+                     (ROOT / "profiles" / "ncu_summary_r06_c4tiled.json", "c4"),
+                     (ROOT / "profiles" / "ncu_summary_r04s_c4tiled.json", "c4"))
 
 
 def log(*a):
@@ -180,10 +184,12 @@ def fp64_peak():
         return 37.0, "fallback: 148 SM x 1.965 GHz x 128 FP64 flop/clk (datasheet ~37 TF)"
 
 
-def ncu_traffic(kernel):
+def ncu_traffic(kernel, cfg):
     """DRAM bytes per launch (read + write) of the kernel whose name starts with `kernel`,
-    from the committed ncu --set full summary (None when it was not captured)."""
-    for f in NCU_SUMMARY_FILES:
+    from the committed ncu --set full summary of config `cfg` (None when it was not captured)."""
+    for f, fcfg in NCU_SUMMARY_FILES:
+        if fcfg != cfg:
+            continue
         try:
             d = json.loads(f.read_text())
             for name, ent in d["kernels"].items():
@@ -453,12 +459,14 @@ def main():
         dom, dflops, dms = "fagp_gram_x (eigenfunctions on chip + modal DMMA Gram + t, partial sum)" if pair else \
             "fagp_gram (fused SYRK + reduce)", gram_flops, g_ms
         traffic = ncu_traffic({1: "fused_gram_split_kernel" if p == 3 and M == 10 else "fused_gram_kernel",
-                               2: "tiled_gram_kernel"}.get(routes[0], "modal_gram_kernel") if pair else "gram_kernel_fast")
+                               2: "tiled_gram_kernel"}.get(routes[0], "modal_gram_kernel") if pair else "gram_kernel_fast",
+                              args.config)
     else:
         dom, dflops, dms = "fagp_predict_x (eigenfunctions on chip + modal DMMA variance + mean)" if pair else \
             "fagp_predict (fused triangular GEMM)", pred_flops, p_ms
         traffic = ncu_traffic({1: "fused_predict_split_kernel" if p == 3 and 9 <= M <= 12 else "fused_predict_kernel",
-                               2: "tiled_predict_kernel"}.get(routes[1], "modal_var_kernel") if pair else "predict_kernel_fast")
+                               2: "tiled_predict_kernel"}.get(routes[1], "modal_var_kernel") if pair else "predict_kernel_fast",
+                              args.config)
     achieved = dflops / (dms / 1e3) / 1e12
     roofline = {"bound": "tensor", "kernel": dom, "achieved": round(achieved, 3), "peak": peak, "unit": "TFLOP/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,

@@ -14,19 +14,24 @@ tag = sys.argv[1]
 out_path = sys.argv[2] if len(sys.argv) > 2 else f"profiles/ncu_summary_{tag}.json"
 
 # ---- launch list (cold-cache, serialised: use the SHARE of the step, not absolute times)
-rows = list(csv.reader(open(f"gpurun_out/{tag}_launches.csv")))
-hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
-h = rows[hi]
-ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
 agg = defaultdict(list)
-for r in rows[hi + 1:]:
-    if len(r) > vi:
-        v = float(r[vi].replace(",", ""))
-        unit = r[ui]
-        us = v / 1e3 if unit in ("ns", "nsecond") else v * 1e3 if unit in ("ms", "msecond") else v
-        name = r[ki].split("(")[0].replace("void ", "")
-        agg[name].append(us)
-total = sum(sum(v) for v in agg.values())
+try:  # the launch list is optional (a full capture of selected kernels alone has none)
+    rows = list(csv.reader(open(f"gpurun_out/{tag}_launches.csv")))
+except OSError:
+    rows = []
+hi = [i for i, r in enumerate(rows) if "Kernel Name" in r]
+if hi:
+    hi = hi[0]
+    h = rows[hi]
+    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    for r in rows[hi + 1:]:
+        if len(r) > vi:
+            v = float(r[vi].replace(",", ""))
+            unit = r[ui]
+            us = v / 1e3 if unit in ("ns", "nsecond") else v * 1e3 if unit in ("ms", "msecond") else v
+            name = r[ki].split("(")[0].replace("void ", "")
+            agg[name].append(us)
+total = sum(sum(v) for v in agg.values()) or 1.0
 launches = [{"kernel": k, "launches": len(v), "total_us": round(sum(v), 1), "avg_us": round(sum(v) / len(v), 1),
              "share": round(sum(v) / total, 4)} for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1]))]
 
@@ -80,7 +85,8 @@ if rr:
                     pass
         tot = sum(s for s, _ in stalls) or 1.0
         ent["top_stalls_pct"] = {k: round(100 * s / tot, 1) for s, k in sorted(stalls, reverse=True)[:5]}
-        if "dram_read_MB" in ent and "dram_write_MB" in ent:
+        if "dram_read_MB" in ent and "dram_write_MB" in ent and ent["dram_read_MB"] == ent["dram_read_MB"] \
+                and ent["dram_write_MB"] == ent["dram_write_MB"]:  # (not NaN)
             ent["dram_bytes_per_launch"] = int(round((ent["dram_read_MB"] + ent["dram_write_MB"]) * 1e6))
         kernels.setdefault(name, ent)
 
