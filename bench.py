@@ -50,7 +50,7 @@ NOISE_VAR = 0.0025
 FP64_PEAK_FILE = ROOT / "profiles" / "fp64_peak_r01.json"
 # committed ncu --set full summaries and the config each was captured on (traffic is per launch of
 # that config's kernel, so it is only reported for the same config)
-NCU_SUMMARY_FILES = ((ROOT / "profiles" / "ncu_summary_r06n.json", "c3"), (ROOT / "profiles" / "ncu_summary_r05.json", "c3"),
+NCU_SUMMARY_FILES = ((ROOT / "profiles" / "ncu_summary_r06y.json", "c3"), (ROOT / "profiles" / "ncu_summary_r06n.json", "c3"), (ROOT / "profiles" / "ncu_summary_r05.json", "c3"),
                      (ROOT / "profiles" / "ncu_summary_r04s.json", "c3"),
                      (ROOT / "profiles" / "ncu_summary_r06_c5tiled.json", "c5"),
                      (ROOT / "profiles" / "ncu_summary_r06_c4tiled.json", "c4"),
