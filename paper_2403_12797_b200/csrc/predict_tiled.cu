@@ -24,6 +24,7 @@
 #include <type_traits>
 #include <cstdio>
 #include <cstring>
+#include <vector>
 
 #include "common.cuh"
 #include "eigfun.cuh"
@@ -61,6 +62,7 @@ struct PPlan {
   int pN;
   int64_t NRL, NP, KP;  // L^(p - pN) (the kK radix span), padded strides
   HermCoef hc;
+  long long* prof;  // diagnostics build (-DFAGP_PTILED_PROF): per CTA [tile, cycles]
 };
 
 static int64_t ipow(int64_t b, int e) {
@@ -115,10 +117,16 @@ static bool make_pplan(int64_t Ns, int p, int M, PPlan& pl) {
   pl.nvar = pl.ntiles;
   if (!add(1, pl.MA, pl.MB)) return false;
   // per-row cost of a tile: its k-steps on the busiest sub-partition + production / epilogue
+  // calibrated with -DFAGP_PTILED_PROF (per-CTA cycles) at C4 and C5: a k-step costs in proportion
+  // to the busiest column group's n-fragments and to the share of column groups with any work (the
+  // others' warps idle), plus a per-row production / epilogue term worth ~9 full k-steps (the old
+  // model's 120 under-weighted it: C5's two mean tiles got 5 CTAs each and ran 9% past the
+  // variance tiles)
   auto cost = [&](const Tile& t) {
     const int ks = int(ceil_div(t.nka, 4));
-    const int cols = tmin(kCF, t.nb);  // n-fragments of the busiest column group
-    return double(ks) * (8.0 * cols + 6.0) + 120.0;
+    const int cols = tmin(kCF, t.nb);                       // n-fragments of the busiest column group
+    const int groups = tmin(4, int(ceil_div(t.nb, kCF)));   // column groups with work
+    return double(ks) * (8.0 * cols + 6.0) * groups / 4.0 + 355.0;
   };
   const int G = tmax(num_sms(), pl.ntiles);
   for (int t = 0; t < pl.ntiles; ++t) pl.cnt[t] = 1;
@@ -213,6 +221,9 @@ tiled_predict_kernel(const double* __restrict__ Xs, BasisView b, const __grid_co
   };
   const int p = pl.p, M = pl.M, L = pl.L;
   const int cta = int(blockIdx.x);
+#ifdef FAGP_PTILED_PROF
+  const long long t_start = clock64();
+#endif
   int T = 0;
   while (T + 1 < pl.ntiles && cta >= pl.first[T + 1]) ++T;
   const Tile tl = pl.tiles[T];
@@ -363,6 +374,12 @@ tiled_predict_kernel(const double* __restrict__ Xs, BasisView b, const __grid_co
   }
   if constexpr (G == 2)
     if (!staggered) asm volatile("bar.arrive 3, %0;" ::"r"(kNT) : "memory");  // group 0 had no block
+#ifdef FAGP_PTILED_PROF
+  if (pl.prof && tid == 0) {
+    pl.prof[2 * cta] = T;
+    pl.prof[2 * cta + 1] = clock64() - t_start;
+  }
+#endif
   if (bad_x) raise_flag(flags, FAGP_FLAG_X_NONFINITE);
 }
 
@@ -409,7 +426,22 @@ static int launch_bw(const double* Xs, const fagp_basis* b, const PPlan& pl, con
   const bool g2 = FB <= 2 && !(sg && sg[0] == '1');
   auto kern = g2 ? tiled_predict_kernel<FA, FB, BW, 2> : tiled_predict_kernel<FA, FB, BW, 1>;
   FAGP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+#ifdef FAGP_PTILED_PROF
+  PPlan pp = pl;
+  FAGP_CUDA_TRY(cudaMalloc(&pp.prof, size_t(2) * pl.grid * sizeof(long long)));
+  kern<<<pl.grid, kNT, smem, s>>>(Xs, view(b), pp, op, part, flags);
+  {
+    std::vector<long long> h(size_t(2) * pl.grid);
+    FAGP_CUDA_TRY(cudaStreamSynchronize(s));
+    FAGP_CUDA_TRY(cudaMemcpy(h.data(), pp.prof, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+    for (int c = 0; c < pl.grid; ++c)
+      fprintf(stderr, "ptiled cta %3d tile %2lld kind %d nka %3d nb %2d cnt %3d cycles %lld\n", c, h[2 * c],
+              pl.tiles[h[2 * c]].kind, pl.tiles[h[2 * c]].nka, pl.tiles[h[2 * c]].nb, pl.cnt[h[2 * c]], h[2 * c + 1]);
+    cudaFree(pp.prof);
+  }
+#else
   kern<<<pl.grid, kNT, smem, s>>>(Xs, view(b), pl, op, part, flags);
+#endif
   FAGP_LAUNCH_CHECK();
   return FAGP_OK;
 }
